@@ -1,0 +1,216 @@
+/*
+ * sr_block.h — C ABI of the B200-native block-layer stochastic-reconfiguration step
+ * (arXiv 2510.08430, "block-layer QGT"; §2, Eqs. 1-3).
+ *
+ * One step, five stages (BASELINE.json north_star):
+ *   (1) sr_jacobian      O_ki = d ln psi(x_k) / d theta_i, grouped by layer      PAPER.md Eq. 2
+ *   (2) sr_local_energy  E_loc(x_k) = sum_x' <x_k|H|x'> psi(x')/psi(x_k)          PAPER.md Eq. 1
+ *   (3) sr_center_force  Obar = O - <O>, F = Obar^H (E_loc - <E_loc>) / N_s      PAPER.md Eq. 2, §2
+ *   (4) sr_block_qgt     S_b = Obar_b^H Obar_b / N_s for every layer block b     PAPER.md Eq. 3
+ *   (5) sr_block_solve   (S_b + lambda I) dtheta_b = -F_b, blocks independent    PAPER.md §2
+ * plus the comparison paths sr_full_qgt_solve (§2 "S . dtheta = -F") and
+ * sr_ntk_solve (§1, sample-space NTK / MinSR), and sr_step / sr_step_host
+ * which run stages (1)-(5) back to back.
+ *
+ * Conventions
+ * -----------
+ * - complex128 values are two interleaved doubles (re, im): the layout of C99
+ *   `double _Complex`, `std::complex<double>`, numpy complex128 and torch.complex128.
+ *   Pointers typed `double*` below that say "complex" point at 2*count doubles.
+ * - Every pointer is a DEVICE pointer unless the argument says (host).  Device
+ *   buffers are owned by the caller; the library never allocates or frees device
+ *   memory, and keeps no state between calls.  Scratch comes in through a
+ *   `workspace` pointer whose size the matching *_workspace_bytes() query returns
+ *   (256-byte aligned base required).
+ * - `stream` is a cudaStream_t (NULL = legacy default stream).  All device work is
+ *   enqueued on it; calls return without synchronising, except sr_step_host.
+ * - Network: complex MLP with widths[0..n_layers] (widths[0] = N sites),
+ *   z_l = W_l h_{l-1} + b_l, h_l = lncosh(z_l) (principal branch), ln psi = sum_j h_L[j].
+ *   theta is complex [n_p]: for each layer l in order, W_l row-major
+ *   [widths[l+1]][widths[l]] then b_l [widths[l+1]].  Layer block b = layer b, columns
+ *   [off_b, off_b + n_b) with n_b = widths[b+1]*(widths[b]+1).  n_layers <= 16 and
+ *   every width <= 256.
+ * - Spins: int8 [n_samples][N], entries +1 / -1.
+ * - Hamiltonian (Pauli units, reading R3): H = sum_b J_b sigma_i.sigma_j over
+ *   the bond list; bonds_ij int32 [n_bonds][2], bond_j double [n_bonds].
+ * - Sample weights: `weights` double [n_samples] summing to 1, or NULL for uniform
+ *   1/n_samples.  Stage (3) stores A_k = sqrt(w_k) (O_k - <O>) in place of O and
+ *   e_k = sqrt(w_k)(E_loc,k - E), so S = A^H A, F = A^H e, T_NTK = A A^H.
+ *
+ * Errors: functions return SR_OK (0) or a negative sr_status; sr_last_error()
+ * returns a thread-local message for the last failure.  Invalid sizes/pointers are
+ * rejected before any work is enqueued.  Kernel faults surface as SR_ERR_CUDA
+ * (possibly from a later call, as with any asynchronous CUDA API).  A
+ * non-positive Cholesky pivot is reported through the optional device `info` word
+ * of the solvers (0 = success, k>0 = first failing pivot row + 1 of the first
+ * failing block) — it cannot happen for lambda > 0 and a Hermitian PSD S.
+ */
+#ifndef SR_BLOCK_H
+#define SR_BLOCK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SR_API __attribute__((visibility("default")))
+#else
+#define SR_API
+#endif
+
+typedef int sr_status;
+#define SR_OK 0
+#define SR_ERR_INVALID (-1)  /* bad size, null pointer, unsupported width */
+#define SR_ERR_CUDA (-2)     /* a CUDA runtime call or kernel launch failed */
+#define SR_ERR_WORKSPACE (-3) /* workspace smaller than the query result */
+
+/* Library version (major*10000 + minor*100 + patch). */
+SR_API int sr_version(void);
+/* Message for the most recent failure on this host thread ("" if none). */
+SR_API const char* sr_last_error(void);
+/* Number of kernel launches issued by this host thread since the last reset
+ * (instrumentation for bench.py's gpu_launches; reset with sr_reset_launch_count). */
+SR_API int64_t sr_launch_count(void);
+SR_API void sr_reset_launch_count(void);
+
+/* ---------------------------------------------------------------- stage (1) ---
+ * sr_jacobian — PAPER.md §2 Eq. 2 "O_i(x) = d_{theta_i} log psi_theta(x)".
+ *   theta    complex [n_p]                       network parameters (layout above)
+ *   spins    int8 [n_samples][widths[0]]
+ *   log_psi  complex [n_samples]   (out)         ln psi(x_k)
+ *   O        complex [n_samples][ldo] (out)      row k = O(x_k); columns [0, n_p) written
+ *   ldo      >= n_p (elements)
+ * Holomorphic derivative; block l columns: W_l (j*fan_in+i) then b_l.  */
+SR_API size_t sr_jacobian_workspace_bytes(int n_layers, const int32_t* widths /*host*/,
+                                          int64_t n_samples);
+SR_API sr_status sr_jacobian(int n_layers, const int32_t* widths /*host*/, const double* theta,
+                             const int8_t* spins, int64_t n_samples, double* log_psi, double* O,
+                             int64_t ldo, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------- stage (2) ---
+ * sr_local_energy — PAPER.md Eq. 1 local energy with the same network evaluated on
+ * every connected configuration x' (x with an anti-aligned bonded pair swapped):
+ *   E_loc(x) = sum_b J_b [ s_i s_j + (1 - s_i s_j) psi(x^{ij})/psi(x) ].
+ *   log_psi  complex [n_samples] (in)  ln psi of the samples (from sr_jacobian)
+ *   e_loc    complex [n_samples] (out) */
+SR_API size_t sr_local_energy_workspace_bytes(int n_layers, const int32_t* widths /*host*/,
+                                              int64_t n_samples, int64_t n_bonds);
+SR_API sr_status sr_local_energy(int n_layers, const int32_t* widths /*host*/,
+                                 const double* theta, int64_t n_bonds, const int32_t* bonds_ij,
+                                 const double* bond_j, const int8_t* spins, int64_t n_samples,
+                                 const double* log_psi, double* e_loc, void* workspace,
+                                 size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------- stage (3) ---
+ * sr_center_force — PAPER.md Eq. 2 centring (Delta O_i = O_i - <O_i>) and the force
+ *   F_i = sum_k w_k conj(Obar_ki) (E_loc,k - E),  E = sum_k w_k E_loc,k.
+ *   O        complex [n_samples][ldo] (in/out)  O on entry, A = sqrt(w) Obar on exit
+ *   weights  double [n_samples] or NULL (uniform)
+ *   e_loc    complex [n_samples] (in)
+ *   energy   complex [1] (out)            E
+ *   e_tilde  complex [n_samples] (out)    e_k = sqrt(w_k) (E_loc,k - E)
+ *   F        complex [n_p] (out) */
+SR_API size_t sr_center_force_workspace_bytes(int64_t n_samples, int64_t n_p);
+SR_API sr_status sr_center_force(int64_t n_samples, int64_t n_p, double* O, int64_t ldo,
+                                 const double* weights, const double* e_loc, double* energy,
+                                 double* e_tilde, double* F, void* workspace,
+                                 size_t workspace_bytes, void* stream);
+
+/* Sample-sharded form of stage (3) (one call per rank; BASELINE.json north_star:
+ * "samples shard naturally").  With n_total samples over all ranks and uniform
+ * weights 1/n_total (weights == NULL) or the rank's slice of global weights:
+ *   sr_column_moments       wsum_O[c] = sum_{k local} w_k O[k][c],  wsum_E = sum_{k local} w_k E_k
+ *   (all-reduce both over ranks -> <O> and E), then
+ *   sr_center_force_global  A_k = sqrt(w_k)(O_k - mean_O) in place, e_tilde_k = sqrt(w_k)(E_k - energy),
+ *                           F_partial = sum_{k local} conj(A_k) e_k   (all-reduce -> F).
+ * Workspace: sr_center_force_workspace_bytes(n_local, n_p). */
+SR_API size_t sr_column_moments_workspace_bytes(int64_t n_local, int64_t n_p);
+SR_API sr_status sr_column_moments(int64_t n_local, int64_t n_total, int64_t n_p, const double* O, int64_t ldo,
+                                   const double* weights, const double* e_loc, double* wsum_O, double* wsum_E,
+                                   void* workspace, size_t workspace_bytes, void* stream);
+SR_API sr_status sr_center_force_global(int64_t n_local, int64_t n_total, int64_t n_p, double* O, int64_t ldo,
+                                        const double* weights, const double* e_loc, const double* mean_O,
+                                        const double* energy, double* e_tilde, double* F_partial,
+                                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------- stage (4) ---
+ * sr_block_qgt — PAPER.md Eq. 3, S_l = <O_l^dag O_l> - <O_l^dag><O_l>, computed per
+ * layer block from the centred, weighted Jacobian A (stage 3 output): S_b = A_b^H A_b.
+ *   block_offsets (host) int64 [n_blocks+1], column ranges of the blocks in A
+ *   S        complex, blocks packed back to back: block b is n_b x n_b row-major at
+ *            element offset sum_{c<b} n_c^2; both triangles written (Hermitian),
+ *            diagonal imaginary parts exactly 0. */
+SR_API size_t sr_block_qgt_workspace_bytes(int n_blocks, const int64_t* block_offsets /*host*/);
+SR_API sr_status sr_block_qgt(int64_t n_samples, int n_blocks,
+                              const int64_t* block_offsets /*host*/, const double* A, int64_t lda,
+                              double* S, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------- stage (5) ---
+ * sr_block_solve — PAPER.md §2: "Each block S_l is inverted independently, using a
+ * uniform diagonal shift lambda", (S_b + lambda I) dtheta_b = -F_b, by a blocked,
+ * batched Cholesky factorisation (all blocks advance together).
+ *   S       packed blocks as written by sr_block_qgt (read only; lower triangle used)
+ *   F       complex [n_p];   dtheta complex [n_p] (out);   info int32 [1] (out) or NULL */
+SR_API size_t sr_block_solve_workspace_bytes(int n_blocks, const int64_t* block_offsets /*host*/);
+SR_API sr_status sr_block_solve(int n_blocks, const int64_t* block_offsets /*host*/,
+                                const double* S, const double* F, double lambda, double* dtheta,
+                                int32_t* info, void* workspace, size_t workspace_bytes,
+                                void* stream);
+
+/* ------------------------------------------------------- comparison paths ---
+ * sr_full_qgt_solve — PAPER.md §2 "S . delta theta = -F" with the full n_p x n_p QGT:
+ *   S = A^H A formed in the workspace, (S + lambda I) dtheta = -F by Cholesky.
+ *   S_out complex [n_p][n_p] (out, optional, may be NULL): copy of S (both triangles). */
+SR_API size_t sr_full_qgt_solve_workspace_bytes(int64_t n_samples, int64_t n_p);
+SR_API sr_status sr_full_qgt_solve(int64_t n_samples, int64_t n_p, const double* A, int64_t lda,
+                                   const double* F, double lambda, double* dtheta,
+                                   double* S_out, int32_t* info, void* workspace,
+                                   size_t workspace_bytes, void* stream);
+
+/* sr_ntk_solve — PAPER.md §1 sample-space reformulation ("inverting the neural
+ * tangent kernel (NTK)-like matrix whose size depends on the number of Monte Carlo
+ * samples"): T = A A^H (n_samples x n_samples), (T + lambda I) y = e,
+ * dtheta = -A^H y.  Equal to sr_full_qgt_solve by the push-through identity.
+ *   e_tilde complex [n_samples] (stage 3 output);  T_out optional copy of T. */
+SR_API size_t sr_ntk_solve_workspace_bytes(int64_t n_samples, int64_t n_p);
+SR_API sr_status sr_ntk_solve(int64_t n_samples, int64_t n_p, const double* A, int64_t lda,
+                              const double* e_tilde, double lambda, double* dtheta,
+                              double* T_out, int32_t* info, void* workspace,
+                              size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------- full step ---
+ * sr_step — stages (1)-(5) back to back on device buffers (uniform weights):
+ *   theta complex [n_p], spins int8 [n_samples][N], bonds as in stage (2);
+ *   dtheta complex [n_p] (out), energy complex [1] (out).
+ * The workspace holds O/A, E_loc, S blocks and the factor storage; the S blocks sit
+ * at offset sr_step_s_offset() of the workspace (for inspection). */
+SR_API size_t sr_step_workspace_bytes(int n_layers, const int32_t* widths /*host*/,
+                                      int64_t n_samples, int64_t n_bonds);
+SR_API size_t sr_step_s_offset(int n_layers, const int32_t* widths /*host*/, int64_t n_samples,
+                               int64_t n_bonds);
+SR_API sr_status sr_step(int n_layers, const int32_t* widths /*host*/, const double* theta,
+                         const int8_t* spins, int64_t n_samples, int64_t n_bonds,
+                         const int32_t* bonds_ij, const double* bond_j, double lambda,
+                         double* dtheta, double* energy, void* workspace, size_t workspace_bytes,
+                         void* stream);
+
+/* sr_step_host — sr_step with HOST inputs and outputs (theta_h, spins_h, bonds_ij_h,
+ * bond_j_h in; dtheta_h, energy_h out).  Copies in, runs the step, copies out, and
+ * synchronises `stream` before returning.  Host buffers should be pinned for
+ * asynchronous copies.  Device workspace as for sr_step plus
+ * sr_step_host_extra_bytes() for the staged inputs/outputs. */
+SR_API size_t sr_step_host_extra_bytes(int n_layers, const int32_t* widths /*host*/,
+                                       int64_t n_samples, int64_t n_bonds);
+SR_API sr_status sr_step_host(int n_layers, const int32_t* widths /*host*/,
+                              const double* theta_h, const int8_t* spins_h, int64_t n_samples,
+                              int64_t n_bonds, const int32_t* bonds_ij_h, const double* bond_j_h,
+                              double lambda, double* dtheta_h, double* energy_h,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SR_BLOCK_H */

@@ -1,0 +1,279 @@
+"""ctypes binding of libsrblock.so (include/sr_block.h): argument marshalling only.
+
+Every function here has the name of the C entry point it wraps, takes torch tensors
+(device memory owned by the caller) and plain Python numbers, checks dtype/device/
+shape, allocates the workspace the matching *_workspace_bytes() query asks for when
+none is given, and calls the C function on the current CUDA stream.  No arithmetic of
+the method happens in Python; there is no CPU fallback: if the library cannot be
+loaded, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from . import build as _build
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsrblock.so")
+
+_vp, _i64, _i32, _sz, _dbl = C.c_void_p, C.c_int64, C.c_int, C.c_size_t, C.c_double
+_I32P = C.POINTER(C.c_int32)
+_I64P = C.POINTER(C.c_int64)
+
+# name -> (restype, argtypes); mirrors include/sr_block.h
+SIGNATURES = {
+    "sr_version": (_i32, []),
+    "sr_last_error": (C.c_char_p, []),
+    "sr_launch_count": (_i64, []),
+    "sr_reset_launch_count": (None, []),
+    "sr_jacobian_workspace_bytes": (_sz, [_i32, _I32P, _i64]),
+    "sr_jacobian": (_i32, [_i32, _I32P, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _sz, _vp]),
+    "sr_local_energy_workspace_bytes": (_sz, [_i32, _I32P, _i64, _i64]),
+    "sr_local_energy": (_i32, [_i32, _I32P, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "sr_center_force_workspace_bytes": (_sz, [_i64, _i64]),
+    "sr_center_force": (_i32, [_i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "sr_column_moments_workspace_bytes": (_sz, [_i64, _i64]),
+    "sr_column_moments": (_i32, [_i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "sr_center_force_global": (_i32, [_i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
+                                      _vp]),
+    "sr_block_qgt_workspace_bytes": (_sz, [_i32, _I64P]),
+    "sr_block_qgt": (_i32, [_i64, _i32, _I64P, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "sr_block_solve_workspace_bytes": (_sz, [_i32, _I64P]),
+    "sr_block_solve": (_i32, [_i32, _I64P, _vp, _vp, _dbl, _vp, _vp, _vp, _sz, _vp]),
+    "sr_full_qgt_solve_workspace_bytes": (_sz, [_i64, _i64]),
+    "sr_full_qgt_solve": (_i32, [_i64, _i64, _vp, _i64, _vp, _dbl, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "sr_ntk_solve_workspace_bytes": (_sz, [_i64, _i64]),
+    "sr_ntk_solve": (_i32, [_i64, _i64, _vp, _i64, _vp, _dbl, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "sr_step_workspace_bytes": (_sz, [_i32, _I32P, _i64, _i64]),
+    "sr_step_s_offset": (_sz, [_i32, _I32P, _i64, _i64]),
+    "sr_step": (_i32, [_i32, _I32P, _vp, _vp, _i64, _i64, _vp, _vp, _dbl, _vp, _vp, _vp, _sz, _vp]),
+    "sr_step_host_extra_bytes": (_sz, [_i32, _I32P, _i64, _i64]),
+    "sr_step_host": (_i32, [_i32, _I32P, _vp, _vp, _i64, _i64, _vp, _vp, _dbl, _vp, _vp, _vp, _sz, _vp]),
+}
+
+
+class SRError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load(build_if_missing: bool = True) -> C.CDLL:
+    """Load libsrblock.so (building it in-tree with nvcc if it is missing or stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_missing and not _build.up_to_date():
+        _build.build()
+    if not os.path.exists(LIB_PATH):
+        raise SRError(f"{LIB_PATH} is missing; run python -m paper_2510_08430_b200.build")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(status: int, name: str):
+    if status != 0:
+        msg = load().sr_last_error().decode()
+        raise SRError(f"{name} failed with status {status}: {msg}")
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _dev(t, dtype, name):
+    if t is None:
+        return
+    if not t.is_cuda:
+        raise SRError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise SRError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise SRError(f"{name} must be contiguous")
+
+
+def _widths(widths):
+    arr = (C.c_int32 * len(widths))(*[int(w) for w in widths])
+    return len(widths) - 1, arr
+
+
+def _offsets(offs):
+    return (C.c_int64 * len(offs))(*[int(o) for o in offs])
+
+
+def _stream(device=None):
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _workspace(nbytes, device, workspace):
+    if workspace is not None:
+        if workspace.numel() * workspace.element_size() < nbytes:
+            raise SRError("workspace too small")
+        return workspace
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def _ws_args(ws):
+    return C.c_void_p(ws.data_ptr()), C.c_size_t(ws.numel() * ws.element_size())
+
+
+def n_params(widths):
+    return sum(int(widths[l + 1]) * (int(widths[l]) + 1) for l in range(len(widths) - 1))
+
+
+def block_offsets(widths):
+    offs = [0]
+    for l in range(len(widths) - 1):
+        offs.append(offs[-1] + int(widths[l + 1]) * (int(widths[l]) + 1))
+    return offs
+
+
+# ------------------------------------------------------------------ stage (1)
+def sr_jacobian(widths, theta, spins, log_psi, O, workspace=None):
+    lib = load()
+    L, w = _widths(widths)
+    ns = spins.shape[0]
+    _dev(theta, torch.complex128, "theta")
+    _dev(spins, torch.int8, "spins")
+    _dev(log_psi, torch.complex128, "log_psi")
+    _dev(O, torch.complex128, "O")
+    ws = _workspace(lib.sr_jacobian_workspace_bytes(L, w, ns), spins.device, workspace)
+    _check(lib.sr_jacobian(L, w, _ptr(theta), _ptr(spins), ns, _ptr(log_psi), _ptr(O), O.shape[1],
+                           *_ws_args(ws), _stream(spins.device)), "sr_jacobian")
+
+
+# ------------------------------------------------------------------ stage (2)
+def sr_local_energy(widths, theta, bonds_ij, bond_j, spins, log_psi, e_loc, workspace=None):
+    lib = load()
+    L, w = _widths(widths)
+    ns, nb = spins.shape[0], bonds_ij.shape[0]
+    _dev(bonds_ij, torch.int32, "bonds_ij")
+    _dev(bond_j, torch.float64, "bond_j")
+    _dev(e_loc, torch.complex128, "e_loc")
+    ws = _workspace(lib.sr_local_energy_workspace_bytes(L, w, ns, nb), spins.device, workspace)
+    _check(lib.sr_local_energy(L, w, _ptr(theta), nb, _ptr(bonds_ij), _ptr(bond_j), _ptr(spins), ns,
+                               _ptr(log_psi), _ptr(e_loc), *_ws_args(ws), _stream(spins.device)),
+           "sr_local_energy")
+
+
+# ------------------------------------------------------------------ stage (3)
+def sr_center_force(O, e_loc, energy, e_tilde, F, weights=None, workspace=None):
+    lib = load()
+    ns, npar = O.shape[0], F.shape[0]
+    _dev(O, torch.complex128, "O")
+    _dev(weights, torch.float64, "weights")
+    ws = _workspace(lib.sr_center_force_workspace_bytes(ns, npar), O.device, workspace)
+    _check(lib.sr_center_force(ns, npar, _ptr(O), O.shape[1], _ptr(weights), _ptr(e_loc), _ptr(energy),
+                               _ptr(e_tilde), _ptr(F), *_ws_args(ws), _stream(O.device)), "sr_center_force")
+
+
+def sr_column_moments(O, e_loc, n_total, wsum_O, wsum_E, weights=None, workspace=None):
+    lib = load()
+    ns, npar = O.shape[0], wsum_O.shape[0]
+    ws = _workspace(lib.sr_column_moments_workspace_bytes(ns, npar), O.device, workspace)
+    _check(lib.sr_column_moments(ns, n_total, npar, _ptr(O), O.shape[1], _ptr(weights), _ptr(e_loc),
+                                 _ptr(wsum_O), _ptr(wsum_E), *_ws_args(ws), _stream(O.device)),
+           "sr_column_moments")
+
+
+def sr_center_force_global(O, e_loc, n_total, mean_O, energy, e_tilde, F_partial, weights=None,
+                           workspace=None):
+    lib = load()
+    ns, npar = O.shape[0], mean_O.shape[0]
+    ws = _workspace(lib.sr_center_force_workspace_bytes(ns, npar), O.device, workspace)
+    _check(lib.sr_center_force_global(ns, n_total, npar, _ptr(O), O.shape[1], _ptr(weights), _ptr(e_loc),
+                                      _ptr(mean_O), _ptr(energy), _ptr(e_tilde), _ptr(F_partial),
+                                      *_ws_args(ws), _stream(O.device)), "sr_center_force_global")
+
+
+# ------------------------------------------------------------------ stage (4)
+def sr_block_qgt(A, offsets, S):
+    lib = load()
+    _dev(A, torch.complex128, "A")
+    _dev(S, torch.complex128, "S")
+    nblk = len(offsets) - 1
+    need = sum((offsets[b + 1] - offsets[b]) ** 2 for b in range(nblk))
+    if S.numel() < need:
+        raise SRError("S too small for the packed blocks")
+    _check(lib.sr_block_qgt(A.shape[0], nblk, _offsets(offsets), _ptr(A), A.shape[1], _ptr(S), None, 0,
+                            _stream(A.device)), "sr_block_qgt")
+
+
+# ------------------------------------------------------------------ stage (5)
+def sr_block_solve(offsets, S, F, lam, dtheta, info=None, workspace=None):
+    lib = load()
+    nblk = len(offsets) - 1
+    off = _offsets(offsets)
+    ws = _workspace(lib.sr_block_solve_workspace_bytes(nblk, off), S.device, workspace)
+    _check(lib.sr_block_solve(nblk, off, _ptr(S), _ptr(F), float(lam), _ptr(dtheta), _ptr(info),
+                              *_ws_args(ws), _stream(S.device)), "sr_block_solve")
+
+
+def sr_full_qgt_solve(A, F, lam, dtheta, S_out=None, info=None, workspace=None):
+    lib = load()
+    ns, npar = A.shape[0], F.shape[0]
+    ws = _workspace(lib.sr_full_qgt_solve_workspace_bytes(ns, npar), A.device, workspace)
+    _check(lib.sr_full_qgt_solve(ns, npar, _ptr(A), A.shape[1], _ptr(F), float(lam), _ptr(dtheta),
+                                 _ptr(S_out), _ptr(info), *_ws_args(ws), _stream(A.device)),
+           "sr_full_qgt_solve")
+
+
+def sr_ntk_solve(A, e_tilde, lam, dtheta, T_out=None, info=None, workspace=None):
+    lib = load()
+    ns, npar = A.shape[0], dtheta.shape[0]
+    ws = _workspace(lib.sr_ntk_solve_workspace_bytes(ns, npar), A.device, workspace)
+    _check(lib.sr_ntk_solve(ns, npar, _ptr(A), A.shape[1], _ptr(e_tilde), float(lam), _ptr(dtheta),
+                            _ptr(T_out), _ptr(info), *_ws_args(ws), _stream(A.device)), "sr_ntk_solve")
+
+
+# ------------------------------------------------------------------ full step
+def sr_step_workspace_bytes(widths, n_samples, n_bonds):
+    L, w = _widths(widths)
+    return int(load().sr_step_workspace_bytes(L, w, n_samples, n_bonds))
+
+
+def sr_step_s_offset(widths, n_samples, n_bonds):
+    L, w = _widths(widths)
+    return int(load().sr_step_s_offset(L, w, n_samples, n_bonds))
+
+
+def sr_step_host_extra_bytes(widths, n_samples, n_bonds):
+    L, w = _widths(widths)
+    return int(load().sr_step_host_extra_bytes(L, w, n_samples, n_bonds))
+
+
+def sr_step(widths, theta, spins, bonds_ij, bond_j, lam, dtheta, energy, workspace):
+    lib = load()
+    L, w = _widths(widths)
+    _check(lib.sr_step(L, w, _ptr(theta), _ptr(spins), spins.shape[0], bonds_ij.shape[0], _ptr(bonds_ij),
+                       _ptr(bond_j), float(lam), _ptr(dtheta), _ptr(energy), *_ws_args(workspace),
+                       _stream(workspace.device)), "sr_step")
+
+
+def sr_step_host(widths, theta_h, spins_h, bonds_ij_h, bond_j_h, lam, dtheta_h, energy_h, workspace):
+    """Host tensors in/out (pinned for async copies); synchronises the stream."""
+    lib = load()
+    L, w = _widths(widths)
+    for t, n in ((theta_h, "theta_h"), (spins_h, "spins_h"), (dtheta_h, "dtheta_h")):
+        if t.is_cuda or not t.is_contiguous():
+            raise SRError(f"{n} must be a contiguous host tensor")
+    _check(lib.sr_step_host(L, w, _ptr(theta_h), _ptr(spins_h), spins_h.shape[0], bonds_ij_h.shape[0],
+                            _ptr(bonds_ij_h), _ptr(bond_j_h), float(lam), _ptr(dtheta_h), _ptr(energy_h),
+                            *_ws_args(workspace), _stream(workspace.device)), "sr_step_host")
+
+
+def sr_launch_count():
+    return int(load().sr_launch_count())
+
+
+def sr_reset_launch_count():
+    load().sr_reset_launch_count()

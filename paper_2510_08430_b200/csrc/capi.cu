@@ -1,0 +1,451 @@
+// capi.cu — extern "C" entry points of libsrblock.so (declared in include/sr_block.h).
+// Argument checking, workspace carving and stage sequencing only; every arithmetic step
+// of the path runs in the kernels of mlp.cu, center.cu, gram.cuh and chol.cu.
+#include <algorithm>
+#include <vector>
+
+#include "chol.cuh"
+#include "gram.cuh"
+#include "net.cuh"
+
+namespace sr {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+void set_error(const std::string& m) { g_err = m; }
+void count_launch(int n) { g_launches += n; }
+
+sr_status jacobian_impl(const NetDesc&, const double*, const int8_t*, long long, double*, double*, long long,
+                        void*, size_t, cudaStream_t);
+size_t jacobian_ws(const NetDesc&, long long);
+size_t local_energy_ws(const NetDesc&, long long, long long);
+sr_status local_energy_impl(const NetDesc&, const double*, long long, const int32_t*, const double*,
+                            const int8_t*, long long, const double*, double*, void*, size_t, cudaStream_t);
+size_t center_force_ws(long long, long long);
+sr_status center_force_impl(long long, long long, double*, long long, const double*, const double*, double*,
+                            double*, double*, void*, size_t, cudaStream_t);
+size_t aHv_ws(long long, long long);
+sr_status column_moments_impl(long long, long long, long long, const double*, long long, const double*, const double*,
+                              double*, double*, void*, size_t, cudaStream_t);
+sr_status center_force_global_impl(long long, long long, long long, double*, long long, const double*,
+                                   const double*, const double*, const double*, double*, double*, void*, size_t,
+                                   cudaStream_t);
+sr_status aHv_impl(long long, long long, const double2*, long long, const double2*, double, double2*, void*,
+                   size_t, cudaStream_t);
+
+namespace {
+
+__global__ void copy_unpad(const double2* __restrict__ src, long long lds, double2* __restrict__ dst,
+                           long long ldd, long long rows, long long cols) {
+  const long long total = rows * cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / cols, c = e % cols;
+    dst[r * ldd + c] = src[r * lds + c];
+  }
+}
+
+sr_status copy_matrix(const double2* src, long long lds, double2* dst, long long ldd, long long rows,
+                      long long cols, cudaStream_t st) {
+  if (rows * cols == 0) return SR_OK;
+  const unsigned g = (unsigned)std::min<long long>((rows * cols + 255) / 256, 8 * kNumSMs);
+  copy_unpad<<<g, 256, 0, st>>>(src, lds, dst, ldd, rows, cols);
+  SR_LAUNCHED();
+  return SR_OK;
+}
+
+bool valid_offsets(int nblk, const int64_t* offs) {
+  if (nblk < 1 || nblk > kMaxBlocks || offs == nullptr || offs[0] != 0) return false;
+  for (int b = 0; b < nblk; b++)
+    if (offs[b + 1] <= offs[b]) return false;
+  return true;
+}
+
+size_t block_solve_ws(int nblk, const int64_t* offs) {
+  std::vector<long long> sizes(nblk);
+  for (int b = 0; b < nblk; b++) sizes[b] = offs[b + 1] - offs[b];
+  Arena a(nullptr, 0);
+  CholSet cs{};
+  carve_chol(a, cs, sizes.data(), nblk);
+  return a.used;
+}
+
+sr_status block_qgt_impl(long long ns, int nblk, const int64_t* offs, const double2* A, long long lda,
+                         double2* S, cudaStream_t st) {
+  gram::ProbSet ps{};
+  long long soff = 0;
+  for (int b = 0; b < nblk; b++) {
+    const long long n = offs[b + 1] - offs[b];
+    gram::add_prob(ps, A + offs[b], lda, A + offs[b], lda, S + soff, n, (int)n, (int)n, ns, true);
+    soff += n * n;
+  }
+  return gram::launch<gram::TN, gram::HERM_STORE>(ps, st);
+}
+
+sr_status block_solve_impl(int nblk, const int64_t* offs, const double2* S, const double2* F, double lam,
+                           double2* dtheta, int* info, void* ws, size_t bytes, cudaStream_t st) {
+  std::vector<long long> sizes(nblk);
+  for (int b = 0; b < nblk; b++) sizes[b] = offs[b + 1] - offs[b];
+  Arena a(ws, bytes);
+  CholSet cs{};
+  cs.info = info;
+  carve_chol(a, cs, sizes.data(), nblk);
+  if (!a.ok()) {
+    set_error("sr_block_solve: workspace too small");
+    return SR_ERR_WORKSPACE;
+  }
+  long long soff = 0;
+  for (int b = 0; b < nblk; b++) {
+    cs.b[b].S = S + soff;
+    cs.b[b].F = F + offs[b];
+    cs.b[b].out = dtheta + offs[b];
+    soff += sizes[b] * sizes[b];
+  }
+  return chol_solve(cs, lam, false, -1.0, st);
+}
+
+struct StepLayout {
+  NetDesc net;
+  std::vector<int64_t> offs;
+  size_t log_psi, O, e_loc, energy, e_tilde, F, S, scratch, scratch_bytes, total;
+  size_t h_theta, h_spins, h_bij, h_bj, h_dtheta, h_energy, host_total;
+};
+
+sr_status step_layout(int n_layers, const int32_t* widths, long long ns, long long nb, StepLayout* L) {
+  SR_TRY(make_net(n_layers, widths, &L->net));
+  const NetDesc& net = L->net;
+  L->offs.assign(n_layers + 1, 0);
+  for (int l = 0; l < n_layers; l++) L->offs[l + 1] = L->offs[l] + (int64_t)net.w[l + 1] * (net.w[l] + 1);
+  long long s_elems = 0;
+  for (int l = 0; l < n_layers; l++) s_elems += (L->offs[l + 1] - L->offs[l]) * (L->offs[l + 1] - L->offs[l]);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += round256(bytes);
+    return o;
+  };
+  const size_t c16 = sizeof(double2);
+  L->log_psi = take(ns * c16);
+  L->O = take((size_t)ns * net.n_p * c16);
+  L->e_loc = take(ns * c16);
+  L->energy = take(c16);
+  L->e_tilde = take(ns * c16);
+  L->F = take(net.n_p * c16);
+  L->S = take((size_t)s_elems * c16);
+  size_t scr = jacobian_ws(net, ns);
+  scr = std::max(scr, local_energy_ws(net, ns, nb));
+  scr = std::max(scr, center_force_ws(ns, net.n_p));
+  scr = std::max(scr, block_solve_ws(n_layers, L->offs.data()));
+  L->scratch_bytes = round256(scr);
+  L->scratch = take(L->scratch_bytes);
+  L->total = off;
+  L->h_theta = take(net.n_p * c16);
+  L->h_spins = take((size_t)ns * net.w[0]);
+  L->h_bij = take((size_t)nb * 2 * sizeof(int32_t));
+  L->h_bj = take((size_t)nb * sizeof(double));
+  L->h_dtheta = take(net.n_p * c16);
+  L->h_energy = take(c16);
+  L->host_total = off - L->total;
+  return SR_OK;
+}
+
+sr_status step_impl(const StepLayout& L, const double* theta, const int8_t* spins, long long ns, long long nb,
+                    const int32_t* bij, const double* bj, double lam, double* dtheta, double* energy, char* ws,
+                    cudaStream_t st) {
+  const NetDesc& net = L.net;
+  double* log_psi = reinterpret_cast<double*>(ws + L.log_psi);
+  double* O = reinterpret_cast<double*>(ws + L.O);
+  double* e_loc = reinterpret_cast<double*>(ws + L.e_loc);
+  double* e_tilde = reinterpret_cast<double*>(ws + L.e_tilde);
+  double* F = reinterpret_cast<double*>(ws + L.F);
+  double2* S = reinterpret_cast<double2*>(ws + L.S);
+  void* scr = ws + L.scratch;
+  SR_TRY(jacobian_impl(net, theta, spins, ns, log_psi, O, net.n_p, scr, L.scratch_bytes, st));
+  SR_TRY(local_energy_impl(net, theta, nb, bij, bj, spins, ns, log_psi, e_loc, scr, L.scratch_bytes, st));
+  SR_TRY(center_force_impl(ns, net.n_p, O, net.n_p, nullptr, e_loc, energy, e_tilde, F, scr, L.scratch_bytes, st));
+  SR_TRY(block_qgt_impl(ns, net.L, L.offs.data(), reinterpret_cast<const double2*>(O), net.n_p, S, st));
+  SR_TRY(block_solve_impl(net.L, L.offs.data(), S, reinterpret_cast<const double2*>(F), lam,
+                          reinterpret_cast<double2*>(dtheta), nullptr, scr, L.scratch_bytes, st));
+  return SR_OK;
+}
+
+}  // namespace
+}  // namespace sr
+
+using namespace sr;
+
+extern "C" {
+
+SR_API int sr_version(void) { return 100; }
+SR_API const char* sr_last_error(void) { return g_err.c_str(); }
+SR_API int64_t sr_launch_count(void) { return g_launches; }
+SR_API void sr_reset_launch_count(void) { g_launches = 0; }
+
+SR_API size_t sr_jacobian_workspace_bytes(int n_layers, const int32_t* widths, int64_t n_samples) {
+  NetDesc net;
+  if (make_net(n_layers, widths, &net) != SR_OK || n_samples < 0) return 0;
+  return jacobian_ws(net, n_samples);
+}
+
+SR_API sr_status sr_jacobian(int n_layers, const int32_t* widths, const double* theta, const int8_t* spins,
+                             int64_t n_samples, double* log_psi, double* O, int64_t ldo, void* workspace,
+                             size_t workspace_bytes, void* stream) {
+  NetDesc net;
+  SR_TRY(make_net(n_layers, widths, &net));
+  SR_CHECK_ARG(n_samples >= 0, "n_samples < 0");
+  SR_CHECK_ARG(ldo >= net.n_p, "ldo < n_p");
+  SR_CHECK_ARG(n_samples == 0 || (theta && spins && log_psi && O && workspace), "null pointer");
+  return jacobian_impl(net, theta, spins, n_samples, log_psi, O, ldo, workspace, workspace_bytes,
+                       (cudaStream_t)stream);
+}
+
+SR_API size_t sr_local_energy_workspace_bytes(int n_layers, const int32_t* widths, int64_t n_samples,
+                                              int64_t n_bonds) {
+  NetDesc net;
+  if (make_net(n_layers, widths, &net) != SR_OK || n_samples < 0 || n_bonds < 0) return 0;
+  return local_energy_ws(net, n_samples, n_bonds);
+}
+
+SR_API sr_status sr_local_energy(int n_layers, const int32_t* widths, const double* theta, int64_t n_bonds,
+                                 const int32_t* bonds_ij, const double* bond_j, const int8_t* spins,
+                                 int64_t n_samples, const double* log_psi, double* e_loc, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  NetDesc net;
+  SR_TRY(make_net(n_layers, widths, &net));
+  SR_CHECK_ARG(n_samples >= 0 && n_bonds >= 0, "negative size");
+  SR_CHECK_ARG(n_samples == 0 || (theta && spins && log_psi && e_loc && workspace), "null pointer");
+  SR_CHECK_ARG(n_bonds == 0 || (bonds_ij && bond_j), "null bond arrays");
+  return local_energy_impl(net, theta, n_bonds, bonds_ij, bond_j, spins, n_samples, log_psi, e_loc, workspace,
+                           workspace_bytes, (cudaStream_t)stream);
+}
+
+SR_API size_t sr_center_force_workspace_bytes(int64_t n_samples, int64_t n_p) {
+  if (n_samples < 0 || n_p < 0) return 0;
+  return center_force_ws(n_samples, n_p);
+}
+
+SR_API sr_status sr_center_force(int64_t n_samples, int64_t n_p, double* O, int64_t ldo, const double* weights,
+                                 const double* e_loc, double* energy, double* e_tilde, double* F, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(n_samples >= 1 && n_p >= 1, "n_samples and n_p must be >= 1");
+  SR_CHECK_ARG(ldo >= n_p, "ldo < n_p");
+  SR_CHECK_ARG(O && e_loc && e_tilde && F && workspace, "null pointer");
+  return center_force_impl(n_samples, n_p, O, ldo, weights, e_loc, energy, e_tilde, F, workspace, workspace_bytes,
+                           (cudaStream_t)stream);
+}
+
+SR_API size_t sr_column_moments_workspace_bytes(int64_t n_local, int64_t n_p) {
+  if (n_local < 0 || n_p < 0) return 0;
+  return center_force_ws(n_local, n_p);
+}
+
+SR_API sr_status sr_column_moments(int64_t n_local, int64_t n_total, int64_t n_p, const double* O, int64_t ldo,
+                                   const double* weights, const double* e_loc, double* wsum_O, double* wsum_E,
+                                   void* workspace, size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(n_local >= 1 && n_total >= n_local && n_p >= 1, "bad sizes");
+  SR_CHECK_ARG(ldo >= n_p, "ldo < n_p");
+  SR_CHECK_ARG(O && e_loc && wsum_O && wsum_E && workspace, "null pointer");
+  return column_moments_impl(n_local, n_total, n_p, O, ldo, weights, e_loc, wsum_O, wsum_E, workspace,
+                             workspace_bytes, (cudaStream_t)stream);
+}
+
+SR_API sr_status sr_center_force_global(int64_t n_local, int64_t n_total, int64_t n_p, double* O, int64_t ldo,
+                                        const double* weights, const double* e_loc, const double* mean_O,
+                                        const double* energy, double* e_tilde, double* F_partial,
+                                        void* workspace, size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(n_local >= 1 && n_total >= n_local && n_p >= 1, "bad sizes");
+  SR_CHECK_ARG(ldo >= n_p, "ldo < n_p");
+  SR_CHECK_ARG(O && e_loc && mean_O && energy && e_tilde && F_partial && workspace, "null pointer");
+  return center_force_global_impl(n_local, n_total, n_p, O, ldo, weights, e_loc, mean_O, energy, e_tilde,
+                                  F_partial, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+SR_API size_t sr_block_qgt_workspace_bytes(int n_blocks, const int64_t* block_offsets) {
+  (void)n_blocks;
+  (void)block_offsets;
+  return 0;
+}
+
+SR_API sr_status sr_block_qgt(int64_t n_samples, int n_blocks, const int64_t* block_offsets, const double* A,
+                              int64_t lda, double* S, void* workspace, size_t workspace_bytes, void* stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  SR_CHECK_ARG(valid_offsets(n_blocks, block_offsets), "block_offsets must start at 0 and increase; 1..24 blocks");
+  SR_CHECK_ARG(n_samples >= 0 && lda >= block_offsets[n_blocks], "lda < n_p");
+  for (int b = 0; b < n_blocks; b++)
+    SR_CHECK_ARG(block_offsets[b + 1] - block_offsets[b] < (1LL << 31), "block too large");
+  SR_CHECK_ARG(A && S, "null pointer");
+  return block_qgt_impl(n_samples, n_blocks, block_offsets, reinterpret_cast<const double2*>(A), lda,
+                        reinterpret_cast<double2*>(S), (cudaStream_t)stream);
+}
+
+SR_API size_t sr_block_solve_workspace_bytes(int n_blocks, const int64_t* block_offsets) {
+  if (!valid_offsets(n_blocks, block_offsets)) return 0;
+  return block_solve_ws(n_blocks, block_offsets);
+}
+
+SR_API sr_status sr_block_solve(int n_blocks, const int64_t* block_offsets, const double* S, const double* F,
+                                double lambda, double* dtheta, int32_t* info, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(valid_offsets(n_blocks, block_offsets), "block_offsets must start at 0 and increase; 1..24 blocks");
+  SR_CHECK_ARG(S && F && dtheta && workspace, "null pointer");
+  SR_CHECK_ARG(lambda >= 0.0, "lambda < 0");
+  return block_solve_impl(n_blocks, block_offsets, reinterpret_cast<const double2*>(S),
+                          reinterpret_cast<const double2*>(F), lambda, reinterpret_cast<double2*>(dtheta), info,
+                          workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+SR_API size_t sr_full_qgt_solve_workspace_bytes(int64_t n_samples, int64_t n_p) {
+  (void)n_samples;
+  if (n_p < 1) return 0;
+  long long sz = n_p;
+  Arena a(nullptr, 0);
+  CholSet cs{};
+  carve_chol(a, cs, &sz, 1);
+  return a.used;
+}
+
+SR_API sr_status sr_full_qgt_solve(int64_t n_samples, int64_t n_p, const double* A, int64_t lda, const double* F,
+                                   double lambda, double* dtheta, double* S_out, int32_t* info, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(n_samples >= 0 && n_p >= 1 && n_p < (1LL << 31), "bad sizes");
+  SR_CHECK_ARG(lda >= n_p, "lda < n_p");
+  SR_CHECK_ARG(A && F && dtheta && workspace, "null pointer");
+  SR_CHECK_ARG(lambda >= 0.0, "lambda < 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  long long sz = n_p;
+  Arena a(workspace, workspace_bytes);
+  CholSet cs{};
+  cs.info = info;
+  carve_chol(a, cs, &sz, 1);
+  if (!a.ok()) {
+    set_error("sr_full_qgt_solve: workspace too small");
+    return SR_ERR_WORKSPACE;
+  }
+  CholBlock& B = cs.b[0];
+  const double2* Ad = reinterpret_cast<const double2*>(A);
+  gram::ProbSet ps{};
+  gram::add_prob(ps, Ad, lda, Ad, lda, B.Fm, B.npad, (int)n_p, (int)n_p, n_samples, true);
+  SR_TRY((gram::launch<gram::TN, gram::HERM_STORE>(ps, st)));
+  if (S_out) SR_TRY(copy_matrix(B.Fm, B.npad, reinterpret_cast<double2*>(S_out), n_p, n_p, n_p, st));
+  B.F = reinterpret_cast<const double2*>(F);
+  B.out = reinterpret_cast<double2*>(dtheta);
+  return chol_solve(cs, lambda, true, -1.0, st);
+}
+
+SR_API size_t sr_ntk_solve_workspace_bytes(int64_t n_samples, int64_t n_p) {
+  if (n_samples < 1 || n_p < 1) return 0;
+  long long sz = n_samples;
+  Arena a(nullptr, 0);
+  CholSet cs{};
+  carve_chol(a, cs, &sz, 1);
+  a.take<double2>(n_samples);
+  return a.used + aHv_ws(n_samples, n_p);
+}
+
+SR_API sr_status sr_ntk_solve(int64_t n_samples, int64_t n_p, const double* A, int64_t lda, const double* e_tilde,
+                              double lambda, double* dtheta, double* T_out, int32_t* info, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(n_samples >= 1 && n_samples < (1LL << 31) && n_p >= 1, "bad sizes");
+  SR_CHECK_ARG(lda >= n_p, "lda < n_p");
+  SR_CHECK_ARG(A && e_tilde && dtheta && workspace, "null pointer");
+  SR_CHECK_ARG(lambda >= 0.0, "lambda < 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  long long sz = n_samples;
+  Arena a(workspace, workspace_bytes);
+  CholSet cs{};
+  cs.info = info;
+  carve_chol(a, cs, &sz, 1);
+  double2* y = a.take<double2>(n_samples);
+  const size_t rest = a.ok() ? workspace_bytes - a.used : 0;
+  if (!a.ok() || rest < aHv_ws(n_samples, n_p)) {
+    set_error("sr_ntk_solve: workspace too small");
+    return SR_ERR_WORKSPACE;
+  }
+  CholBlock& B = cs.b[0];
+  const double2* Ad = reinterpret_cast<const double2*>(A);
+  gram::ProbSet ps{};
+  gram::add_prob(ps, Ad, lda, Ad, lda, B.Fm, B.npad, (int)n_samples, (int)n_samples, n_p, true);
+  SR_TRY((gram::launch<gram::NH, gram::HERM_STORE>(ps, st)));
+  if (T_out)
+    SR_TRY(copy_matrix(B.Fm, B.npad, reinterpret_cast<double2*>(T_out), n_samples, n_samples, n_samples, st));
+  B.F = reinterpret_cast<const double2*>(e_tilde);
+  B.out = y;
+  SR_TRY(chol_solve(cs, lambda, true, 1.0, st));
+  return aHv_impl(n_samples, n_p, Ad, lda, y, -1.0, reinterpret_cast<double2*>(dtheta), a.base + a.used, rest, st);
+}
+
+SR_API size_t sr_step_workspace_bytes(int n_layers, const int32_t* widths, int64_t n_samples, int64_t n_bonds) {
+  StepLayout L;
+  if (n_samples < 1 || n_bonds < 0 || step_layout(n_layers, widths, n_samples, n_bonds, &L) != SR_OK) return 0;
+  return L.total;
+}
+
+SR_API size_t sr_step_s_offset(int n_layers, const int32_t* widths, int64_t n_samples, int64_t n_bonds) {
+  StepLayout L;
+  if (n_samples < 1 || n_bonds < 0 || step_layout(n_layers, widths, n_samples, n_bonds, &L) != SR_OK) return 0;
+  return L.S;
+}
+
+SR_API sr_status sr_step(int n_layers, const int32_t* widths, const double* theta, const int8_t* spins,
+                         int64_t n_samples, int64_t n_bonds, const int32_t* bonds_ij, const double* bond_j,
+                         double lambda, double* dtheta, double* energy, void* workspace, size_t workspace_bytes,
+                         void* stream) {
+  SR_CHECK_ARG(n_samples >= 1 && n_bonds >= 0, "bad sizes");
+  StepLayout L;
+  SR_TRY(step_layout(n_layers, widths, n_samples, n_bonds, &L));
+  SR_CHECK_ARG(theta && spins && dtheta && workspace, "null pointer");
+  SR_CHECK_ARG(n_bonds == 0 || (bonds_ij && bond_j), "null bond arrays");
+  SR_CHECK_ARG(lambda >= 0.0, "lambda < 0");
+  if (workspace_bytes < L.total) {
+    set_error("sr_step: workspace too small");
+    return SR_ERR_WORKSPACE;
+  }
+  double* e = energy ? energy : reinterpret_cast<double*>(static_cast<char*>(workspace) + L.energy);
+  return step_impl(L, theta, spins, n_samples, n_bonds, bonds_ij, bond_j, lambda, dtheta, e,
+                   static_cast<char*>(workspace), (cudaStream_t)stream);
+}
+
+SR_API size_t sr_step_host_extra_bytes(int n_layers, const int32_t* widths, int64_t n_samples, int64_t n_bonds) {
+  StepLayout L;
+  if (n_samples < 1 || n_bonds < 0 || step_layout(n_layers, widths, n_samples, n_bonds, &L) != SR_OK) return 0;
+  return L.host_total;
+}
+
+SR_API sr_status sr_step_host(int n_layers, const int32_t* widths, const double* theta_h, const int8_t* spins_h,
+                              int64_t n_samples, int64_t n_bonds, const int32_t* bonds_ij_h, const double* bond_j_h,
+                              double lambda, double* dtheta_h, double* energy_h, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(n_samples >= 1 && n_bonds >= 0, "bad sizes");
+  StepLayout L;
+  SR_TRY(step_layout(n_layers, widths, n_samples, n_bonds, &L));
+  SR_CHECK_ARG(theta_h && spins_h && dtheta_h && workspace, "null pointer");
+  SR_CHECK_ARG(n_bonds == 0 || (bonds_ij_h && bond_j_h), "null bond arrays");
+  if (workspace_bytes < L.total + L.host_total) {
+    set_error("sr_step_host: workspace too small");
+    return SR_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = static_cast<char*>(workspace);
+  const size_t c16 = sizeof(double2);
+  const long long np = L.net.n_p;
+  double* theta = reinterpret_cast<double*>(ws + L.h_theta);
+  int8_t* spins = reinterpret_cast<int8_t*>(ws + L.h_spins);
+  int32_t* bij = reinterpret_cast<int32_t*>(ws + L.h_bij);
+  double* bj = reinterpret_cast<double*>(ws + L.h_bj);
+  double* dtheta = reinterpret_cast<double*>(ws + L.h_dtheta);
+  double* energy = reinterpret_cast<double*>(ws + L.h_energy);
+  SR_CUDA(cudaMemcpyAsync(theta, theta_h, np * c16, cudaMemcpyHostToDevice, st));
+  SR_CUDA(cudaMemcpyAsync(spins, spins_h, (size_t)n_samples * L.net.w[0], cudaMemcpyHostToDevice, st));
+  if (n_bonds) {
+    SR_CUDA(cudaMemcpyAsync(bij, bonds_ij_h, (size_t)n_bonds * 2 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    SR_CUDA(cudaMemcpyAsync(bj, bond_j_h, (size_t)n_bonds * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  SR_TRY(step_impl(L, theta, spins, n_samples, n_bonds, bij, bj, lambda, dtheta, energy, ws, st));
+  SR_CUDA(cudaMemcpyAsync(dtheta_h, dtheta, np * c16, cudaMemcpyDeviceToHost, st));
+  if (energy_h) SR_CUDA(cudaMemcpyAsync(energy_h, energy, c16, cudaMemcpyDeviceToHost, st));
+  SR_CUDA(cudaStreamSynchronize(st));
+  return SR_OK;
+}
+
+}  // extern "C"

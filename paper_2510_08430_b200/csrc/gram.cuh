@@ -1,0 +1,271 @@
+// gram.cuh — FP64 tensor-core (DMMA.8x8x4) complex tile engine.
+//
+// One engine serves every dense contraction of the step:
+//   stage (4)  S_b = A_b^H A_b         (flavor TN: operands K-major, A conjugated)   PAPER.md Eq. 3
+//   full QGT   S   = A^H A              (flavor TN)                                   PAPER.md §2
+//   NTK        T   = A A^H              (flavor NH: operands row-major along K, B conjugated)
+//   Cholesky   trailing update C -= L_p L_p^H and the panel TRSM L_ip = A_ip Linv^H (flavor NH)
+// Tile 64x64 complex per CTA, K step 16, 256 threads = 8 warps (2 x 4), warp tile 32x16
+// complex = 4 x 2 DMMA 8x8 sub-tiles, each complex product as 4 real DMMAs (re/im planes
+// de-interleaved from the LDS.128 of one complex element).  Operand tiles are staged by
+// a 3-stage cp.async pipeline (16-byte copies, zero-fill outside the matrix) into padded
+// shared-memory tiles whose strides make every fragment load bank-conflict free.
+#pragma once
+#include "common.cuh"
+
+namespace sr {
+namespace gram {
+
+constexpr int BM = 64;   // tile rows   (complex)
+constexpr int BN = 64;   // tile cols   (complex)
+constexpr int BK = 16;   // K per stage (complex)
+constexpr int kStages = 3;
+constexpr int kThreads = 256;
+constexpr int kMaxProbs = 24;
+
+// Operand storage flavors.
+//  TN: a(m,k) = conj(A[k*lda + m]), b(k,n) = B[k*ldb + n]   (tile smem [BK][64+2])
+//  NH: a(m,k) = A[m*lda + k],       b(k,n) = conj(B[n*ldb + k]) (tile smem [64][BK+4])
+enum Flavor { TN = 0, NH = 1 };
+// Epilogues: C = tile with conj-transposed mirror (Hermitian result, diagonal imag = 0);
+// C -= tile; C = tile.
+enum Epi { HERM_STORE = 0, SUB = 1, STORE = 2 };
+
+struct Prob {
+  const double2* A;
+  const double2* B;
+  double2* C;
+  long long lda, ldb, ldc;
+  int M, N;           // C is M x N (LOWER tile sets use M == N and tiles I >= J)
+  long long K;
+  int lower;          // 1: tiles with I >= J only; 0: all Mt x Nt tiles
+  int tiles_n;        // Nt (column tiles)
+  long long tile_begin;
+};
+
+struct ProbSet {
+  int count;
+  long long total_tiles;
+  Prob p[kMaxProbs];
+};
+
+constexpr int TN_LD = BM + 2;   // 66 complex = 1056 B per k-row  (1056 mod 128 = 32)
+constexpr int NH_LD = BK + 4;   // 20 complex =  320 B per m-row  ( 320 mod 128 = 64)
+template <int FL>
+constexpr int tile_elems() { return FL == TN ? BK * TN_LD : BM * NH_LD; }   // 1056 / 1280
+template <int FL>
+constexpr size_t smem_bytes() { return (size_t)kStages * 2 * tile_elems<FL>() * sizeof(double2); }
+// TN (the QGT Gram): 101 KB -> 2 CTAs per SM; NH: 123 KB -> 1 CTA per SM.
+template <int FL>
+constexpr int min_blocks() { return FL == TN ? 2 : 1; }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Load one K-stage of the operand covering rows/cols [r0, r0+64) of the matrix.
+// TN: smem[k][m] <- X[(k0+k)*ld + r0+m];  NH: smem[m][k] <- X[(r0+m)*ld + k0+k].
+template <int FL>
+__device__ __forceinline__ void load_tile(double2* s, const double2* X, long long ld, int r0, int rmax,
+                                          long long k0, long long K) {
+#pragma unroll
+  for (int it = 0; it < (BK * 64) / kThreads; it++) {
+    const int e = threadIdx.x + it * kThreads;
+    int kk, mm;
+    if (FL == TN) {
+      kk = e >> 6;
+      mm = e & 63;
+    } else {
+      mm = e >> 4;
+      kk = e & 15;
+    }
+    const long long gk = k0 + kk;
+    const int gm = r0 + mm;
+    const bool v = (gk < K) && (gm < rmax);
+    const double2* src = v ? (FL == TN ? X + gk * ld + gm : X + (long long)gm * ld + gk) : X;
+    double2* dst = FL == TN ? s + kk * TN_LD + mm : s + mm * NH_LD + kk;
+    cp_async16(dst, src, v);
+  }
+}
+
+// Fragment fetch: element (row r, k) of a 64-row operand tile.
+template <int FL>
+__device__ __forceinline__ double2 frag(const double2* s, int r, int k) {
+  return FL == TN ? s[k * TN_LD + r] : s[r * NH_LD + k];
+}
+
+__device__ __forceinline__ void tile_of(const ProbSet& ps, long long t, int& pi, int& I, int& J) {
+  pi = 0;
+#pragma unroll 1
+  while (pi + 1 < ps.count && t >= ps.p[pi + 1].tile_begin) pi++;
+  const long long lt = t - ps.p[pi].tile_begin;
+  if (ps.p[pi].lower) {
+    long long i = (long long)((sqrt(8.0 * (double)lt + 1.0) - 1.0) * 0.5);
+    while ((i + 1) * (i + 2) / 2 <= lt) i++;
+    while (i * (i + 1) / 2 > lt) i--;
+    I = (int)i;
+    J = (int)(lt - i * (i + 1) / 2);
+  } else {
+    I = (int)(lt / ps.p[pi].tiles_n);
+    J = (int)(lt % ps.p[pi].tiles_n);
+  }
+}
+
+template <int FL, int EP>
+__global__ void __launch_bounds__(kThreads, min_blocks<FL>()) tile_kernel(const __grid_constant__ ProbSet ps) {
+  extern __shared__ __align__(16) double2 smem[];
+  int pi, I, J;
+  tile_of(ps, blockIdx.x, pi, I, J);
+  const Prob& P = ps.p[pi];
+  const int m0 = I * BM, n0 = J * BN;
+  const long long K = P.K;
+  const int KT = (int)((K + BK - 1) / BK);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int lr = lane >> 2, lk = lane & 3;
+
+  double acc_r[4][2][2], acc_i[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int b = 0; b < 2; b++) {
+      acc_r[a][b][0] = acc_r[a][b][1] = 0.0;
+      acc_i[a][b][0] = acc_i[a][b][1] = 0.0;
+    }
+
+  constexpr int TE = tile_elems<FL>();
+  auto sA = [&](int st) { return smem + (size_t)st * 2 * TE; };
+  auto sB = [&](int st) { return smem + (size_t)st * 2 * TE + TE; };
+
+#pragma unroll
+  for (int s = 0; s < kStages - 1; s++) {
+    if (s < KT) {
+      load_tile<FL>(sA(s), P.A, P.lda, m0, P.M, (long long)s * BK, K);
+      load_tile<FL>(sB(s), P.B, P.ldb, n0, P.N, (long long)s * BK, K);
+    }
+    cp_commit();
+  }
+
+#pragma unroll 1
+  for (int kt = 0; kt < KT; kt++) {
+    cp_wait<kStages - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + kStages - 1;
+      const int st = nk % kStages;
+      if (nk < KT) {
+        load_tile<FL>(sA(st), P.A, P.lda, m0, P.M, (long long)nk * BK, K);
+        load_tile<FL>(sB(st), P.B, P.ldb, n0, P.N, (long long)nk * BK, K);
+      }
+      cp_commit();
+    }
+    const double2* a_s = sA(kt % kStages);
+    const double2* b_s = sB(kt % kStages);
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double ar[4], ai[4], nai[4], br[2], bi[2];
+#pragma unroll
+      for (int mi = 0; mi < 4; mi++) {
+        const double2 v = frag<FL>(a_s, wm * 32 + mi * 8 + lr, k4 + lk);
+        ar[mi] = v.x;
+        ai[mi] = FL == TN ? -v.y : v.y;   // a(m,k) = conj(.) in TN
+        nai[mi] = -ai[mi];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 2; ni++) {
+        const double2 v = frag<FL>(b_s, wn * 16 + ni * 8 + lr, k4 + lk);
+        br[ni] = v.x;
+        bi[ni] = FL == NH ? -v.y : v.y;   // b(k,n) = conj(.) in NH
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+        for (int ni = 0; ni < 2; ni++) {
+          // (ar + i ai)(br + i bi) = (ar br - ai bi) + i (ar bi + ai br)
+          dmma(acc_r[mi][ni][0], acc_r[mi][ni][1], ar[mi], br[ni]);
+          dmma(acc_i[mi][ni][0], acc_i[mi][ni][1], ar[mi], bi[ni]);
+          dmma(acc_r[mi][ni][0], acc_r[mi][ni][1], nai[mi], bi[ni]);
+          dmma(acc_i[mi][ni][0], acc_i[mi][ni][1], ai[mi], br[ni]);
+        }
+    }
+  }
+  cp_wait<0>();
+
+  // Epilogue: lane holds C[m][n], C[m][n+1] of each 8x8 sub-tile, m = .. + lane/4,
+  // n = .. + 2*(lane%4).
+#pragma unroll
+  for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+    for (int ni = 0; ni < 2; ni++) {
+      const int m = m0 + wm * 32 + mi * 8 + lr;
+      const int nb = n0 + wn * 16 + ni * 8 + 2 * lk;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int n = nb + h;
+        if (m >= P.M || n >= P.N) continue;
+        double2 v = make_double2(acc_r[mi][ni][h], acc_i[mi][ni][h]);
+        double2* c = P.C + (long long)m * P.ldc + n;
+        if (EP == HERM_STORE) {
+          if (m == n) v.y = 0.0;
+          *c = v;
+          if (I != J) P.C[(long long)n * P.ldc + m] = cconj(v);
+        } else if (EP == SUB) {
+          *c = csub(*c, v);
+        } else {
+          *c = v;
+        }
+      }
+    }
+}
+
+// Host helpers -----------------------------------------------------------------
+inline int tiles(long long n, int b) { return (int)((n + b - 1) / b); }
+
+inline void add_prob(ProbSet& ps, const double2* A, long long lda, const double2* B, long long ldb, double2* C,
+                     long long ldc, int M, int N, long long K, bool lower) {
+  Prob& p = ps.p[ps.count];
+  p.A = A;
+  p.B = B;
+  p.C = C;
+  p.lda = lda;
+  p.ldb = ldb;
+  p.ldc = ldc;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.lower = lower ? 1 : 0;
+  const int tm = tiles(M, BM), tn = tiles(N, BN);
+  p.tiles_n = tn;
+  p.tile_begin = ps.total_tiles;
+  ps.total_tiles += lower ? (long long)tm * (tm + 1) / 2 : (long long)tm * tn;
+  ps.count++;
+}
+
+template <int FL, int EP>
+inline sr_status launch(const ProbSet& ps, cudaStream_t st) {
+  if (ps.total_tiles == 0) return SR_OK;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SR_CUDA(cudaFuncSetAttribute(tile_kernel<FL, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem_bytes<FL>()));
+    attr_set = true;
+  }
+  tile_kernel<FL, EP><<<(unsigned)ps.total_tiles, kThreads, smem_bytes<FL>(), st>>>(ps);
+  SR_LAUNCHED();
+  return SR_OK;
+}
+
+}  // namespace gram
+}  // namespace sr
