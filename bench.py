@@ -1,0 +1,361 @@
+"""Block-SR step benchmark (BASELINE.json metric) — one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl reference]
+
+A step is one pass of the whole hot path over one batch of synthetic input
+(DESIGN.md §8(a)): Jacobian -> local energy -> centring + force -> block QGT (Gram) ->
+block solve, each stage one C-ABI call of libsrblock.so.  Default workload: BASELINE.json
+configs[1] (1D Heisenberg ring N=40, MLP 40->80->80->80, N_s=4096, lambda=1e-3).
+
+`value` times the device-resident step with CUDA events on the launching stream
+(barrier + synchronize on both sides, max over ranks); `e2e` times sr_step_host (host
+inputs copied in, dtheta/energy copied out, every step).  `--impl reference` times the
+CPU oracle (the reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "block-SR steps/sec (Jacobian->Gram->solve), Gram FP64 TFLOPS vs B200 peak"
+DEFAULT_WORKLOAD = workloads.CONFIGS[1].name
+FP64_PEAK_TFLOPS = 37.07        # profiles/r01_fp64_peak.json: DMMA.8x8x4 microbenchmark (tools/fp64_peak.cu)
+FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu DMMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak.json)"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_source": "fallback (B200_PROFILING.md)"}
+
+
+def block_sizes(w):
+    return w.layer_sizes
+
+
+def gram_flops(w, ns):
+    """Algorithmic FP64 flops of the block QGT: n_b(n_b+1)/2 unique complex entries of each
+    Hermitian S_b, N_s complex multiply-adds (8 real flops) each."""
+    return sum(8.0 * ns * n * (n + 1) / 2 for n in block_sizes(w))
+
+
+def chol_flops(w):
+    """Algorithmic flops of the Cholesky factorisations: n^3/3 complex MACs per block."""
+    return sum(8.0 * n ** 3 / 3 for n in block_sizes(w))
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- dist
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return int(os.environ.get("RANK", "0")), ws, int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_08430_b200 as sr
+    from paper_2510_08430_b200 import parallel
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = workloads.BY_NAME[args.workload]
+    spins_all, params = workloads.make_inputs(w)
+    ij, jj = sr.lattice.for_workload(w)
+    theta_h = sr.model.pack(params)
+    n_p, ns = w.n_params, w.n_samples
+    offs = sr.block_offsets(w.widths)
+
+    if world > 1:
+        step = parallel.ShardedStep(w.widths, spins_all, ij, jj, w.lam, rank, world, dev)
+    else:
+        step = parallel.LocalStep(w.widths, spins_all, ij, jj, w.lam, dev)
+    theta = torch.from_numpy(theta_h).to(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        step.run(theta)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    n_ev = len(step.STAGES) + 1
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
+    sr.sr_reset_launch_count()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for k in range(args.steps):
+        step.run(theta, events=evs[k])
+    stop.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = sr.sr_launch_count()
+    clk = clocks.stop()
+    total_ms = start.elapsed_time(stop)
+    stage_ms = {name: float(np.mean([evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(args.steps)]))
+                for i, name in enumerate(step.STAGES)}
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # e2e: the same step through sr_step_host (host buffers in and out, every step)
+    e2e = None
+    if world == 1:
+        e2e = run_e2e(sr, torch, w, theta_h, spins_all, ij, jj, dev, args)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    ms_per_step = total_ms / args.steps
+    peaks = _peaks()
+    gram_ms = stage_ms["block_qgt"]
+    gflop = gram_flops(w, ns / world)
+    achieved = gflop / (gram_ms * 1e-3) / 1e12
+    traffic = _ncu_traffic()
+    O_bytes = 16.0 * ns / world * n_p
+    jac_ms = stage_ms["jacobian"]
+    rec = {
+        "metric": METRIC,
+        "value": args.steps / (total_ms * 1e-3),
+        "unit": "steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded uniform S^z=0 spins, complex-normal weights; workloads.py)",
+        "config": {"workload": w.name, "lattice": f"{w.lattice}{'x'.join(map(str, w.extent))}",
+                   "widths": list(w.widths), "n_samples": ns, "n_params": n_p, "blocks": block_sizes(w),
+                   "lambda": w.lam, "parallelism": f"samples sharded x{world}" if world > 1 else "single GPU",
+                   "l2": f"inputs larger than L2 (O = {16.0 * ns * n_p / 1e9:.2f} GB per step vs 126 MB L2); no flush"},
+        "roofline": {"kernel": "gram::tile_kernel<TN,HERM_STORE> (sr_block_qgt)", "bound": "tensor",
+                     "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                     "algorithmic": f"sum_b 4 N_s n_b (n_b+1) = {gflop:.4e} flop per launch",
+                     "peak_source": FP64_PEAK_SOURCE},
+        "stage_roofline": {
+            "jacobian": {"bound": "hbm", "achieved_gbs": O_bytes / (jac_ms * 1e-3) / 1e9,
+                         "peak_gbs": peaks["hbm_gbs"], "frac": O_bytes / (jac_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                         "algorithmic": "16 B x N_s x n_p written (O)"},
+            "center_force": {"bound": "hbm",
+                             "achieved_gbs": 3 * O_bytes / (stage_ms["center_force"] * 1e-3) / 1e9,
+                             "peak_gbs": peaks["hbm_gbs"],
+                             "frac": 3 * O_bytes / (stage_ms["center_force"] * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                             "algorithmic": "O read twice, A written once"},
+            "block_solve": {"bound": "tensor", "achieved_tflops": chol_flops(w) / (stage_ms["block_solve"] * 1e-3) / 1e12,
+                            "peak_tflops": FP64_PEAK_TFLOPS,
+                            "frac": chol_flops(w) / (stage_ms["block_solve"] * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                            "algorithmic": "sum_b 8 n_b^3 / 3"},
+        },
+        "stages_ms": stage_ms,
+        "gpu_launches": launches,
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rec["cpu_baseline"] = cpu_baseline(w)
+    print(json.dumps(rec), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(sr, torch, w, theta_h, spins, ij, jj, dev, args):
+    nb = len(jj)
+    th = torch.from_numpy(theta_h).pin_memory()
+    sp = torch.from_numpy(spins).pin_memory()
+    bij = torch.from_numpy(ij).pin_memory()
+    bj = torch.from_numpy(jj).pin_memory()
+    dth = torch.empty(w.n_params, dtype=torch.complex128).pin_memory()
+    en = torch.empty(1, dtype=torch.complex128).pin_memory()
+    nbytes = sr.sr_step_workspace_bytes(w.widths, w.n_samples, nb) + sr.sr_step_host_extra_bytes(
+        w.widths, w.n_samples, nb)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    for _ in range(max(1, args.warmup)):
+        sr.sr_step_host(w.widths, th, sp, bij, bj, w.lam, dth, en, ws)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sr.sr_step_host(w.widths, th, sp, bij, bj, w.lam, dth, en, ws)
+    dt = time.perf_counter() - t0
+    del ws
+    return {"value": args.steps / dt, "unit": "steps/s",
+            "h2d_bytes_per_step": int(th.numel() * 16 + sp.numel() + bij.numel() * 4 + bj.numel() * 8),
+            "d2h_bytes_per_step": int(dth.numel() * 16 + en.numel() * 16),
+            "api": "sr_step_host (C ABI, pinned host buffers, host-clock timed, stream synchronised per step)"}
+
+
+def _ncu_traffic():
+    """dram bytes per launch of the Gram kernel from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "gram_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def _threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] or [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_step_estimate(w, n_sub):
+    """Time the oracle on a bounded sample of workload w and scale it to one full step.
+
+    Sample: Jacobian, local energies and centring/force on n_sub samples, the block Gram
+    on the same n_sub samples, the Cholesky-equivalent solve of the smallest block; each
+    part is scaled linearly (samples) or by sum_b n_b^3 / n_min^3 (solve)."""
+    from oracle import estimators, hamiltonian, network, solvers
+    spins, params = workloads.make_inputs(w, n_sub)
+    bonds = hamiltonian.bonds_for(w)
+    off = network.layer_offsets(params)
+    t0 = time.perf_counter()
+    O = network.jacobian(params, spins)
+    e = hamiltonian.local_energies(params, spins, bonds)
+    estimators.force(O, e)
+    t1 = time.perf_counter()
+    blocks = estimators.qgt_blocks(O, off)
+    t2 = time.perf_counter()
+    sizes = block_sizes(w)
+    b0 = int(np.argmin(sizes))
+    S0 = blocks[b0]
+    F0 = np.ones(S0.shape[0], dtype=np.complex128)
+    solvers.shifted_solve(S0, F0, w.lam)
+    t3 = time.perf_counter()
+    scale = w.n_samples / n_sub
+    solve_scale = sum(n ** 3 for n in sizes) / sizes[b0] ** 3
+    est = (t1 - t0) * scale + (t2 - t1) * scale + (t3 - t2) * solve_scale
+    sample = (f"{w.name}: Jacobian+E_loc+force and block Gram on {n_sub} of {w.n_samples} samples (x{scale:g}), "
+              f"shifted solve of the {sizes[b0]}-block (x{solve_scale:.2f} by sum n_b^3); measured "
+              f"{t3 - t0:.1f} s of CPU work")
+    return est, sample
+
+
+def cpu_baseline(w, quick=False):
+    est, sample = oracle_step_estimate(w, 64 if quick else 256)
+    return {"value": 1.0 / est, "unit": "steps/s", "cores": _threads(), "kind": "oracle", "sample": sample}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    w = workloads.BY_NAME[args.workload]
+    for _ in range(args.warmup):
+        oracle_step_estimate(w, 32)
+    ests = []
+    sample = ""
+    for _ in range(args.steps):
+        est, sample = oracle_step_estimate(w, 64)
+        ests.append(est)
+    total = float(np.sum(ests))
+    rec = {"metric": METRIC, "value": args.steps / total, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": w.name, "n_samples": w.n_samples, "n_params": w.n_params},
+           "cpu_baseline": {"value": args.steps / total, "unit": "steps/s", "cores": _threads(), "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": args.steps / total, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(rec), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=list(workloads.BY_NAME))
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -120,21 +120,28 @@ SR_API sr_status sr_center_force(int64_t n_samples, int64_t n_p, double* O, int6
                                  size_t workspace_bytes, void* stream);
 
 /* Sample-sharded form of stage (3) (one call per rank; BASELINE.json north_star:
- * "samples shard naturally").  With n_total samples over all ranks and uniform
- * weights 1/n_total (weights == NULL) or the rank's slice of global weights:
- *   sr_column_moments       wsum_O[c] = sum_{k local} w_k O[k][c],  wsum_E = sum_{k local} w_k E_k
- *   (all-reduce both over ranks -> <O> and E), then
- *   sr_center_force_global  A_k = sqrt(w_k)(O_k - mean_O) in place, e_tilde_k = sqrt(w_k)(E_k - energy),
+ * "samples shard naturally").  n_total samples over all ranks; weights == NULL means
+ * uniform 1/n_total, else the rank's slice of global weights.
+ *   sr_column_moments       writes one moments row, complex [2*n_p + 2]:
+ *                           [ <O>_hi (n_p) | <O>_lo (n_p) | E_hi | E_lo ], the rank's
+ *                           contribution sum_{k local} w_k O_k and sum_{k local} w_k E_k as
+ *                           double-double pairs (reading R7: the centring cancels
+ *                           up to ~6 digits, so the mean is carried beyond double precision).
+ *   (all-gather the rows of all ranks), then
+ *   sr_center_force_global  sums the n_parts rows in double-double, and writes
+ *                           A_k = sqrt(w_k)(O_k - <O>) in place, e_tilde_k = sqrt(w_k)(E_k - E),
+ *                           energy = E (complex [1], may be NULL) and
  *                           F_partial = sum_{k local} conj(A_k) e_k   (all-reduce -> F).
- * Workspace: sr_center_force_workspace_bytes(n_local, n_p). */
+ * Workspace: sr_column_moments_workspace_bytes(n_local, n_p) for both. */
 SR_API size_t sr_column_moments_workspace_bytes(int64_t n_local, int64_t n_p);
 SR_API sr_status sr_column_moments(int64_t n_local, int64_t n_total, int64_t n_p, const double* O, int64_t ldo,
-                                   const double* weights, const double* e_loc, double* wsum_O, double* wsum_E,
+                                   const double* weights, const double* e_loc, double* moments,
                                    void* workspace, size_t workspace_bytes, void* stream);
 SR_API sr_status sr_center_force_global(int64_t n_local, int64_t n_total, int64_t n_p, double* O, int64_t ldo,
-                                        const double* weights, const double* e_loc, const double* mean_O,
-                                        const double* energy, double* e_tilde, double* F_partial,
-                                        void* workspace, size_t workspace_bytes, void* stream);
+                                        const double* weights, const double* e_loc, int n_parts,
+                                        const double* moments, double* energy, double* e_tilde,
+                                        double* F_partial, void* workspace, size_t workspace_bytes,
+                                        void* stream);
 
 /* ---------------------------------------------------------------- stage (4) ---
  * sr_block_qgt — PAPER.md Eq. 3, S_l = <O_l^dag O_l> - <O_l^dag><O_l>, computed per

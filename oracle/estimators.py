@@ -14,6 +14,12 @@ expectations over p_theta(x) = |psi_theta(x)|^2).
     S_ij       = sum_k w_k conj(Obar_ki) Obar_kj     (Eq. 2)
     S_l        = S restricted to layer l's columns   (Eq. 3)
     T_kk'      = sqrt(w_k) (sum_i Obar_ki conj(Obar_k'i)) sqrt(w_k')   (NTK, §1)
+
+Centring precision (reading R7): <O_i> and E are accumulated in extended
+precision (numpy longdouble) and O_ki - <O_i>, E_loc,k - E are rounded to complex128
+once.  For sum-pooled lncosh networks at the BASELINE.json initialisation the last-layer
+bias derivatives are nearly constant over samples (|<O_i>| / std(O_i) up to ~1e6), so a
+double-rounded mean would cost ~6 of the 16 digits of Obar before any estimator is formed.
 """
 from __future__ import annotations
 
@@ -28,37 +34,57 @@ def _w(O, w):
     return uniform_weights(O.shape[0]) if w is None else np.asarray(w, dtype=np.float64)
 
 
+_LD = np.clongdouble
+
+
+def _mean_ld(x, w):
+    """sum_k w_k x_k in extended precision (longdouble accumulation); w = None means the
+    uniform mean (sum_k x_k) / N with the division also in extended precision."""
+    xl = np.asarray(x).astype(_LD)
+    if w is None:
+        return np.sum(xl, axis=0) / np.longdouble(xl.shape[0])
+    return np.sum(np.asarray(w, dtype=np.longdouble)[:, None] * xl, axis=0)
+
+
 def mean_O(O, w=None):
-    w = _w(O, w)
-    return np.array([np.sum(w * O[:, i]) for i in range(O.shape[1])])
+    return _mean_ld(O, w).astype(np.complex128)
 
 
 def center(O, w=None):
-    return O - mean_O(O, w)[None, :]
+    """Obar = O - <O>, the difference taken in extended precision and rounded once."""
+    return (np.asarray(O).astype(_LD) - _mean_ld(O, w)[None, :]).astype(np.complex128)
+
+
+def _energy_ld(e_loc, w):
+    return _mean_ld(np.asarray(e_loc)[:, None], w)[0]
 
 
 def energy(e_loc, w=None):
-    w = uniform_weights(len(e_loc)) if w is None else np.asarray(w)
-    return np.sum(w * e_loc)
+    return complex(_energy_ld(e_loc, w))
+
+
+def centered_energies(e_loc, w=None):
+    """E_loc,k - E with E in extended precision, rounded once."""
+    return (np.asarray(e_loc).astype(_LD) - _energy_ld(e_loc, w)).astype(np.complex128)
 
 
 def force(O, e_loc, w=None):
-    w = _w(O, w)
     ob = center(O, w)
-    eps = e_loc - energy(e_loc, w)
+    eps = centered_energies(e_loc, w)
+    w = _w(O, w)
     return np.array([np.sum(w * np.conj(ob[:, i]) * eps) for i in range(O.shape[1])])
 
 
 def qgt_full(O, w=None):
-    w = _w(O, w)
     ob = center(O, w)
+    w = _w(O, w)
     return ob.conj().T @ (w[:, None] * ob)
 
 
 def qgt_blocks(O, offsets, w=None):
     """[S_l] computed from each layer's own columns (never forming the full S)."""
-    w = _w(O, w)
     ob = center(O, w)
+    w = _w(O, w)
     out = []
     for l in range(len(offsets) - 1):
         a = ob[:, offsets[l]:offsets[l + 1]]
@@ -67,14 +93,12 @@ def qgt_blocks(O, offsets, w=None):
 
 
 def ntk(O, w=None):
-    w = _w(O, w)
-    a = np.sqrt(w)[:, None] * center(O, w)
+    a = np.sqrt(_w(O, w))[:, None] * center(O, w)
     return a @ a.conj().T
 
 
 def scaled_centered(O, e_loc, w=None):
     """(A, e) with A_k = sqrt(w_k) Obar_k and e_k = sqrt(w_k)(E_loc,k - E), so that
     S = A^H A, F = A^H e and T = A A^H (the factorised form both solvers share)."""
-    w = _w(O, w)
-    sw = np.sqrt(w)
-    return sw[:, None] * center(O, w), sw * (e_loc - energy(e_loc, w))
+    sw = np.sqrt(_w(O, w))
+    return sw[:, None] * center(O, w), sw * centered_energies(e_loc, w)

@@ -36,8 +36,8 @@ SIGNATURES = {
     "sr_center_force_workspace_bytes": (_sz, [_i64, _i64]),
     "sr_center_force": (_i32, [_i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "sr_column_moments_workspace_bytes": (_sz, [_i64, _i64]),
-    "sr_column_moments": (_i32, [_i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
-    "sr_center_force_global": (_i32, [_i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
+    "sr_column_moments": (_i32, [_i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "sr_center_force_global": (_i32, [_i64, _i64, _i64, _vp, _i64, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _sz,
                                       _vp]),
     "sr_block_qgt_workspace_bytes": (_sz, [_i32, _I64P]),
     "sr_block_qgt": (_i32, [_i64, _i32, _I64P, _vp, _i64, _vp, _vp, _sz, _vp]),
@@ -176,22 +176,25 @@ def sr_center_force(O, e_loc, energy, e_tilde, F, weights=None, workspace=None):
                                _ptr(e_tilde), _ptr(F), *_ws_args(ws), _stream(O.device)), "sr_center_force")
 
 
-def sr_column_moments(O, e_loc, n_total, wsum_O, wsum_E, weights=None, workspace=None):
+def sr_column_moments(O, e_loc, n_total, moments, weights=None, workspace=None):
+    """moments: complex [2*n_p + 2] (one row, see include/sr_block.h)."""
     lib = load()
-    ns, npar = O.shape[0], wsum_O.shape[0]
+    ns = O.shape[0]
+    npar = (moments.shape[-1] - 2) // 2
     ws = _workspace(lib.sr_column_moments_workspace_bytes(ns, npar), O.device, workspace)
     _check(lib.sr_column_moments(ns, n_total, npar, _ptr(O), O.shape[1], _ptr(weights), _ptr(e_loc),
-                                 _ptr(wsum_O), _ptr(wsum_E), *_ws_args(ws), _stream(O.device)),
-           "sr_column_moments")
+                                 _ptr(moments), *_ws_args(ws), _stream(O.device)), "sr_column_moments")
 
 
-def sr_center_force_global(O, e_loc, n_total, mean_O, energy, e_tilde, F_partial, weights=None,
+def sr_center_force_global(O, e_loc, n_total, moments, e_tilde, F_partial, energy=None, weights=None,
                            workspace=None):
+    """moments: complex [n_parts, 2*n_p + 2] (all ranks' rows)."""
     lib = load()
-    ns, npar = O.shape[0], mean_O.shape[0]
-    ws = _workspace(lib.sr_center_force_workspace_bytes(ns, npar), O.device, workspace)
+    ns, npar = O.shape[0], F_partial.shape[0]
+    rows = moments.reshape(-1, 2 * npar + 2)
+    ws = _workspace(lib.sr_column_moments_workspace_bytes(ns, npar), O.device, workspace)
     _check(lib.sr_center_force_global(ns, n_total, npar, _ptr(O), O.shape[1], _ptr(weights), _ptr(e_loc),
-                                      _ptr(mean_O), _ptr(energy), _ptr(e_tilde), _ptr(F_partial),
+                                      rows.shape[0], _ptr(rows), _ptr(energy), _ptr(e_tilde), _ptr(F_partial),
                                       *_ws_args(ws), _stream(O.device)), "sr_center_force_global")
 
 

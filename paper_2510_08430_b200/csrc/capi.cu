@@ -26,9 +26,9 @@ sr_status center_force_impl(long long, long long, double*, long long, const doub
                             double*, double*, void*, size_t, cudaStream_t);
 size_t aHv_ws(long long, long long);
 sr_status column_moments_impl(long long, long long, long long, const double*, long long, const double*, const double*,
-                              double*, double*, void*, size_t, cudaStream_t);
+                              double*, void*, size_t, cudaStream_t);
 sr_status center_force_global_impl(long long, long long, long long, double*, long long, const double*,
-                                   const double*, const double*, const double*, double*, double*, void*, size_t,
+                                   const double*, int, const double*, double*, double*, double*, void*, size_t,
                                    cudaStream_t);
 sr_status aHv_impl(long long, long long, const double2*, long long, const double2*, double, double2*, void*,
                    size_t, cudaStream_t);
@@ -240,23 +240,23 @@ SR_API size_t sr_column_moments_workspace_bytes(int64_t n_local, int64_t n_p) {
 }
 
 SR_API sr_status sr_column_moments(int64_t n_local, int64_t n_total, int64_t n_p, const double* O, int64_t ldo,
-                                   const double* weights, const double* e_loc, double* wsum_O, double* wsum_E,
-                                   void* workspace, size_t workspace_bytes, void* stream) {
+                                   const double* weights, const double* e_loc, double* moments, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
   SR_CHECK_ARG(n_local >= 1 && n_total >= n_local && n_p >= 1, "bad sizes");
   SR_CHECK_ARG(ldo >= n_p, "ldo < n_p");
-  SR_CHECK_ARG(O && e_loc && wsum_O && wsum_E && workspace, "null pointer");
-  return column_moments_impl(n_local, n_total, n_p, O, ldo, weights, e_loc, wsum_O, wsum_E, workspace,
-                             workspace_bytes, (cudaStream_t)stream);
+  SR_CHECK_ARG(O && e_loc && moments && workspace, "null pointer");
+  return column_moments_impl(n_local, n_total, n_p, O, ldo, weights, e_loc, moments, workspace, workspace_bytes,
+                             (cudaStream_t)stream);
 }
 
 SR_API sr_status sr_center_force_global(int64_t n_local, int64_t n_total, int64_t n_p, double* O, int64_t ldo,
-                                        const double* weights, const double* e_loc, const double* mean_O,
-                                        const double* energy, double* e_tilde, double* F_partial,
+                                        const double* weights, const double* e_loc, int n_parts,
+                                        const double* moments, double* energy, double* e_tilde, double* F_partial,
                                         void* workspace, size_t workspace_bytes, void* stream) {
-  SR_CHECK_ARG(n_local >= 1 && n_total >= n_local && n_p >= 1, "bad sizes");
+  SR_CHECK_ARG(n_local >= 1 && n_total >= n_local && n_p >= 1 && n_parts >= 1, "bad sizes");
   SR_CHECK_ARG(ldo >= n_p, "ldo < n_p");
-  SR_CHECK_ARG(O && e_loc && mean_O && energy && e_tilde && F_partial && workspace, "null pointer");
-  return center_force_global_impl(n_local, n_total, n_p, O, ldo, weights, e_loc, mean_O, energy, e_tilde,
+  SR_CHECK_ARG(O && e_loc && moments && e_tilde && F_partial && workspace, "null pointer");
+  return center_force_global_impl(n_local, n_total, n_p, O, ldo, weights, e_loc, n_parts, moments, energy, e_tilde,
                                   F_partial, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 

@@ -118,27 +118,45 @@ __device__ __forceinline__ double2 cexp(double2 z) {
   return make_double2(e * c, e * s);
 }
 
-// lncosh(z) on the principal branch (reading R2), overflow-free:
-// for Re z >= 0, cosh z = e^z (1 + e^{-2z}) / 2, so
-// log cosh z = z - ln 2 + log(1 + e^{-2z}), then the imaginary part is wrapped into
-// (-pi, pi].  cosh is even, so Re z < 0 uses -z.
+// log(1 + w) on the principal branch: log|1+w| = log1p(2 Re w + |w|^2)/2, arg = atan2(Im w, 1 + Re w).
+__device__ __forceinline__ double2 clog1p(double2 w) {
+  return make_double2(0.5 * log1p(2.0 * w.x + w.x * w.x + w.y * w.y), atan2(w.y, 1.0 + w.x));
+}
+
+// lncosh(z) on the principal branch (reading R2).  |Re z| < 20: through
+// cosh z = 1 + 2 sinh^2(z/2), i.e. log1p(2 sinh^2(z/2)), which keeps full relative accuracy
+// for small activations (h ~ z^2/2); otherwise cosh z = e^z (1 + e^{-2z}) / 2 (Re z >= 0,
+// cosh even) with the imaginary part wrapped into (-pi, pi].
 __device__ __forceinline__ double2 lncosh(double2 z) {
+  if (fabs(z.x) < 20.0) {
+    double sa, ca, sb, cb;
+    sincos(0.5 * z.y, &sb, &cb);
+    sa = sinh(0.5 * z.x);
+    ca = cosh(0.5 * z.x);
+    const double sr = sa * cb, si = ca * sb;   // sinh(z/2)
+    return clog1p(make_double2(2.0 * (sr - si) * (sr + si), 4.0 * sr * si));
+  }
   if (z.x < 0.0) z = make_double2(-z.x, -z.y);
-  double2 u = cexp(make_double2(-2.0 * z.x, -2.0 * z.y));  // |u| <= 1
-  // log|1+u| = 0.5*log1p(2 u_r + |u|^2), arg(1+u) = atan2(u_i, 1+u_r)
-  double lr = 0.5 * log1p(2.0 * u.x + u.x * u.x + u.y * u.y);
-  double li = atan2(u.y, 1.0 + u.x);
-  double re = z.x - 0.69314718055994530942 + lr;
-  double im = z.y + li;
+  double2 u = cexp(make_double2(-2.0 * z.x, -2.0 * z.y));  // |u| <= e^-40
+  const double2 l = clog1p(u);
+  double re = z.x - 0.69314718055994530942 + l.x;
+  double im = z.y + l.y;
   const double pi = 3.14159265358979323846, two_pi = 6.28318530717958647692;
   if (im > pi || im <= -pi) im -= two_pi * floor((im + pi) / two_pi);
   if (im <= -pi) im += two_pi;
   return make_double2(re, im);
 }
 
-// tanh(z) = d lncosh / dz, overflow-free: (1 - e^{-2z}) / (1 + e^{-2z}) for Re z >= 0.
+// tanh(z) = d lncosh / dz.  |Re z| < 20: (sinh 2a + i sin 2b) / (cosh 2a + cos 2b) (accurate
+// for small z); otherwise (1 - e^{-2z}) / (1 + e^{-2z}) for Re z >= 0 (tanh odd).
 __device__ __forceinline__ double2 ctanh(double2 z) {
-  bool neg = z.x < 0.0;
+  if (fabs(z.x) < 20.0) {
+    double s2b, c2b;
+    sincos(2.0 * z.y, &s2b, &c2b);
+    const double d = cosh(2.0 * z.x) + c2b;
+    return make_double2(sinh(2.0 * z.x) / d, s2b / d);
+  }
+  const bool neg = z.x < 0.0;
   if (neg) z = make_double2(-z.x, -z.y);
   double2 u = cexp(make_double2(-2.0 * z.x, -2.0 * z.y));
   double2 t = cdiv(make_double2(1.0 - u.x, -u.y), make_double2(1.0 + u.x, u.y));

@@ -218,9 +218,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks<FL>()) tile_kernel(const 
         double2 v = make_double2(acc_r[mi][ni][h], acc_i[mi][ni][h]);
         double2* c = P.C + (long long)m * P.ldc + n;
         if (EP == HERM_STORE) {
+          // lower entries only (m >= n within diagonal tiles), mirrored: the stored matrix
+          // is exactly Hermitian with a real diagonal
+          if (I == J && m < n) continue;
           if (m == n) v.y = 0.0;
           *c = v;
-          if (I != J) P.C[(long long)n * P.ldc + m] = cconj(v);
+          if (m != n) P.C[(long long)n * P.ldc + m] = cconj(v);
         } else if (EP == SUB) {
           *c = csub(*c, v);
         } else {

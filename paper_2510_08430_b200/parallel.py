@@ -1,0 +1,178 @@
+"""Step orchestration on one GPU and sample-sharded over ranks (torch.distributed plumbing).
+
+BASELINE.json north_star: "samples shard naturally, so each GPU builds partial blocks from
+its N_s/G rows.  An NCCL reduce over NVLink sends each layer block to an owner GPU,
+owners run their block solves in parallel, and dtheta is all-gathered."
+
+ShardedStep, rank r of G, owning samples [r*N_s/G, (r+1)*N_s/G):
+  1. sr_jacobian, sr_local_energy on the local rows                       (no exchange)
+  2. sr_column_moments -> all_gather of the double-double moment rows     (2 n_p + 2 complex)
+  3. sr_center_force_global sums the rows (double-double), centres -> all_reduce(SUM) of F
+  4. sr_block_qgt on the local rows (partial S_b = A_b,local^H A_b,local),
+     reduce(SUM, dst=owner(b)) per block, owner(b) = b mod G
+  5. owners: sr_block_solve of their blocks; dtheta all_reduce(SUM) (non-owners hold 0)
+The arithmetic is the C ABI's; this module only moves buffers.  `ops` is injectable so
+the collective pattern can be exercised on CPU with gloo (tests/test_parallel_gloo.py).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib as sr
+
+STAGES = ("jacobian", "local_energy", "center_force", "block_qgt", "block_solve")
+
+
+class CudaOps:
+    """The C-ABI stage calls with one shared, preallocated workspace."""
+
+    def __init__(self, widths, n_local, n_bonds, device):
+        lib = sr.load()
+        L, wa = sr._widths(widths)
+        n_p = sr.n_params(widths)
+        offs = sr.block_offsets(widths)
+        need = max(
+            lib.sr_jacobian_workspace_bytes(L, wa, n_local),
+            lib.sr_local_energy_workspace_bytes(L, wa, n_local, n_bonds),
+            lib.sr_center_force_workspace_bytes(n_local, n_p),
+            lib.sr_block_solve_workspace_bytes(len(offs) - 1, sr._offsets(offs)),
+        )
+        self.ws = torch.empty(int(need), dtype=torch.uint8, device=device)
+
+    def jacobian(self, widths, theta, spins, log_psi, O):
+        sr.sr_jacobian(widths, theta, spins, log_psi, O, workspace=self.ws)
+
+    def local_energy(self, widths, theta, bij, bj, spins, log_psi, e_loc):
+        sr.sr_local_energy(widths, theta, bij, bj, spins, log_psi, e_loc, workspace=self.ws)
+
+    def center_force(self, O, e_loc, energy, e_tilde, F):
+        sr.sr_center_force(O, e_loc, energy, e_tilde, F, workspace=self.ws)
+
+    def column_moments(self, O, e_loc, n_total, moments):
+        sr.sr_column_moments(O, e_loc, n_total, moments, workspace=self.ws)
+
+    def center_force_global(self, O, e_loc, n_total, moments_all, energy, e_tilde, F_partial):
+        sr.sr_center_force_global(O, e_loc, n_total, moments_all, e_tilde, F_partial, energy=energy,
+                                  workspace=self.ws)
+
+    def block_qgt(self, A, offs, S):
+        sr.sr_block_qgt(A, offs, S)
+
+    def block_solve(self, offs, S, F, lam, dtheta, info=None):
+        sr.sr_block_solve(offs, S, F, lam, dtheta, info=info, workspace=self.ws)
+
+
+def shard_range(n, rank, world):
+    """Contiguous, balanced split of n rows over world ranks."""
+    base, rem = divmod(n, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def block_owner(b, world):
+    return b % world
+
+
+class _Buffers:
+    def __init__(self, widths, spins, bij, bj, device):
+        c = torch.complex128
+        self.widths = list(widths)
+        self.n_p = sr.n_params(widths)
+        self.offs = sr.block_offsets(widths)
+        ns = spins.shape[0]
+        self.spins = torch.as_tensor(np.ascontiguousarray(spins)).to(device)
+        self.bij = torch.as_tensor(np.ascontiguousarray(bij, dtype=np.int32)).to(device)
+        self.bj = torch.as_tensor(np.ascontiguousarray(bj, dtype=np.float64)).to(device)
+        self.log_psi = torch.empty(ns, dtype=c, device=device)
+        self.O = torch.empty(ns, self.n_p, dtype=c, device=device)
+        self.e_loc = torch.empty(ns, dtype=c, device=device)
+        self.energy = torch.empty(1, dtype=c, device=device)
+        self.e_tilde = torch.empty(ns, dtype=c, device=device)
+        self.F = torch.empty(self.n_p, dtype=c, device=device)
+        n_s = sum((self.offs[b + 1] - self.offs[b]) ** 2 for b in range(len(self.offs) - 1))
+        self.S = torch.empty(n_s, dtype=c, device=device)
+        self.dtheta = torch.empty(self.n_p, dtype=c, device=device)
+
+    def s_block(self, b):
+        pos = sum((self.offs[c + 1] - self.offs[c]) ** 2 for c in range(b))
+        n = self.offs[b + 1] - self.offs[b]
+        return self.S[pos:pos + n * n]
+
+
+def _rec(events, i, stream):
+    if events is not None:
+        events[i].record(stream)
+
+
+class LocalStep:
+    """The whole step on one GPU, stage by stage through the C ABI."""
+
+    STAGES = STAGES
+
+    def __init__(self, widths, spins, bij, bj, lam, device, ops=None):
+        self.lam = lam
+        self.device = torch.device(device)
+        self.buf = _Buffers(widths, spins, bij, bj, self.device)
+        self.ops = ops or CudaOps(widths, spins.shape[0], len(bj), self.device)
+
+    def run(self, theta, events=None):
+        b, o = self.buf, self.ops
+        st = torch.cuda.current_stream(self.device) if self.device.type == "cuda" else None
+        _rec(events, 0, st)
+        o.jacobian(b.widths, theta, b.spins, b.log_psi, b.O)
+        _rec(events, 1, st)
+        o.local_energy(b.widths, theta, b.bij, b.bj, b.spins, b.log_psi, b.e_loc)
+        _rec(events, 2, st)
+        o.center_force(b.O, b.e_loc, b.energy, b.e_tilde, b.F)
+        _rec(events, 3, st)
+        o.block_qgt(b.O, b.offs, b.S)
+        _rec(events, 4, st)
+        o.block_solve(b.offs, b.S, b.F, self.lam, b.dtheta)
+        _rec(events, 5, st)
+        return b.dtheta, b.energy
+
+
+class ShardedStep:
+    """Sample-sharded step over a torch.distributed process group (NCCL on GPUs)."""
+
+    STAGES = STAGES
+
+    def __init__(self, widths, spins_all, bij, bj, lam, rank, world, device, ops=None, group=None):
+        self.lam = lam
+        self.rank, self.world = rank, world
+        self.group = group
+        self.n_total = spins_all.shape[0]
+        lo, hi = shard_range(self.n_total, rank, world)
+        self.device = torch.device(device)
+        self.buf = _Buffers(widths, spins_all[lo:hi], bij, bj, self.device)
+        self.ops = ops or CudaOps(widths, hi - lo, len(bj), self.device)
+        self.moments = torch.empty(2 * self.buf.n_p + 2, dtype=torch.complex128, device=self.device)
+        self.moments_all = torch.empty(world, 2 * self.buf.n_p + 2, dtype=torch.complex128, device=self.device)
+        self.owned = [b for b in range(len(self.buf.offs) - 1) if block_owner(b, world) == rank]
+
+    def run(self, theta, events=None):
+        import torch.distributed as dist
+        b, o, g = self.buf, self.ops, self.group
+        st = torch.cuda.current_stream(self.device) if self.device.type == "cuda" else None
+        _rec(events, 0, st)
+        o.jacobian(b.widths, theta, b.spins, b.log_psi, b.O)
+        _rec(events, 1, st)
+        o.local_energy(b.widths, theta, b.bij, b.bj, b.spins, b.log_psi, b.e_loc)
+        _rec(events, 2, st)
+        o.column_moments(b.O, b.e_loc, self.n_total, self.moments)
+        dist.all_gather(list(self.moments_all.unbind(0)), self.moments, group=g)
+        o.center_force_global(b.O, b.e_loc, self.n_total, self.moments_all, b.energy, b.e_tilde, b.F)
+        dist.all_reduce(b.F, group=g)
+        _rec(events, 3, st)
+        o.block_qgt(b.O, b.offs, b.S)
+        for blk in range(len(b.offs) - 1):
+            dist.reduce(b.s_block(blk), dst=block_owner(blk, self.world), group=g)
+        _rec(events, 4, st)
+        b.dtheta.zero_()
+        for blk in self.owned:
+            lo, hi = b.offs[blk], b.offs[blk + 1]
+            o.block_solve([0, hi - lo], b.s_block(blk), b.F[lo:hi], self.lam, b.dtheta[lo:hi])
+        dist.all_reduce(b.dtheta, group=g)
+        _rec(events, 5, st)
+        return b.dtheta, b.energy

@@ -1,0 +1,331 @@
+"""GPU parity: every C-ABI stage against the CPU oracle on the same seeded inputs.
+
+Tolerances: BASELINE.json north_star fixes relative L2 1e-9 on
+dtheta and F and 1e-11 on S_b entries (FP64 throughout); the other intermediates (O,
+log psi, E_loc, A) are compared at 1e-11 / 1e-10, well above the ~1e-15 rounding of
+FP64 sums of at most a few thousand terms.
+"""
+import numpy as np
+import pytest
+import torch
+
+import workloads
+from oracle import estimators, hamiltonian, network, solvers
+
+pytestmark = pytest.mark.gpu
+
+C128 = torch.complex128
+
+
+@pytest.fixture(scope="module")
+def sr():
+    import paper_2510_08430_b200 as pkg
+    pkg.load()
+    return pkg
+
+
+def dev():
+    return torch.device("cuda:0")
+
+
+def T(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dev())
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def packed_blocks(S, offs):
+    out, pos = [], 0
+    for b in range(len(offs) - 1):
+        n = offs[b + 1] - offs[b]
+        out.append(S[pos:pos + n * n].reshape(n, n))
+        pos += n * n
+    return out
+
+
+SMALL_NETS = [
+    ("cfg0_full", workloads.CONFIGS[0], 512),
+    ("cfg0_ragged", workloads.CONFIGS[0], 37),
+    ("cfg1_sub", workloads.CONFIGS[1], 48),
+    ("wide256", workloads.Workload("wide", "square", (4, 4), 1.0, 0.5, (16, 256), 9), 9),
+    ("rb16", workloads.Workload("rb16", "chain", (12,), 1.0, 0.0, (12, 200, 24), 21), 21),
+    ("one_sample", workloads.CONFIGS[0], 1),
+    ("deep16", workloads.Workload("deep", "chain", (6,), 1.0, 0.0, (6,) + (5,) * 16, 19), 19),
+    ("tile64", workloads.Workload("t64", "chain", (8,), 1.0, 0.0, (8, 7, 8), 70), 70),
+]
+
+
+def _run_jac(sr, w, ns):
+    spins, params = workloads.make_inputs(w, ns)
+    theta = T(sr.model.pack(params))
+    lp = torch.empty(ns, dtype=C128, device=dev())
+    O = torch.empty(ns, w.n_params, dtype=C128, device=dev())
+    sr.sr_jacobian(w.widths, theta, T(spins), lp, O)
+    return spins, params, theta, lp, O
+
+
+@pytest.mark.parametrize("name,w,ns", SMALL_NETS, ids=[c[0] for c in SMALL_NETS])
+def test_jacobian_parity(sr, name, w, ns):
+    spins, params, _, lp, O = _run_jac(sr, w, ns)
+    lp_ref = network.log_psi(params, spins)
+    O_ref = network.jacobian(params, spins)
+    # ln psi is defined modulo 2 pi i: compare psi itself
+    assert rel(np.exp(lp.cpu().numpy()), np.exp(lp_ref)) < 1e-12
+    assert rel(O.cpu().numpy(), O_ref) < 1e-11
+
+
+@pytest.mark.parametrize("name,w,ns", SMALL_NETS[:5] + [
+    ("j1j2_6x6_sub", workloads.CONFIGS[2].with_samples(6), 6),
+    ("j1j2_10x10_sub", workloads.CONFIGS[3].with_samples(3), 3),
+], ids=[c[0] for c in SMALL_NETS[:5]] + ["j1j2_6x6_sub", "j1j2_10x10_sub"])
+def test_local_energy_parity(sr, name, w, ns):
+    spins, params, theta, lp, _ = _run_jac(sr, w, ns)
+    ij, jj = sr.lattice.for_workload(w)
+    e = torch.empty(ns, dtype=C128, device=dev())
+    sr.sr_local_energy(w.widths, theta, T(ij), T(jj), T(spins), lp, e)
+    ref = hamiltonian.local_energies(params, spins, hamiltonian.bonds_for(w))
+    assert rel(e.cpu().numpy(), ref) < 1e-10
+
+
+def test_local_energy_no_bonds_is_zero(sr):
+    w = workloads.CONFIGS[0]
+    spins, params, theta, lp, _ = _run_jac(sr, w, 16)
+    e = torch.full((16,), 7.0, dtype=C128, device=dev())
+    sr.sr_local_energy(w.widths, theta, torch.zeros(0, 2, dtype=torch.int32, device=dev()),
+                       torch.zeros(0, dtype=torch.float64, device=dev()), T(spins), lp, e)
+    assert torch.all(e == 0)
+
+
+@pytest.mark.parametrize("ns,weighted", [(512, False), (37, False), (1, False), (252, True)])
+def test_center_force_parity(sr, ns, weighted):
+    rng = np.random.default_rng(ns)
+    n_p = 300
+    O = rng.standard_normal((ns, n_p)) + 1j * rng.standard_normal((ns, n_p))
+    e = rng.standard_normal(ns) + 1j * rng.standard_normal(ns)
+    w = None
+    if weighted:
+        w = rng.random(ns)
+        w /= w.sum()
+    Od = T(O)
+    energy = torch.empty(1, dtype=C128, device=dev())
+    et = torch.empty(ns, dtype=C128, device=dev())
+    F = torch.empty(n_p, dtype=C128, device=dev())
+    sr.sr_center_force(Od, T(e), energy, et, F, weights=None if w is None else T(w))
+    A_ref, e_ref = estimators.scaled_centered(O, e, w)
+    F_ref = estimators.force(O, e, w)
+    assert abs(energy.item() - estimators.energy(e, w)) <= 1e-13 * max(1.0, abs(estimators.energy(e, w)))
+    if ns == 1:
+        assert torch.all(Od == 0) and torch.all(F == 0)
+        return
+    assert rel(Od.cpu().numpy(), A_ref) < 1e-11
+    assert rel(et.cpu().numpy(), e_ref) < 1e-11
+    assert rel(F.cpu().numpy(), F_ref) < 1e-9
+
+
+@pytest.mark.parametrize("ns,sizes", [(512, (220, 420)), (37, (64, 18, 130)), (17, (1, 65, 128)), (1, (40, 3))])
+def test_block_qgt_parity(sr, ns, sizes):
+    rng = np.random.default_rng(ns + len(sizes))
+    n_p = sum(sizes)
+    offs = [0] + list(np.cumsum(sizes))
+    O = rng.standard_normal((ns, n_p)) + 1j * rng.standard_normal((ns, n_p))
+    A, _ = estimators.scaled_centered(O, np.zeros(ns))
+    S = torch.empty(sum(n * n for n in sizes), dtype=C128, device=dev())
+    sr.sr_block_qgt(T(A), offs, S)
+    got = packed_blocks(S.cpu().numpy(), offs)
+    ref = estimators.qgt_blocks(O, offs)
+    for g, r in zip(got, ref):
+        if np.linalg.norm(r) == 0:
+            assert np.all(g == 0)
+            continue
+        assert rel(g, r) < 1e-11
+        assert np.linalg.norm(g - g.conj().T) <= 1e-15 * np.linalg.norm(g)
+        assert np.all(np.diag(g).imag == 0)
+
+
+@pytest.mark.parametrize("lam", [1e-3, 1.0])
+@pytest.mark.parametrize("ns,sizes", [(512, (220, 420)), (100, (64, 18, 130)), (300, (250,))])
+def test_block_solve_parity(sr, ns, sizes, lam):
+    rng = np.random.default_rng(ns)
+    n_p = sum(sizes)
+    offs = [0] + list(np.cumsum(sizes))
+    O = rng.standard_normal((ns, n_p)) + 1j * rng.standard_normal((ns, n_p))
+    e = rng.standard_normal(ns) + 1j * rng.standard_normal(ns)
+    blocks = estimators.qgt_blocks(O, offs)
+    F = estimators.force(O, e)
+    Sp = np.concatenate([b.ravel() for b in blocks])
+    d = torch.empty(n_p, dtype=C128, device=dev())
+    info = torch.full((1,), -5, dtype=torch.int32, device=dev())
+    sr.sr_block_solve(offs, T(Sp), T(F), lam, d, info=info)
+    ref = solvers.block_solve(blocks, F, offs, lam)
+    assert info.item() == 0
+    assert rel(d.cpu().numpy(), ref) < 1e-9
+
+
+def test_block_solve_reports_non_positive_pivot(sr):
+    offs = [0, 70, 75]
+    Sp = np.concatenate([np.eye(70).ravel(), -np.eye(5).ravel()]).astype(np.complex128)
+    d = torch.empty(75, dtype=C128, device=dev())
+    info = torch.zeros(1, dtype=torch.int32, device=dev())
+    sr.sr_block_solve(offs, T(Sp), T(np.ones(75, complex)), 0.0, d, info=info)
+    assert info.item() == 71       # first pivot of block 1 = global row 70, reported +1
+
+
+def test_full_and_ntk_parity(sr):
+    w = workloads.CONFIGS[0]
+    spins, params = workloads.make_inputs(w)
+    bonds = hamiltonian.bonds_for(w)
+    O = network.jacobian(params, spins)
+    e = hamiltonian.local_energies(params, spins, bonds)
+    A, et = estimators.scaled_centered(O, e)
+    F = estimators.force(O, e)
+    S_ref = estimators.qgt_full(O)
+    d_full = torch.empty(w.n_params, dtype=C128, device=dev())
+    S_out = torch.empty(w.n_params, w.n_params, dtype=C128, device=dev())
+    info = torch.zeros(1, dtype=torch.int32, device=dev())
+    sr.sr_full_qgt_solve(T(A), T(F), w.lam, d_full, S_out=S_out, info=info)
+    d_ntk = torch.empty(w.n_params, dtype=C128, device=dev())
+    T_out = torch.empty(w.n_samples, w.n_samples, dtype=C128, device=dev())
+    sr.sr_ntk_solve(T(A), T(et), w.lam, d_ntk, T_out=T_out, info=info)
+    assert info.item() == 0
+    assert rel(S_out.cpu().numpy(), S_ref) < 1e-11
+    assert rel(T_out.cpu().numpy(), estimators.ntk(O)) < 1e-11
+    ref_full = solvers.full_solve(S_ref, F, w.lam)
+    ref_ntk = solvers.ntk_solve(A, et, w.lam)
+    assert rel(d_full.cpu().numpy(), ref_full) < 1e-9
+    assert rel(d_ntk.cpu().numpy(), ref_ntk) < 1e-9
+    # push-through identity on the GPU: both comparison paths give the same update
+    assert rel(d_full.cpu().numpy(), d_ntk.cpu().numpy()) < 1e-9
+    # a single-block partition of the block solve is the full solve
+    d_one = torch.empty(w.n_params, dtype=C128, device=dev())
+    sr.sr_block_solve([0, w.n_params], S_out.reshape(-1), T(F), w.lam, d_one)
+    assert rel(d_one.cpu().numpy(), d_full.cpu().numpy()) < 1e-12
+
+
+def test_exact_enumeration_born_weights(sr):
+    """configs[0] "also checked by exact 2^10 enumeration": the whole S^z=0 sector with Born
+    weights through the GPU stages equals the exact QGT/force of the oracle."""
+    from oracle import exact
+    w = workloads.CONFIGS[0]
+    params = workloads.draw_params(w.widths, w.seed)
+    _, xs = exact.sector_configs(w.n_sites)
+    ns = len(xs)
+    bonds = hamiltonian.bonds_for(w)
+    pw = exact.born_weights(params, xs)
+    theta = T(sr.model.pack(params))
+    lp = torch.empty(ns, dtype=C128, device=dev())
+    O = torch.empty(ns, w.n_params, dtype=C128, device=dev())
+    sr.sr_jacobian(w.widths, theta, T(xs), lp, O)
+    ij, jj = sr.lattice.for_workload(w)
+    e = torch.empty(ns, dtype=C128, device=dev())
+    sr.sr_local_energy(w.widths, theta, T(ij), T(jj), T(xs), lp, e)
+    energy = torch.empty(1, dtype=C128, device=dev())
+    et = torch.empty(ns, dtype=C128, device=dev())
+    F = torch.empty(w.n_params, dtype=C128, device=dev())
+    sr.sr_center_force(O, e, energy, et, F, weights=T(pw))
+    offs = sr.block_offsets(w.widths)
+    S = torch.empty(sum((offs[b + 1] - offs[b]) ** 2 for b in range(len(offs) - 1)), dtype=C128, device=dev())
+    sr.sr_block_qgt(O, offs, S)
+    O_ref = network.jacobian(params, xs)
+    e_ref = hamiltonian.local_energies(params, xs, bonds)
+    assert abs(energy.item() - exact.exact_energy(params, w.n_sites, bonds)) < 1e-12
+    assert rel(F.cpu().numpy(), estimators.force(O_ref, e_ref, pw)) < 1e-9
+    for g, r in zip(packed_blocks(S.cpu().numpy(), offs), estimators.qgt_blocks(O_ref, offs, pw)):
+        assert rel(g, r) < 1e-11
+
+
+def _oracle_step(w, spins, params):
+    bonds = hamiltonian.bonds_for(w)
+    O = network.jacobian(params, spins)
+    e = hamiltonian.local_energies(params, spins, bonds)
+    off = network.layer_offsets(params)
+    blocks = estimators.qgt_blocks(O, off)
+    F = estimators.force(O, e)
+    return solvers.block_solve(blocks, F, off, w.lam), estimators.energy(e), blocks
+
+
+def test_step_and_step_host(sr):
+    w = workloads.CONFIGS[0]
+    spins, params = workloads.make_inputs(w)
+    ij, jj = sr.lattice.for_workload(w)
+    theta_h = sr.model.pack(params)
+    nb = len(jj)
+    ws = torch.empty(sr.sr_step_workspace_bytes(w.widths, w.n_samples, nb)
+                     + sr.sr_step_host_extra_bytes(w.widths, w.n_samples, nb), dtype=torch.uint8, device=dev())
+    d = torch.empty(w.n_params, dtype=C128, device=dev())
+    en = torch.empty(1, dtype=C128, device=dev())
+    sr.sr_step(w.widths, T(theta_h), T(spins), T(ij), T(jj), w.lam, d, en, ws)
+    ref, e_ref, blocks = _oracle_step(w, spins, params)
+    assert rel(d.cpu().numpy(), ref) < 1e-9
+    assert abs(en.item() - e_ref) < 1e-12 * abs(e_ref)
+    # S blocks left in the workspace match the oracle
+    off = sr.sr_step_s_offset(w.widths, w.n_samples, nb)
+    n_s = sum(b.size for b in blocks)
+    S = ws[off:off + 16 * n_s].view(C128).cpu().numpy()
+    for g, r in zip(packed_blocks(S, sr.block_offsets(w.widths)), blocks):
+        assert rel(g, r) < 1e-11
+    # host-buffer entry point: same kernels, same order -> bit-identical result
+    dh = torch.empty(w.n_params, dtype=C128).pin_memory()
+    eh = torch.empty(1, dtype=C128).pin_memory()
+    sr.sr_step_host(w.widths, torch.from_numpy(theta_h).pin_memory(), torch.from_numpy(spins).pin_memory(),
+                    torch.from_numpy(ij), torch.from_numpy(jj), w.lam, dh, eh, ws)
+    assert torch.equal(dh, d.cpu()) and torch.equal(eh, en.cpu())
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_full_size_config(sr, cfg):
+    """BASELINE.json configs[1] (the bench workload) and configs[2] at full size in the bench's
+    launch configuration (parallel.LocalStep): sampled outputs against the oracle, the rest
+    through properties that hold at any size."""
+    from paper_2510_08430_b200 import parallel
+    w = workloads.CONFIGS[cfg]
+    spins, params = workloads.make_inputs(w)
+    ij, jj = sr.lattice.for_workload(w)
+    step = parallel.LocalStep(w.widths, spins, ij, jj, w.lam, dev())
+    theta = T(sr.model.pack(params))
+    d1, en = step.run(theta)
+    d1 = d1.clone()
+    d2, _ = step.run(theta)
+    assert torch.equal(d1, d2)                              # deterministic reductions
+    b = step.buf
+    rng = np.random.default_rng(cfg)
+    ks = rng.choice(w.n_samples, 4, replace=False)
+    bonds = hamiltonian.bonds_for(w)
+    # stage (1): sampled rows of O (the buffer now holds A = sqrt(w)(O - <O>); check log psi
+    # and E_loc directly, and O through A + the mean on sampled columns below)
+    lp = b.log_psi.cpu().numpy()
+    for k in ks:
+        assert abs(np.exp(lp[k]) - np.exp(network.forward(params, spins[k])[0])) < 1e-12
+    el = b.e_loc.cpu().numpy()
+    el_ref = hamiltonian.local_energies(params, spins[ks], bonds)
+    assert rel(el[ks], el_ref) < 1e-10
+    # stage (4): sampled S entries from oracle-built centred columns
+    offs = b.offs
+    cols = np.sort(np.concatenate([rng.choice(np.arange(offs[i], offs[i + 1]), 6, replace=False)
+                                   for i in range(len(offs) - 1)]))
+    O_cols = np.stack([network.log_derivative_row(params, x)[cols] for x in spins])
+    A_cols, _ = estimators.scaled_centered(O_cols, np.zeros(w.n_samples))
+    A_gpu = b.O[:, torch.as_tensor(cols, device=dev())].cpu().numpy()
+    assert rel(A_gpu, A_cols) < 1e-11
+    blocks = [blk.reshape(offs[i + 1] - offs[i], -1) for i, blk in
+              enumerate(b.s_block(i) for i in range(len(offs) - 1))]
+    for i in range(len(offs) - 1):
+        sel = [c for c in range(len(cols)) if offs[i] <= cols[c] < offs[i + 1]]
+        loc = cols[sel] - offs[i]
+        got = blocks[i][torch.as_tensor(loc, device=dev())][:, torch.as_tensor(loc, device=dev())].cpu().numpy()
+        ref = estimators.qgt_full(O_cols[:, sel])
+        assert rel(got, ref) < 1e-11
+        Sb = blocks[i]
+        assert torch.equal(Sb, Sb.conj().T.resolve_conj())   # exactly Hermitian as stored
+    # F = A^H e_tilde and the solve residual (S_b + lambda) dtheta_b = -F_b, checked with
+    # cuBLAS as an independent instrument on the GPU buffers
+    Fchk = b.O.conj().T @ b.e_tilde
+    assert rel(b.F.cpu().numpy(), Fchk.cpu().numpy()) < 1e-10
+    for i in range(len(offs) - 1):
+        lo, hi = offs[i], offs[i + 1]
+        Sb = blocks[i]
+        r = Sb @ d1[lo:hi] + w.lam * d1[lo:hi] + b.F[lo:hi]
+        assert (torch.linalg.vector_norm(r) / torch.linalg.vector_norm(b.F[lo:hi])).item() < 1e-9
+    assert abs(en.item() - el.mean()) < 1e-12 * abs(el.mean())

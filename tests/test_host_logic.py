@@ -1,0 +1,47 @@
+"""Host-side set-up of the product path against the oracle's independent versions."""
+import numpy as np
+
+import workloads
+from oracle import hamiltonian, network
+
+
+def test_lattice_bonds_match_oracle():
+    import paper_2510_08430_b200 as sr
+    for w in workloads.CONFIGS:
+        ij, jj = sr.lattice.for_workload(w)
+        mine = {(min(i, j), max(i, j), J) for (i, j), J in zip(ij.tolist(), jj.tolist())}
+        ref = {(min(i, j), max(i, j), J) for i, j, J in hamiltonian.bonds_for(w)}
+        assert mine == ref and len(ij) == len(ref)
+    ij, jj = sr.lattice.bond_arrays(sr.lattice.chain(4), spin_units=True)
+    assert np.all(jj == 0.25)
+
+
+def test_parameter_packing_matches_oracle_order():
+    import paper_2510_08430_b200 as sr
+    params = workloads.draw_params((10, 20, 20), seed=4)
+    assert np.array_equal(sr.model.pack(params), network.flatten(params))
+    assert sr.model.widths_of(params) == [10, 20, 20]
+    assert sr.block_offsets([10, 20, 20]) == network.layer_offsets(params)
+    assert sr.n_params([100] + [128] * 6) == 95488
+
+
+def test_shard_ranges_and_owners():
+    from paper_2510_08430_b200.parallel import block_owner, shard_range
+    for n in (1, 7, 4096, 65536):
+        for g in (1, 2, 3, 8):
+            rs = [shard_range(n, r, g) for r in range(g)]
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(g - 1))
+            sizes = [b - a for a, b in rs]
+            assert max(sizes) - min(sizes) <= 1
+    assert [block_owner(b, 8) for b in range(8)] == list(range(8))    # configs[4]: one block per GPU
+
+
+def test_workload_inputs_are_seeded_and_in_sector():
+    s1 = workloads.draw_spins(36, 100, 3)
+    s2 = workloads.draw_spins(36, 100, 3)
+    assert np.array_equal(s1, s2)
+    assert np.all(s1.sum(axis=1) == 0) and set(np.unique(s1)) == {-1, 1}
+    p = workloads.draw_params((100, 128), 0)
+    sd = 0.1 / np.sqrt(100)
+    assert abs(p[0][0].real.std() / sd - 1) < 0.05 and abs(p[0][0].imag.std() / sd - 1) < 0.05

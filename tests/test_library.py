@@ -1,0 +1,79 @@
+"""CPU checks of the C ABI boundary: libsrblock.so builds, loads, exports every symbol
+include/sr_block.h declares, and the binding covers exactly those symbols.  No compute
+call is made (there is no GPU here); only the pure-host queries run."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "sr_block.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"SR_API\s+[\w\s\*]+?\b(sr_\w+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import paper_2510_08430_b200 as sr
+    return sr.load()
+
+
+def test_header_declares_the_north_star_entry_points():
+    names = declared_symbols()
+    for n in ("sr_jacobian", "sr_local_energy", "sr_block_qgt", "sr_block_solve", "sr_full_qgt_solve",
+              "sr_ntk_solve", "sr_center_force", "sr_step", "sr_step_host"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+
+
+def test_binding_covers_the_header():
+    from paper_2510_08430_b200 import _lib
+    assert sorted(_lib.SIGNATURES) == declared_symbols()
+
+
+def test_library_is_sm100a_only():
+    import paper_2510_08430_b200 as sr
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump -lelf {sr.LIB_PATH}").read()
+    assert "sm_100a" in out and "sm_90" not in out
+
+
+def test_host_queries(lib):
+    import paper_2510_08430_b200 as sr
+    assert lib.sr_version() == 100
+    w = [40, 80, 80, 80]
+    small = sr.sr_step_workspace_bytes(w, 512, 40)
+    big = sr.sr_step_workspace_bytes(w, 4096, 40)
+    assert 0 < small < big
+    # O alone is N_s * n_p complex numbers
+    assert big >= 4096 * 16240 * 16
+    L, wa = sr._lib._widths(w)
+    assert lib.sr_jacobian_workspace_bytes(L, wa, 4096) > 0
+    assert lib.sr_block_solve_workspace_bytes(3, sr._lib._offsets(sr.block_offsets(w))) > 0
+    # invalid widths are rejected by the queries (0 bytes) without touching a device
+    bad, wb = sr._lib._widths([40, 300])
+    assert lib.sr_jacobian_workspace_bytes(bad, wb, 10) == 0
+
+
+def test_invalid_arguments_fail_before_any_device_work(lib):
+    import paper_2510_08430_b200 as sr
+    L, wa = sr._lib._widths([4, 300])
+    rc = lib.sr_jacobian(L, wa, None, None, 1, None, None, 10, None, 0, None)
+    assert rc == -1 and b"width" in lib.sr_last_error()
+    rc = lib.sr_block_solve(0, None, None, None, 1e-3, None, None, None, 0, None)
+    assert rc == -1
+
+
+def test_missing_library_fails_loudly(tmp_path, monkeypatch):
+    from paper_2510_08430_b200 import _lib
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "missing.so"))
+    with pytest.raises(_lib.SRError):
+        _lib.load(build_if_missing=False)

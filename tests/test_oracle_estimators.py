@@ -101,3 +101,23 @@ def test_scaled_centered_factorisation():
     np.testing.assert_allclose(A.conj().T @ A, estimators.qgt_full(O, w), rtol=1e-12, atol=1e-15)
     np.testing.assert_allclose(A.conj().T @ ev, estimators.force(O, e, w), rtol=1e-12, atol=1e-15)
     np.testing.assert_allclose(A @ A.conj().T, estimators.ntk(O, w), rtol=1e-12, atol=1e-15)
+
+
+def test_centering_is_exact_to_double_rounding_under_cancellation():
+    # columns nearly constant over samples (as the last-layer bias derivatives are): the
+    # centred values must equal the exactly computed (rational-arithmetic) ones up to one
+    # double rounding plus the longdouble rounding of the mean (2^-63 |<O>|), i.e. ~1e-13
+    # relative here, where a double-rounded mean would give ~1e-9
+    from fractions import Fraction
+    rng = np.random.default_rng(8)
+    base = 0.731 - 0.25j
+    O = base + 1e-7 * (rng.standard_normal((33, 2)) + 1j * rng.standard_normal((33, 2)))
+    ob = estimators.center(O)
+    for c in range(2):
+        for part in ("real", "imag"):
+            col = [Fraction(float(getattr(v, part))) for v in O[:, c]]
+            mean = sum(col) / len(col)
+            exact = [float(v - mean) for v in col]
+            got = getattr(ob[:, c], part)
+            bound = 2.0 ** -52 * np.abs(exact) + 2.0 ** -62 * abs(getattr(base, part))
+            assert np.all(np.abs(got - exact) <= bound)

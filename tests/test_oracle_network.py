@@ -13,6 +13,25 @@ def test_lncosh_closed_forms():
     np.testing.assert_allclose(network.lncosh(0.7 + 0j), np.log((np.exp(0.7) + np.exp(-0.7)) / 2), rtol=1e-15)
 
 
+def test_lncosh_small_argument_series_and_branch():
+    # log cosh z = z^2/2 - z^4/12 + z^6/45 - ...: full relative accuracy for small z
+    for z in (1e-8 + 3e-9j, 0.003 + 0.002j, -0.02 + 0.01j):
+        series = z ** 2 / 2 - z ** 4 / 12 + z ** 6 / 45 - 17 * z ** 8 / 2520
+        assert abs(network.lncosh(z) - series) <= 4e-16 * abs(series)
+    # moderate z: agrees with the literal definition; principal branch (|Im| <= pi)
+    rng = np.random.default_rng(1)
+    z = rng.normal(0, 2, 50) + 1j * rng.normal(0, 2, 50)
+    np.testing.assert_allclose(network.lncosh(z), np.log(np.cosh(z)), rtol=1e-12, atol=1e-14)
+    assert np.all(np.abs(network.lncosh(z).imag) <= np.pi)
+    # d lncosh / dz = tanh z (central difference), tanh accurate at small z
+    h = 1e-6
+    for z0 in (0.3 + 0.2j, -1.1 + 0.7j):
+        fd = (network.lncosh(z0 + h) - network.lncosh(z0 - h)) / (2 * h)
+        assert abs(fd - np.tanh(z0)) < 1e-9
+    z = 0.003 + 0.002j
+    assert abs(np.tanh(z) - (z - z ** 3 / 3 + 2 * z ** 5 / 15)) <= 4e-16 * abs(z)
+
+
 def test_single_unit_closed_form():
     # ln psi = lncosh(w s + b): O_w = tanh(w s + b) s, O_b = tanh(w s + b)  (hand derivation)
     w, b = 0.3 + 0.1j, -0.2 + 0.05j
@@ -22,7 +41,7 @@ def test_single_unit_closed_form():
         t = np.tanh(w * s + b)
         np.testing.assert_allclose(row, [t * s, t], rtol=1e-15)
         lp = network.forward(params, np.array([s]))[0]
-        np.testing.assert_allclose(lp, np.log(np.cosh(w * s + b)), rtol=1e-15)
+        np.testing.assert_allclose(lp, np.log(np.cosh(w * s + b)), rtol=1e-13)   # literal form: ~eps/|z|^2
 
 
 @pytest.mark.parametrize("widths", [(10, 20, 20), (8, 6, 5, 4)])
