@@ -20,7 +20,6 @@ namespace sr {
 namespace {
 
 constexpr int NB = 64;
-constexpr int LDT = NB + 1;
 
 __global__ void chol_init(CholSet cs, double lam, int inplace) {
   const int b = blockIdx.y;
@@ -47,84 +46,93 @@ __global__ void chol_init(CholSet cs, double lam, int inplace) {
     B.rhs[r] = r < n ? B.F[r] : make_double2(0.0, 0.0);
 }
 
-// One CTA per active block.  Factors the diagonal tile of panel p in place, writes
-// Linv_p, and replaces b_p by y_p = Linv_p b_p.
+// One CTA per active block: factor the 64x64 diagonal tile of panel p, its inverse Linv_p
+// and y_p = Linv_p b_p in ONE sweep of 64 steps.  Step c works on the unscaled column c
+// (a_rc, pivot d_c = a_cc):
+//   Cholesky trailing part   T[r][s] -= a_rc conj(a_sc) / d_c        (c < s <= r)
+//   forward substitution     Y[r][j] -= a_rc Y[c][j] / d_c            (c < r, j <= c; j = 64: b)
+// with Y = [I | b] on entry; at the end L[r][c] = a_rc / sqrt(d_c), L[c][c] = sqrt(d_c),
+// Linv[r][j] = Y[r][j] / sqrt(d_r), y_r = Y[r][64] / sqrt(d_r).
+// Thread (r, q) = (t/4, t%4) keeps the 16 entries s = q + 4k of row r of T and of Y in
+// registers.  Column c of T and row c of Y are published to a double-buffered shared strip
+// by their owners at the end of step c-1 (inside the unrolled update loop, so no register
+// array is ever indexed dynamically); one barrier per step.
 __global__ void __launch_bounds__(256) chol_diag(CholSet cs, ActiveList act, int p) {
-  extern __shared__ double2 sm[];
-  double2* T = sm;              // [64][65]  factor tile
-  double2* X = sm + NB * LDT;   // [64][65]  inverse
-  __shared__ double2 yb[NB];
+  __shared__ double2 colc[2][NB];       // T[.][c]   (published column)
+  __shared__ double2 rowc[2][NB + 4];   // Y[c][.]   (published row; [NB] = rhs entry)
+  __shared__ double piv[NB];
   const CholBlock& B = cs.b[act.idx[blockIdx.x]];
   const long long np = B.npad;
   double2* tile = B.Fm + (long long)p * NB * np + (long long)p * NB;
-  const int t = threadIdx.x;
-  for (int e = t; e < NB * NB; e += 256) {
-    const int r = e >> 6, c = e & 63;
-    T[r * LDT + c] = c <= r ? tile[(long long)r * np + c] : make_double2(0.0, 0.0);
+  const int t = threadIdx.x, r = t >> 2, q = t & 3;
+  double2 tr[16], yr[16];
+  double2 rhs = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    const int s = q + 4 * k;
+    tr[k] = s <= r ? tile[(long long)r * np + s] : make_double2(0.0, 0.0);
+    yr[k] = make_double2(s == r ? 1.0 : 0.0, 0.0);
   }
-  if (t < NB) yb[t] = B.rhs[(long long)p * NB + t];
-  __syncthreads();
-  // unblocked right-looking Cholesky, lower
-  const int tr = t >> 2, tq = t & 3;
+  if (q == 0) {
+    rhs = B.rhs[(long long)p * NB + r];
+    colc[0][r] = tr[0];
+  }
+  if (r == 0) {
+#pragma unroll
+    for (int k = 0; k < 16; k++) rowc[0][q + 4 * k] = yr[k];
+    if (q == 0) rowc[0][NB] = rhs;
+  }
   for (int c = 0; c < NB; c++) {
-    __syncthreads();  // step c-1's trailing update (which wrote T[c][c]) is visible
-    double d = T[c * LDT + c].x;
+    const int buf = c & 1, nbuf = buf ^ 1;
+    __syncthreads();
+    double d = colc[buf][c].x;
     if (!(d > 0.0)) {
       if (t == 0 && cs.info) atomicCAS(cs.info, 0, (int)(B.row_base + (long long)p * NB + c + 1));
       d = 1.0;
     }
-    const double sd = sqrt(d), isd = 1.0 / sd;
-    __syncthreads();
-    if (t == 0) T[c * LDT + c] = make_double2(sd, 0.0);
-    if (t > c && t < NB) T[t * LDT + c] = cscale(T[t * LDT + c], isd);
-    __syncthreads();
-    if (tr > c) {
-      const double2 lrc = T[tr * LDT + c];
-      for (int s = c + 1 + tq; s <= tr; s += 4) {
-        const double2 lsc = T[s * LDT + c];
-        // T[r][s] -= L[r][c] conj(L[s][c])
-        double2 v = T[tr * LDT + s];
-        v.x -= lrc.x * lsc.x + lrc.y * lsc.y;
-        v.y -= lrc.y * lsc.x - lrc.x * lsc.y;
-        T[tr * LDT + s] = v;
-      }
-    }
-  }
-  __syncthreads();
-  // X = L^{-1}: column j per quad of lanes, forward substitution, quad-reduced sums.
-  {
-    const int j = t >> 2, q = t & 3;
-    for (int r = 0; r < NB; r++) {
-      double2 s = make_double2(0.0, 0.0);
-      if (r >= j)
-        for (int k = j + q; k < r; k += 4) cfma(s, T[r * LDT + k], X[k * LDT + j]);
-      s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
-      s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
-      s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
-      s.y += __shfl_xor_sync(0xffffffffu, s.y, 2);
-      if (q == 0) {
-        double2 x = make_double2(0.0, 0.0);
-        if (r >= j) {
-          const double inv = 1.0 / T[r * LDT + r].x;
-          x = make_double2(((r == j ? 1.0 : 0.0) - s.x) * inv, -s.y * inv);
+    if (t == 0) piv[c] = d;
+    if (r > c) {
+      const double inv = 1.0 / d;
+      const double2 a = colc[buf][r];
+      const double2 g = make_double2(a.x * inv, a.y * inv);   // a_rc / d_c
+#pragma unroll
+      for (int k = 0; k < 16; k++) {
+        const int s = q + 4 * k;
+        if (s > c && s <= r) {                                // T[r][s] -= g conj(a_sc)
+          const double2 bb = colc[buf][s];
+          tr[k].x -= g.x * bb.x + g.y * bb.y;
+          tr[k].y -= g.y * bb.x - g.x * bb.y;
+          if (s == c + 1) colc[nbuf][r] = tr[k];              // publish column c+1
         }
-        X[r * LDT + j] = x;
+        if (s <= c) {                                         // Y[r][s] -= g Y[c][s]
+          const double2 y = rowc[buf][s];
+          yr[k].x -= g.x * y.x - g.y * y.y;
+          yr[k].y -= g.x * y.y + g.y * y.x;
+        }
       }
-      __syncwarp();
+      if (q == 0) {
+        const double2 y = rowc[buf][NB];
+        rhs.x -= g.x * y.x - g.y * y.y;
+        rhs.y -= g.x * y.y + g.y * y.x;
+      }
+      if (r == c + 1) {                                       // publish row c+1 of Y (final now)
+#pragma unroll
+        for (int k = 0; k < 16; k++) rowc[nbuf][q + 4 * k] = yr[k];
+        if (q == 0) rowc[nbuf][NB] = rhs;
+      }
     }
   }
   __syncthreads();
   double2* linv = B.linv + (long long)p * NB * NB;
-  for (int e = t; e < NB * NB; e += 256) {
-    const int r = e >> 6, c = e & 63;
-    if (c <= r) tile[(long long)r * np + c] = T[r * LDT + c];
-    linv[e] = X[r * LDT + c];
+  const double isr = 1.0 / sqrt(piv[r]);
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    const int s = q + 4 * k;
+    if (s < r) tile[(long long)r * np + s] = cscale(tr[k], 1.0 / sqrt(piv[s]));
+    else if (s == r) tile[(long long)r * np + s] = make_double2(sqrt(piv[r]), 0.0);
+    linv[r * NB + s] = s <= r ? cscale(yr[k], isr) : make_double2(0.0, 0.0);
   }
-  if (t < NB) {
-    double2 y = make_double2(0.0, 0.0);
-    for (int c = 0; c <= t; c++) cfma(y, X[t * LDT + c], yb[c]);
-    B.rhs[(long long)p * NB + t] = y;
-  }
+  if (q == 0) B.rhs[(long long)p * NB + r] = cscale(rhs, isr);
 }
 
 // b_i -= sum_c L[i][p*64 + c] y_p[c] for rows i >= (p+1)*64 (one warp per row).
@@ -149,9 +157,12 @@ __global__ void chol_rhs_update(CholSet cs, ActiveList act, int p) {
 }
 
 // x_p = Linv_p^H y_p (into xout), then y_c -= sum_c' conj(L[p*64 + c'][c]) x_p[c'] for c < p*64.
+// Each CTA owns 64 columns; 256 threads = 64 columns x 4 row quarters, reduced in a fixed
+// order through shared memory (deterministic).
 __global__ void __launch_bounds__(256) chol_back(CholSet cs, ActiveList act, int p) {
   __shared__ double2 ys[NB];
   __shared__ double2 xs[NB];
+  __shared__ double2 red[4][NB];
   const CholBlock& B = cs.b[act.idx[blockIdx.y]];
   const long long np = B.npad;
   const int t = threadIdx.x;
@@ -159,7 +170,6 @@ __global__ void __launch_bounds__(256) chol_back(CholSet cs, ActiveList act, int
   __syncthreads();
   const double2* linv = B.linv + (long long)p * NB * NB;
   {
-    // 4 lanes per output c, rows r >= c split by r % 4
     const int c = t >> 2, q = t & 3;
     double2 s = make_double2(0.0, 0.0);
     for (int r = c + q; r < NB; r += 4) cfma_conj(s, linv[r * NB + c], ys[r]);
@@ -172,12 +182,20 @@ __global__ void __launch_bounds__(256) chol_back(CholSet cs, ActiveList act, int
   __syncthreads();
   if (blockIdx.x == 0 && t < NB) B.xout[(long long)p * NB + t] = xs[t];
   const long long ncol = (long long)p * NB;
-  for (long long c = (long long)blockIdx.x * 256 + t; c < ncol; c += (long long)gridDim.x * 256) {
+  const int cl = t & 63, rq = t >> 6;
+  for (long long c0 = (long long)blockIdx.x * NB; c0 < ncol; c0 += (long long)gridDim.x * NB) {
+    const long long c = c0 + cl;
     double2 s = make_double2(0.0, 0.0);
-    const double2* col = B.Fm + (long long)p * NB * np + c;
-#pragma unroll 8
-    for (int r = 0; r < NB; r++) cfma_conj(s, col[(long long)r * np], xs[r]);
-    B.rhs[c] = csub(B.rhs[c], s);
+    const double2* col = B.Fm + ((long long)p * NB + rq * 16) * np + c;
+#pragma unroll 4
+    for (int r = 0; r < 16; r++) cfma_conj(s, col[(long long)r * np], xs[rq * 16 + r]);
+    red[rq][cl] = s;
+    __syncthreads();
+    if (rq == 0) {
+      double2 v = cadd(cadd(red[0][cl], red[1][cl]), cadd(red[2][cl], red[3][cl]));
+      B.rhs[c] = csub(B.rhs[c], v);
+    }
+    __syncthreads();
   }
 }
 
@@ -218,12 +236,6 @@ sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStr
     chol_init<<<g, 256, 0, st>>>(cs, lam, inplace ? 1 : 0);
     SR_LAUNCHED();
   }
-  const size_t diag_smem = 2 * NB * LDT * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    SR_CUDA(cudaFuncSetAttribute(chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem));
-    attr = true;
-  }
   for (int p = 0; p < pmax; p++) {
     ActiveList act;
     act.n = 0;
@@ -233,7 +245,7 @@ sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStr
         act.idx[act.n++] = b;
         max_trail = std::max(max_trail, cs.b[b].npad - (long long)(p + 1) * NB);
       }
-    chol_diag<<<act.n, 256, diag_smem, st>>>(cs, act, p);
+    chol_diag<<<act.n, 256, 0, st>>>(cs, act, p);
     SR_LAUNCHED();
     if (max_trail <= 0) continue;
     gram::ProbSet trsm{}, trail{};
@@ -260,8 +272,7 @@ sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStr
     act.n = 0;
     for (int b = 0; b < cs.count; b++)
       if (cs.b[b].P > p) act.idx[act.n++] = b;
-    const long long ncol = (long long)p * NB;
-    dim3 g((unsigned)std::max<long long>(1, (ncol + 255) / 256), (unsigned)act.n);
+    dim3 g((unsigned)std::max(1, p), (unsigned)act.n);
     chol_back<<<g, 256, 0, st>>>(cs, act, p);
     SR_LAUNCHED();
   }

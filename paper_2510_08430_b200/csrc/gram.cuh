@@ -19,9 +19,9 @@ namespace gram {
 constexpr int BM = 64;   // tile rows   (complex)
 constexpr int BN = 64;   // tile cols   (complex)
 constexpr int BK = 16;   // K per stage (complex)
-constexpr int kStages = 3;
 constexpr int kThreads = 256;
 constexpr int kMaxProbs = 24;
+constexpr int kBand = 16;     // tile rows per rasterisation band (lower-triangle tile sets)
 
 // Operand storage flavors.
 //  TN: a(m,k) = conj(A[k*lda + m]), b(k,n) = B[k*ldb + n]   (tile smem [BK][64+2])
@@ -53,11 +53,14 @@ constexpr int TN_LD = BM + 2;   // 66 complex = 1056 B per k-row  (1056 mod 128 
 constexpr int NH_LD = BK + 4;   // 20 complex =  320 B per m-row  ( 320 mod 128 = 64)
 template <int FL>
 constexpr int tile_elems() { return FL == TN ? BK * TN_LD : BM * NH_LD; }   // 1056 / 1280
+// Pipeline depth: TN (the QGT Gram, long K) 3 stages = 101 KB; NH (Cholesky TRSM/trailing
+// update with K = 64, NTK Gram) 2 stages = 82 KB.  Both fit 2 CTAs per SM.
 template <int FL>
-constexpr size_t smem_bytes() { return (size_t)kStages * 2 * tile_elems<FL>() * sizeof(double2); }
-// TN (the QGT Gram): 101 KB -> 2 CTAs per SM; NH: 123 KB -> 1 CTA per SM.
+constexpr int stages() { return FL == TN ? 3 : 2; }
 template <int FL>
-constexpr int min_blocks() { return FL == TN ? 2 : 1; }
+constexpr size_t smem_bytes() { return (size_t)stages<FL>() * 2 * tile_elems<FL>() * sizeof(double2); }
+template <int FL>
+constexpr int min_blocks() { return 2; }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -111,11 +114,29 @@ __device__ __forceinline__ void tile_of(const ProbSet& ps, long long t, int& pi,
   while (pi + 1 < ps.count && t >= ps.p[pi + 1].tile_begin) pi++;
   const long long lt = t - ps.p[pi].tile_begin;
   if (ps.p[pi].lower) {
+    // row of lt in row-major lower-triangle order
     long long i = (long long)((sqrt(8.0 * (double)lt + 1.0) - 1.0) * 0.5);
     while ((i + 1) * (i + 2) / 2 <= lt) i++;
     while (i * (i + 1) / 2 > lt) i--;
-    I = (int)i;
-    J = (int)(lt - i * (i + 1) / 2);
+    // Band rasterisation: rows are grouped in bands of kBand tile rows and each band is
+    // walked column-major, so the CTAs resident at one time share few operand strips
+    // (L2 reuse of the K-slabs instead of whole-matrix re-reads from HBM per wave).
+    const long long T = ps.p[pi].tiles_n;
+    const long long r0 = (i / kBand) * kBand, r1 = min(T, r0 + kBand), nb = r1 - r0;
+    const long long u = lt - r0 * (r0 + 1) / 2;
+    if (u < (r0 + 1) * nb) {
+      J = (int)(u / nb);
+      I = (int)(r0 + u % nb);
+    } else {
+      long long v = u - (r0 + 1) * nb, sz = nb - 1, col = r0 + 1;
+      while (v >= sz) {
+        v -= sz;
+        sz--;
+        col++;
+      }
+      J = (int)col;
+      I = (int)(col + v);
+    }
   } else {
     I = (int)(lt / ps.p[pi].tiles_n);
     J = (int)(lt % ps.p[pi].tiles_n);
@@ -146,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<FL>()) tile_kernel(const 
     }
 
   constexpr int TE = tile_elems<FL>();
+  constexpr int kStages = stages<FL>();
   auto sA = [&](int st) { return smem + (size_t)st * 2 * TE; };
   auto sB = [&](int st) { return smem + (size_t)st * 2 * TE + TE; };
 
