@@ -141,30 +141,46 @@ def run_gpu(args):
     for _ in range(args.warmup):
         step.run(theta)
     torch.cuda.synchronize(dev)
+
+    # per-stage breakdown: eager launches with CUDA events between the C-ABI stage calls
+    n_ev = len(step.STAGES) + 1
+    n_stage_runs = max(1, min(args.steps, 3))
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(n_stage_runs)]
+    sr.sr_reset_launch_count()
+    for k in range(n_stage_runs):
+        step.run(theta, events=evs[k])
+    torch.cuda.synchronize(dev)
+    launches = sr.sr_launch_count() // n_stage_runs
+    stage_ms = {name: float(np.mean([evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(n_stage_runs)]))
+                for i, name in enumerate(step.STAGES)}
+
+    use_graph = world == 1 and not args.no_graph
+    if use_graph:
+        step.capture(theta)                  # the whole step as one CUDA graph
+        for _ in range(args.warmup):
+            step.replay()
+    torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
 
     clocks = ClockSampler(local)
     clocks.start()
-    n_ev = len(step.STAGES) + 1
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
-    sr.sr_reset_launch_count()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(stream)
     for k in range(args.steps):
-        step.run(theta, events=evs[k])
+        if use_graph:
+            step.replay()
+        else:
+            step.run(theta)
     stop.record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    launches = sr.sr_launch_count()
     clk = clocks.stop()
     total_ms = start.elapsed_time(stop)
-    stage_ms = {name: float(np.mean([evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(args.steps)]))
-                for i, name in enumerate(step.STAGES)}
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -224,7 +240,9 @@ def run_gpu(args):
                             "algorithmic": "sum_b 4 n_b^3 / 3 (ZPOTRF)"},
         },
         "stages_ms": stage_ms,
-        "gpu_launches": launches,
+        "gpu_launches": launches * args.steps,
+        "launches_per_step": launches,
+        "cuda_graph": use_graph,
         "clocks": clk,
         "e2e": e2e,
     }
@@ -349,6 +367,7 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=list(workloads.BY_NAME))
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch stage by stage instead of one CUDA graph")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -10,7 +10,9 @@
 //                    Linv_p, and y_p = Linv_p b_p (forward substitution folded in)
 //   trsm (engine)    L_ip = A_ip Linv_p^H for every row tile i > p      (DMMA, NH/STORE)
 //   chol_rhs_update  b_i -= L_ip y_p
-//   trail (engine)   A_ij -= L_ip L_jp^H for i >= j > p                  (DMMA, NH/SUB)
+//   inner (engine)   A_ij -= L_ip L_jp^H for the strip's later columns j (DMMA, NH/SUB)
+// and after every strip of 4 panels one deferred trailing update with K = 256:
+//   trail (engine)   A_ij -= L_i,strip L_j,strip^H for i >= j beyond the strip (NH/SUB)
 // then back substitution L^H x = y panel by panel (x_p = Linv_p^H y_p, then
 // y_{<p} -= L_p,<p^H x_p) and dtheta = -x.
 #include "chol.cuh"
@@ -46,93 +48,104 @@ __global__ void chol_init(CholSet cs, double lam, int inplace) {
     B.rhs[r] = r < n ? B.F[r] : make_double2(0.0, 0.0);
 }
 
-// One CTA per active block: factor the 64x64 diagonal tile of panel p, its inverse Linv_p
-// and y_p = Linv_p b_p in ONE sweep of 64 steps.  Step c works on the unscaled column c
-// (a_rc, pivot d_c = a_cc):
-//   Cholesky trailing part   T[r][s] -= a_rc conj(a_sc) / d_c        (c < s <= r)
-//   forward substitution     Y[r][j] -= a_rc Y[c][j] / d_c            (c < r, j <= c; j = 64: b)
-// with Y = [I | b] on entry; at the end L[r][c] = a_rc / sqrt(d_c), L[c][c] = sqrt(d_c),
-// Linv[r][j] = Y[r][j] / sqrt(d_r), y_r = Y[r][64] / sqrt(d_r).
-// Thread (r, q) = (t/4, t%4) keeps the 16 entries s = q + 4k of row r of T and of Y in
-// registers.  Column c of T and row c of Y are published to a double-buffered shared strip
-// by their owners at the end of step c-1 (inside the unrolled update loop, so no register
-// array is ever indexed dynamically); one barrier per step.
+// One CTA per active block: factor the 64x64 diagonal tile of panel p (left-looking), its
+// inverse X = Linv_p (row by row) and y_p = Linv_p b_p.  Step c, one barrier:
+//   d_c     = A[c][c] - sum_{k<c} |L[c][k]|^2                      (every quad, redundantly)
+//   L[r][c] = (A[r][c] - sum_{k<c} L[r][k] conj(L[c][k])) / sqrt(d_c)   rows r > c
+//   X[c][j] = -(sum_{j<=k<c} L[c][k] X[k][j]) / sqrt(d_c)               j = r < c
+//   L[c][c] = sqrt(d_c), X[c][c] = 1/sqrt(d_c)                          quad r == c
+// Quad (r, q) = (t/4, t%4) splits each dot product over k = q mod 4 and reduces with two
+// shuffles.  Everything reads only entries finalised in earlier steps.
+constexpr int LDS = NB + 4;   // 1088-byte rows: conflict-free quad access
+constexpr size_t kDiagSmem = (size_t)2 * NB * LDS * sizeof(double2);
 __global__ void __launch_bounds__(256) chol_diag(CholSet cs, ActiveList act, int p) {
-  __shared__ double2 colc[2][NB];       // T[.][c]   (published column)
-  __shared__ double2 rowc[2][NB + 4];   // Y[c][.]   (published row; [NB] = rhs entry)
-  __shared__ double piv[NB];
+  extern __shared__ double2 dsm[];
+  double2* T = dsm;              // [64][LDS]: A (lower), columns replaced by L as they finish
+  double2* X = dsm + NB * LDS;   // [64][LDS]: Linv rows
+  __shared__ double2 bsh[NB];
   const CholBlock& B = cs.b[act.idx[blockIdx.x]];
   const long long np = B.npad;
   double2* tile = B.Fm + (long long)p * NB * np + (long long)p * NB;
   const int t = threadIdx.x, r = t >> 2, q = t & 3;
-  double2 tr[16], yr[16];
-  double2 rhs = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int k = 0; k < 16; k++) {
-    const int s = q + 4 * k;
-    tr[k] = s <= r ? tile[(long long)r * np + s] : make_double2(0.0, 0.0);
-    yr[k] = make_double2(s == r ? 1.0 : 0.0, 0.0);
+  for (int e = t; e < NB * NB; e += 256) {
+    const int rr = e >> 6, c = e & 63;
+    T[rr * LDS + c] = c <= rr ? tile[(long long)rr * np + c] : make_double2(0.0, 0.0);
+    X[rr * LDS + c] = make_double2(0.0, 0.0);
   }
-  if (q == 0) {
-    rhs = B.rhs[(long long)p * NB + r];
-    colc[0][r] = tr[0];
-  }
-  if (r == 0) {
-#pragma unroll
-    for (int k = 0; k < 16; k++) rowc[0][q + 4 * k] = yr[k];
-    if (q == 0) rowc[0][NB] = rhs;
-  }
+  if (t < NB) bsh[t] = B.rhs[(long long)p * NB + t];
+  __syncthreads();
   for (int c = 0; c < NB; c++) {
-    const int buf = c & 1, nbuf = buf ^ 1;
-    __syncthreads();
-    double d = colc[buf][c].x;
+    // pivot: d = A[c][c] - sum_{k<c} |L[c][k]|^2
+    double dp0 = 0.0, dp1 = 0.0;
+    int k = q;
+    for (; k + 4 < c; k += 8) {
+      const double2 u = T[c * LDS + k], v = T[c * LDS + k + 4];
+      dp0 = fma(u.x, u.x, fma(u.y, u.y, dp0));
+      dp1 = fma(v.x, v.x, fma(v.y, v.y, dp1));
+    }
+    if (k < c) {
+      const double2 u = T[c * LDS + k];
+      dp0 = fma(u.x, u.x, fma(u.y, u.y, dp0));
+    }
+    double dsum = dp0 + dp1;
+    dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
+    dsum += __shfl_xor_sync(0xffffffffu, dsum, 2);
+    double d = T[c * LDS + c].x - dsum;
     if (!(d > 0.0)) {
       if (t == 0 && cs.info) atomicCAS(cs.info, 0, (int)(B.row_base + (long long)p * NB + c + 1));
       d = 1.0;
     }
-    if (t == 0) piv[c] = d;
+    const double isd = 1.0 / sqrt(d);
+    double2 s0 = make_double2(0.0, 0.0), s1 = s0;
     if (r > c) {
-      const double inv = 1.0 / d;
-      const double2 a = colc[buf][r];
-      const double2 g = make_double2(a.x * inv, a.y * inv);   // a_rc / d_c
-#pragma unroll
-      for (int k = 0; k < 16; k++) {
-        const int s = q + 4 * k;
-        if (s > c && s <= r) {                                // T[r][s] -= g conj(a_sc)
-          const double2 bb = colc[buf][s];
-          tr[k].x -= g.x * bb.x + g.y * bb.y;
-          tr[k].y -= g.y * bb.x - g.x * bb.y;
-          if (s == c + 1) colc[nbuf][r] = tr[k];              // publish column c+1
-        }
-        if (s <= c) {                                         // Y[r][s] -= g Y[c][s]
-          const double2 y = rowc[buf][s];
-          yr[k].x -= g.x * y.x - g.y * y.y;
-          yr[k].y -= g.x * y.y + g.y * y.x;
-        }
+      // sum_{k<c} L[r][k] conj(L[c][k])
+      int kk = q;
+      for (; kk + 4 < c; kk += 8) {
+        cfma_conj(s0, T[c * LDS + kk], T[r * LDS + kk]);
+        cfma_conj(s1, T[c * LDS + kk + 4], T[r * LDS + kk + 4]);
       }
-      if (q == 0) {
-        const double2 y = rowc[buf][NB];
-        rhs.x -= g.x * y.x - g.y * y.y;
-        rhs.y -= g.x * y.y + g.y * y.x;
+      if (kk < c) cfma_conj(s0, T[c * LDS + kk], T[r * LDS + kk]);
+    } else if (r < c) {
+      // sum_{r<=k<c} L[c][k] X[k][r]
+      int kk = r + q;
+      for (; kk + 4 < c; kk += 8) {
+        cfma(s0, T[c * LDS + kk], X[kk * LDS + r]);
+        cfma(s1, T[c * LDS + kk + 4], X[(kk + 4) * LDS + r]);
       }
-      if (r == c + 1) {                                       // publish row c+1 of Y (final now)
-#pragma unroll
-        for (int k = 0; k < 16; k++) rowc[nbuf][q + 4 * k] = yr[k];
-        if (q == 0) rowc[nbuf][NB] = rhs;
+      if (kk < c) cfma(s0, T[c * LDS + kk], X[kk * LDS + r]);
+    }
+    double2 sum = cadd(s0, s1);
+    sum.x += __shfl_xor_sync(0xffffffffu, sum.x, 1);
+    sum.y += __shfl_xor_sync(0xffffffffu, sum.y, 1);
+    sum.x += __shfl_xor_sync(0xffffffffu, sum.x, 2);
+    sum.y += __shfl_xor_sync(0xffffffffu, sum.y, 2);
+    if (q == 0) {
+      if (r > c) {
+        T[r * LDS + c] = cscale(csub(T[r * LDS + c], sum), isd);
+      } else if (r < c) {
+        X[c * LDS + r] = make_double2(-sum.x * isd, -sum.y * isd);
+      } else {
+        T[c * LDS + c] = make_double2(d * isd, 0.0);   // sqrt(d)
+        X[c * LDS + c] = make_double2(isd, 0.0);
       }
     }
+    __syncthreads();
   }
-  __syncthreads();
   double2* linv = B.linv + (long long)p * NB * NB;
-  const double isr = 1.0 / sqrt(piv[r]);
-#pragma unroll
-  for (int k = 0; k < 16; k++) {
-    const int s = q + 4 * k;
-    if (s < r) tile[(long long)r * np + s] = cscale(tr[k], 1.0 / sqrt(piv[s]));
-    else if (s == r) tile[(long long)r * np + s] = make_double2(sqrt(piv[r]), 0.0);
-    linv[r * NB + s] = s <= r ? cscale(yr[k], isr) : make_double2(0.0, 0.0);
+  for (int e = t; e < NB * NB; e += 256) {
+    const int rr = e >> 6, c = e & 63;
+    if (c <= rr) tile[(long long)rr * np + c] = T[rr * LDS + c];
+    linv[e] = X[rr * LDS + c];
   }
-  if (q == 0) B.rhs[(long long)p * NB + r] = cscale(rhs, isr);
+  {
+    double2 y = make_double2(0.0, 0.0);
+    for (int c = q; c <= r; c += 4) cfma(y, X[r * LDS + c], bsh[c]);
+    y.x += __shfl_xor_sync(0xffffffffu, y.x, 1);
+    y.y += __shfl_xor_sync(0xffffffffu, y.y, 1);
+    y.x += __shfl_xor_sync(0xffffffffu, y.x, 2);
+    y.y += __shfl_xor_sync(0xffffffffu, y.y, 2);
+    if (q == 0) B.rhs[(long long)p * NB + r] = y;
+  }
 }
 
 // b_i -= sum_c L[i][p*64 + c] y_p[c] for rows i >= (p+1)*64 (one warp per row).
@@ -225,9 +238,86 @@ void carve_chol(Arena& a, CholSet& cs, const long long* sizes, int nblk) {
   }
 }
 
+namespace {
+
+// Factorisation + substitutions of ONE block on one stream (two-level blocking, see header).
+sr_status solve_block(CholSet& cs, int b, cudaStream_t st) {
+  const CholBlock& B = cs.b[b];
+  ActiveList act;
+  act.n = 1;
+  act.idx[0] = b;
+  // Two-level blocking: strips of kStrip panels.  Inside a strip each panel p is factored
+  // (chol_diag), its column solved (TRSM), the RHS updated, and only the strip's own later
+  // columns updated (K = 64); the rest of the trailing matrix receives one deferred update
+  // per strip with K = 64 * kStrip, which is where the flops are (4x the arithmetic
+  // intensity of a per-panel update, 4x fewer passes over the trailing matrix).
+  constexpr int kStrip = 4;
+  for (int p0 = 0; p0 < B.P; p0 += kStrip) {
+    const int pend = std::min(p0 + kStrip, B.P);
+    for (int p = p0; p < pend; p++) {
+      chol_diag<<<1, 256, kDiagSmem, st>>>(cs, act, p);
+      SR_LAUNCHED();
+      const long long m = B.npad - (long long)(p + 1) * NB;
+      if (m <= 0) continue;
+      gram::ProbSet trsm{}, inner{};
+      double2* panel = B.Fm + (long long)(p + 1) * NB * B.npad + (long long)p * NB;
+      gram::add_prob(trsm, panel, B.npad, B.linv + (long long)p * NB * NB, NB, panel, B.npad, (int)m, NB, NB, false);
+      for (int jj = p + 1; jj < pend; jj++) {   // later columns of the strip, rows i >= jj
+        const double2* lrows = B.Fm + (long long)jj * NB * B.npad + (long long)p * NB;
+        double2* cblk = B.Fm + (long long)jj * NB * B.npad + (long long)jj * NB;
+        gram::add_prob(inner, lrows, B.npad, lrows, B.npad, cblk, B.npad, (int)(B.npad - (long long)jj * NB), NB, NB,
+                       false);
+      }
+      SR_TRY((gram::launch<gram::NH, gram::STORE>(trsm, st)));
+      dim3 g((unsigned)std::min<long long>((m + 7) / 8, 4 * kNumSMs), 1);
+      chol_rhs_update<<<g, 256, 0, st>>>(cs, act, p);
+      SR_LAUNCHED();
+      SR_TRY((gram::launch<gram::NH, gram::SUB>(inner, st)));
+    }
+    const long long m = B.npad - (long long)pend * NB;
+    if (m > 0) {   // deferred trailing update of the strip, K = 64 * (pend - p0)
+      gram::ProbSet trail{};
+      const double2* lp = B.Fm + (long long)pend * NB * B.npad + (long long)p0 * NB;
+      double2* trailing = B.Fm + (long long)pend * NB * B.npad + (long long)pend * NB;
+      gram::add_prob(trail, lp, B.npad, lp, B.npad, trailing, B.npad, (int)m, (int)m, (long long)(pend - p0) * NB, true);
+      SR_TRY((gram::launch<gram::NH, gram::SUB>(trail, st)));
+    }
+  }
+  for (int p = B.P - 1; p >= 0; p--) {
+    dim3 g((unsigned)std::max(1, p), 1);
+    chol_back<<<g, 256, 0, st>>>(cs, act, p);
+    SR_LAUNCHED();
+  }
+  return SR_OK;
+}
+
+// Side streams for independent blocks (created once per process; high priority so the
+// latency-bound panel chain of one block is scheduled ahead of another block's big update).
+constexpr int kSideStreams = 8;
+struct SidePool {
+  cudaStream_t s[kSideStreams];
+  cudaEvent_t fork, join[kSideStreams];
+  bool ok = false;
+};
+sr_status side_pool(SidePool*& out) {
+  static SidePool pool;
+  if (!pool.ok) {
+    int lo = 0, hi = 0;
+    SR_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    for (int i = 0; i < kSideStreams; i++) {
+      SR_CUDA(cudaStreamCreateWithPriority(&pool.s[i], cudaStreamNonBlocking, hi));
+      SR_CUDA(cudaEventCreateWithFlags(&pool.join[i], cudaEventDisableTiming));
+    }
+    SR_CUDA(cudaEventCreateWithFlags(&pool.fork, cudaEventDisableTiming));
+    pool.ok = true;
+  }
+  out = &pool;
+  return SR_OK;
+}
+
+}  // namespace
+
 sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStream_t st) {
-  int pmax = 0;
-  for (int b = 0; b < cs.count; b++) pmax = std::max(pmax, cs.b[b].P);
   if (cs.info) SR_CUDA(cudaMemsetAsync(cs.info, 0, sizeof(int), st));
   {
     long long mx = 0;
@@ -236,45 +326,27 @@ sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStr
     chol_init<<<g, 256, 0, st>>>(cs, lam, inplace ? 1 : 0);
     SR_LAUNCHED();
   }
-  for (int p = 0; p < pmax; p++) {
-    ActiveList act;
-    act.n = 0;
-    long long max_trail = 0;
-    for (int b = 0; b < cs.count; b++)
-      if (cs.b[b].P > p) {
-        act.idx[act.n++] = b;
-        max_trail = std::max(max_trail, cs.b[b].npad - (long long)(p + 1) * NB);
-      }
-    chol_diag<<<act.n, 256, 0, st>>>(cs, act, p);
-    SR_LAUNCHED();
-    if (max_trail <= 0) continue;
-    gram::ProbSet trsm{}, trail{};
-    for (int i = 0; i < act.n; i++) {
-      const CholBlock& B = cs.b[act.idx[i]];
-      const long long m = B.npad - (long long)(p + 1) * NB;
-      if (m <= 0) continue;
-      double2* panel = B.Fm + (long long)(p + 1) * NB * B.npad + (long long)p * NB;
-      gram::add_prob(trsm, panel, B.npad, B.linv + (long long)p * NB * NB, NB, panel, B.npad, (int)m, NB, NB,
-                     false);
-      double2* trailing = B.Fm + (long long)(p + 1) * NB * B.npad + (long long)(p + 1) * NB;
-      gram::add_prob(trail, panel, B.npad, panel, B.npad, trailing, B.npad, (int)m, (int)m, NB, true);
-    }
-    SR_TRY((gram::launch<gram::NH, gram::STORE>(trsm, st)));
-    {
-      dim3 g((unsigned)std::min<long long>((max_trail + 7) / 8, 4 * kNumSMs), (unsigned)act.n);
-      chol_rhs_update<<<g, 256, 0, st>>>(cs, act, p);
-      SR_LAUNCHED();
-    }
-    SR_TRY((gram::launch<gram::NH, gram::SUB>(trail, st)));
+  static bool diag_attr = false;
+  if (!diag_attr) {
+    SR_CUDA(cudaFuncSetAttribute(chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagSmem));
+    diag_attr = true;
   }
-  for (int p = pmax - 1; p >= 0; p--) {
-    ActiveList act;
-    act.n = 0;
-    for (int b = 0; b < cs.count; b++)
-      if (cs.b[b].P > p) act.idx[act.n++] = b;
-    dim3 g((unsigned)std::max(1, p), (unsigned)act.n);
-    chol_back<<<g, 256, 0, st>>>(cs, act, p);
-    SR_LAUNCHED();
+  if (cs.count == 1) {
+    SR_TRY(solve_block(cs, 0, st));
+  } else {
+    // independent blocks on side streams, forked from and joined back into `st`
+    SidePool* pool;
+    SR_TRY(side_pool(pool));
+    SR_CUDA(cudaEventRecord(pool->fork, st));
+    for (int b = 0; b < cs.count; b++) {
+      cudaStream_t sb = pool->s[b % kSideStreams];
+      SR_CUDA(cudaStreamWaitEvent(sb, pool->fork, 0));
+      SR_TRY(solve_block(cs, b, sb));
+    }
+    for (int i = 0; i < std::min(cs.count, kSideStreams); i++) {
+      SR_CUDA(cudaEventRecord(pool->join[i], pool->s[i]));
+      SR_CUDA(cudaStreamWaitEvent(st, pool->join[i], 0));
+    }
   }
   {
     long long mx = 0;

@@ -132,6 +132,20 @@ class LocalStep:
         _rec(events, 5, st)
         return b.dtheta, b.energy
 
+    # --- CUDA graph of the whole step (the ~1000 launches of a step replayed as one) ---
+    def capture(self, theta):
+        """Capture run(theta) into a CUDA graph; theta's buffer is read at replay time."""
+        self.run(theta)                      # warm: lazy attributes, side streams
+        torch.cuda.synchronize(self.device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.run(theta)
+        return self.graph
+
+    def replay(self):
+        self.graph.replay()
+        return self.buf.dtheta, self.buf.energy
+
 
 class ShardedStep:
     """Sample-sharded step over a torch.distributed process group (NCCL on GPUs)."""
