@@ -155,6 +155,30 @@ SR_API sr_status sr_block_qgt(int64_t n_samples, int n_blocks,
                               const int64_t* block_offsets /*host*/, const double* A, int64_t lda,
                               double* S, void* workspace, size_t workspace_bytes, void* stream);
 
+/* sr_block_qgt_i8 — the same S_b = A_b^H A_b (same layout and contract as sr_block_qgt) on
+ * the tcgen05 integer tensor cores: every column of A is scaled by a power of two, split
+ * into seven exact int8 digit slices (54 bits), the slice products sum_{p+q<=6} C_p^T Y_q
+ * are accumulated EXACTLY in int32 TMEM by tcgen05.mma kind::i8 and recombined in FP64
+ * (the Ozaki splitting scheme; DESIGN.md §5 and reading R10).  Error: at most ~2^-51 of
+ * n_samples * max_k|A_ki| * max_k|A_kj| per entry, the size of an FP64 dot product's.
+ * Workspace: sr_block_qgt_i8_workspace_bytes(n_samples, ...) bytes (digit slices,
+ * 42 bytes per sample per parameter of the largest group of blocks, plus column scales).
+ * Errors: SR_ERR_INVALID on bad sizes, SR_ERR_WORKSPACE if the workspace is too small. */
+SR_API size_t sr_block_qgt_i8_workspace_bytes(int64_t n_samples, int n_blocks,
+                                              const int64_t* block_offsets /*host*/);
+SR_API sr_status sr_block_qgt_i8(int64_t n_samples, int n_blocks,
+                                 const int64_t* block_offsets /*host*/, const double* A, int64_t lda,
+                                 double* S, void* workspace, size_t workspace_bytes, void* stream);
+
+/* sr_set_gram_engine — which engine sr_step uses for stage (4) (and the Cholesky trailing
+ * updates do not change): SR_GRAM_FP64 = FP64 DMMA tensor cores (sr_block_qgt),
+ * SR_GRAM_INT8 = int8 tcgen05 digit slices (sr_block_qgt_i8).  Process-wide; returns the
+ * previous setting, or -1 for an unknown engine (setting unchanged). */
+#define SR_GRAM_FP64 0
+#define SR_GRAM_INT8 1
+SR_API int sr_set_gram_engine(int engine);
+SR_API int sr_get_gram_engine(void);
+
 /* ---------------------------------------------------------------- stage (5) ---
  * sr_block_solve — PAPER.md §2: "Each block S_l is inverted independently, using a
  * uniform diagonal shift lambda", (S_b + lambda I) dtheta_b = -F_b, by a blocked,

@@ -41,6 +41,10 @@ SIGNATURES = {
                                       _vp]),
     "sr_block_qgt_workspace_bytes": (_sz, [_i32, _I64P]),
     "sr_block_qgt": (_i32, [_i64, _i32, _I64P, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "sr_block_qgt_i8_workspace_bytes": (_sz, [_i64, _i32, _I64P]),
+    "sr_block_qgt_i8": (_i32, [_i64, _i32, _I64P, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "sr_set_gram_engine": (_i32, [_i32]),
+    "sr_get_gram_engine": (_i32, []),
     "sr_block_solve_workspace_bytes": (_sz, [_i32, _I64P]),
     "sr_block_solve": (_i32, [_i32, _I64P, _vp, _vp, _dbl, _vp, _vp, _vp, _sz, _vp]),
     "sr_full_qgt_solve_workspace_bytes": (_sz, [_i64, _i64]),
@@ -209,6 +213,36 @@ def sr_block_qgt(A, offsets, S):
         raise SRError("S too small for the packed blocks")
     _check(lib.sr_block_qgt(A.shape[0], nblk, _offsets(offsets), _ptr(A), A.shape[1], _ptr(S), None, 0,
                             _stream(A.device)), "sr_block_qgt")
+
+
+def sr_block_qgt_i8(A, offsets, S, workspace=None):
+    """Stage (4) on the int8 tcgen05 tensor cores (digit slices; include/sr_block.h)."""
+    lib = load()
+    _dev(A, torch.complex128, "A")
+    _dev(S, torch.complex128, "S")
+    nblk = len(offsets) - 1
+    need = sum((offsets[b + 1] - offsets[b]) ** 2 for b in range(nblk))
+    if S.numel() < need:
+        raise SRError("S too small for the packed blocks")
+    off = _offsets(offsets)
+    ws = _workspace(lib.sr_block_qgt_i8_workspace_bytes(A.shape[0], nblk, off), A.device, workspace)
+    _check(lib.sr_block_qgt_i8(A.shape[0], nblk, off, _ptr(A), A.shape[1], _ptr(S), *_ws_args(ws),
+                               _stream(A.device)), "sr_block_qgt_i8")
+
+
+GRAM_FP64, GRAM_INT8 = 0, 1
+
+
+def sr_set_gram_engine(engine):
+    """Engine of sr_step's stage (4): GRAM_FP64 (DMMA) or GRAM_INT8 (tcgen05 digit slices)."""
+    prev = int(load().sr_set_gram_engine(int(engine)))
+    if prev < 0:
+        raise SRError(f"unknown gram engine {engine}")
+    return prev
+
+
+def sr_get_gram_engine():
+    return int(load().sr_get_gram_engine())
 
 
 # ------------------------------------------------------------------ stage (5)

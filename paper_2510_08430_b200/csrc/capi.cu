@@ -7,6 +7,7 @@
 #include "chol.cuh"
 #include "gram.cuh"
 #include "net.cuh"
+#include "ozaki.cuh"
 
 namespace sr {
 
@@ -14,6 +15,7 @@ thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
 void set_error(const std::string& m) { g_err = m; }
 void count_launch(int n) { g_launches += n; }
+int g_gram_engine = SR_GRAM_FP64;
 
 sr_status jacobian_impl(const NetDesc&, const double*, const int8_t*, long long, double*, double*, long long,
                         void*, size_t, cudaStream_t);
@@ -136,6 +138,7 @@ sr_status step_layout(int n_layers, const int32_t* widths, long long ns, long lo
   scr = std::max(scr, local_energy_ws(net, ns, nb));
   scr = std::max(scr, center_force_ws(ns, net.n_p));
   scr = std::max(scr, block_solve_ws(n_layers, L->offs.data()));
+  scr = std::max(scr, oz::workspace_bytes(ns, n_layers, L->offs.data()));
   L->scratch_bytes = round256(scr);
   L->scratch = take(L->scratch_bytes);
   L->total = off;
@@ -163,7 +166,11 @@ sr_status step_impl(const StepLayout& L, const double* theta, const int8_t* spin
   SR_TRY(jacobian_impl(net, theta, spins, ns, log_psi, O, net.n_p, scr, L.scratch_bytes, st));
   SR_TRY(local_energy_impl(net, theta, nb, bij, bj, spins, ns, log_psi, e_loc, scr, L.scratch_bytes, st));
   SR_TRY(center_force_impl(ns, net.n_p, O, net.n_p, nullptr, e_loc, energy, e_tilde, F, scr, L.scratch_bytes, st));
-  SR_TRY(block_qgt_impl(ns, net.L, L.offs.data(), reinterpret_cast<const double2*>(O), net.n_p, S, st));
+  if (g_gram_engine == SR_GRAM_INT8)
+    SR_TRY(oz::block_qgt_i8(ns, net.L, L.offs.data(), reinterpret_cast<const double2*>(O), net.n_p, S, scr,
+                            L.scratch_bytes, st));
+  else
+    SR_TRY(block_qgt_impl(ns, net.L, L.offs.data(), reinterpret_cast<const double2*>(O), net.n_p, S, st));
   SR_TRY(block_solve_impl(net.L, L.offs.data(), S, reinterpret_cast<const double2*>(F), lam,
                           reinterpret_cast<double2*>(dtheta), nullptr, scr, L.scratch_bytes, st));
   return SR_OK;
@@ -278,6 +285,30 @@ SR_API sr_status sr_block_qgt(int64_t n_samples, int n_blocks, const int64_t* bl
   return block_qgt_impl(n_samples, n_blocks, block_offsets, reinterpret_cast<const double2*>(A), lda,
                         reinterpret_cast<double2*>(S), (cudaStream_t)stream);
 }
+
+SR_API size_t sr_block_qgt_i8_workspace_bytes(int64_t n_samples, int n_blocks, const int64_t* block_offsets) {
+  if (n_samples < 0 || !valid_offsets(n_blocks, block_offsets)) return 0;
+  return oz::workspace_bytes(n_samples, n_blocks, block_offsets);
+}
+
+SR_API sr_status sr_block_qgt_i8(int64_t n_samples, int n_blocks, const int64_t* block_offsets, const double* A,
+                                 int64_t lda, double* S, void* workspace, size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(valid_offsets(n_blocks, block_offsets), "block_offsets must start at 0 and increase; 1..24 blocks");
+  SR_CHECK_ARG(n_samples >= 0 && lda >= block_offsets[n_blocks], "lda < n_p");
+  SR_CHECK_ARG(block_offsets[n_blocks] < (1LL << 31) / oz::kSlices, "n_p too large for the slice tensor map");
+  SR_CHECK_ARG(n_samples <= (1LL << 31) / 8, "n_samples too large");
+  SR_CHECK_ARG(A && S, "null pointer");
+  return oz::block_qgt_i8(n_samples, n_blocks, block_offsets, reinterpret_cast<const double2*>(A), lda,
+                          reinterpret_cast<double2*>(S), workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+SR_API int sr_set_gram_engine(int engine) {
+  if (engine != SR_GRAM_FP64 && engine != SR_GRAM_INT8) return -1;
+  const int prev = g_gram_engine;
+  g_gram_engine = engine;
+  return prev;
+}
+SR_API int sr_get_gram_engine(void) { return g_gram_engine; }
 
 SR_API size_t sr_block_solve_workspace_bytes(int n_blocks, const int64_t* block_offsets) {
   if (!valid_offsets(n_blocks, block_offsets)) return 0;

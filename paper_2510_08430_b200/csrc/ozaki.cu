@@ -1,0 +1,542 @@
+// ozaki.cu — stage (4), S_b = A_b^H A_b (Eq. 3; north_star (4)), on the tcgen05
+// integer tensor cores by exact digit splitting (the Ozaki scheme).
+//
+// FP64 has no tcgen05 kind; B200's FP64 tensor path is the legacy DMMA.8x8x4 (37 TFLOP/s
+// measured, gram.cuh).  tcgen05.mma kind::i8 runs at 4.5 POPS nominal, so the Gram is
+// evaluated as a short sum of EXACT int8 x int8 -> int32 products:
+//
+//   1. column scaling: every column j of A (a parameter) gets an exponent E_j with
+//      max_k max(|Re A_kj|, |Im A_kj|) < 2^E_j, and X_kj = rint(A_kj 2^(54 - E_j)) is an
+//      integer with |X| < 2^54 (rounding error <= 2^-55 of the column maximum);
+//   2. digits: X = sum_{p=0..6} d_p 256^(6-p), d_1..d_6 in [-128, 127] (balanced base-256),
+//      |d_0| <= 64 — seven int8 slices;
+//   3. real embedding: Re S = C^T C and Im S = C^T D over K' = 2 N_s, with
+//      C = [Re A; Im A] and D = [Im A; -Re A] (so S = A^H A exactly);
+//   4. products: G_t = sum_{p+q=t} C_p^T Y_q (Y = C or D) for t = 0..6, each an exact int32
+//      accumulation in TMEM (|G_t| <= 7 * 128^2 * 16384 < 2^31 per K' chunk of 16384);
+//      the dropped terms p+q >= 7 weigh <= 2^-51 of the leading one, i.e. the result carries
+//      FP64-level error relative to max|A_.i| max|A_.j| (about what a K-long FP64 dot
+//      product of the same columns commits);
+//   5. recombination in FP64: S_ij = 2^(E_i + E_j - 60) sum_t 256^(6-t) G_t (Horner).
+//
+// Kernels: oz_colmax (column maxima), oz_split (digits, transposed to K-major int8 rows
+// [slice][column][Re A | Im A | -Re A]), gram_i8 (persistent, warp-specialised: one TMA
+// producer lane, one MMA-issuing lane, four epilogue warps; 128 x 64 tiles of the
+// lower triangle, 28 tcgen05.mma per 32-byte K step into 7 TMEM accumulators).
+#include <cuda.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "ozaki.cuh"
+
+namespace sr {
+namespace oz {
+namespace {
+
+constexpr int BM = 128;                   // tile rows (i, A-operand rows, TMEM lanes)
+constexpr int BN = 64;                    // tile cols (j, B-operand rows, TMEM columns per accumulator)
+constexpr int BKB = 64;                   // K bytes per pipeline stage (one 64-byte swizzle row)
+constexpr int kStages = 2;
+constexpr int kASlice = BM * BKB;         // 8 KB
+constexpr int kBSlice = BN * BKB;         // 4 KB
+constexpr int kAStage = kSlices * kASlice;
+constexpr int kStageBytes = kSlices * (kASlice + kBSlice);   // 86016
+constexpr int kChunkK = 16384;            // K' per exact int32 accumulation
+constexpr int kBand = 8;                  // row panels per rasterisation band
+constexpr int kMaxBlk = 24;
+constexpr int kThreads = 192;             // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
+constexpr size_t kSmem = (size_t)kStages * kStageBytes + 1024 + 256;
+// tcgen05 instruction descriptor: D s32 (bits 4-5 = 2), A/B signed int8 (bits 7-9, 10-12 = 1),
+// both K-major, N >> 3 at bit 17, M >> 4 at bit 24.
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+struct Blk {
+  long long col0;        // first row of this block in the slice matrix (column of A within the group)
+  long long soff;        // element offset of S_b
+  long long tile_begin;  // first global tile index (tiles come in Re/Im pairs)
+  int n, RT, CT;
+};
+struct Params {
+  int nblk;
+  int kstages;           // K' / BKB
+  int spc;               // stages per exact accumulation chunk
+  long long Kp;          // padded sample count (bytes per slice-row segment)
+  long long total_tiles;
+  double2* S;
+  const int* expo;
+  Blk b[kMaxBlk];
+};
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+// Bounded wait: a lost arrival traps (kernel error) after ~20 s instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  long long t0 = 0;
+  for (int it = 0;; it++) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (it == 0) t0 = clock64();
+    else if ((it & 1023) == 0 && clock64() - t0 > 40000000000LL) __trap();
+  }
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(acc));
+}
+// K-major operand, 64-byte swizzle: 8-row core groups 512 bytes apart (SBO), LBO unused (1),
+// descriptor version 1 (sm_100), layout type 4 = SWIZZLE_64B.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// Global tile t -> (block, row panel I, column panel J, pass).  Within a block the lower
+// triangle tiles (J <= 2I + 1, i.e. some i >= j) are rasterised in bands of kBand row
+// panels, column-major inside a band, and come in (Re, Im) pairs sharing the A panel.
+__device__ __forceinline__ void decode(const Params& P, long long t, int& b, int& I, int& J, int& pass) {
+  b = 0;
+  while (b + 1 < P.nblk && t >= P.b[b + 1].tile_begin) b++;
+  long long u = t - P.b[b].tile_begin;
+  pass = (int)(u & 1);
+  u >>= 1;
+  const int RT = P.b[b].RT, CT = P.b[b].CT;
+  for (int I0 = 0; I0 < RT; I0 += kBand) {
+    const int I1 = min(RT, I0 + kBand), h = I1 - I0;
+    long long cnt = 0;
+    for (int i = I0; i < I1; i++) cnt += min(CT, 2 * i + 2);
+    if (u >= cnt) {
+      u -= cnt;
+      continue;
+    }
+    const int full = min(CT, 2 * I0);
+    if (u < (long long)full * h) {
+      J = (int)(u / h);
+      I = I0 + (int)(u % h);
+      return;
+    }
+    u -= (long long)full * h;
+    for (int j = full; j < CT; j++) {
+      const int lo = max(I0, j >> 1);
+      const int c = I1 - lo;
+      if (u < c) {
+        J = j;
+        I = lo + (int)u;
+        return;
+      }
+      u -= c;
+    }
+  }
+  I = J = 0;   // unreachable for t < total_tiles
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gram_i8(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b, const Params P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
+  const uint32_t tfull = smem_u32(bars + 2 * kStages), tempty = smem_u32(bars + 2 * kStages + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm_b) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t smem_base = smem_u32(smem);
+
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer
+      int s = 0;
+      uint32_t ph = 0;
+      for (long long t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+        int b, I, J, pass;
+        decode(P, t, b, I, J, pass);
+        const int rowA = (int)(P.b[b].col0 + (long long)I * BM);
+        const int rowB = (int)(P.b[b].col0 + (long long)J * BN);
+        const int kB = pass ? (int)P.Kp : 0;
+        for (int kk = 0; kk < P.kstages; kk++) {
+          mbar_wait(empty0 + 8 * s, ph ^ 1);
+          mbar_expect_tx(full0 + 8 * s, kStageBytes);
+          const uint32_t sa = smem_base + s * kStageBytes;
+          tma_load_3d(sa, &tm_a, kk * BKB, rowA, 0, full0 + 8 * s);
+          tma_load_3d(sa + kAStage, &tm_b, kB + kk * BKB, rowB, 0, full0 + 8 * s);
+          if (++s == kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // ---------------- MMA issuer (one thread for the CTA)
+      int s = 0;
+      uint32_t ph = 0, acc_ph = 0;
+      for (long long t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+        for (int kk = 0; kk < P.kstages; kk++) {
+          const int kin = kk % P.spc;
+          if (kin == 0) {   // accumulators drained by the epilogue?
+            mbar_wait(tempty, acc_ph ^ 1);
+            acc_ph ^= 1;
+            tc_fence_after();
+          }
+          mbar_wait(full0 + 8 * s, ph);
+          tc_fence_after();
+          const uint32_t sa = smem_base + s * kStageBytes, sb = sa + kAStage;
+#pragma unroll
+          for (int ks = 0; ks < BKB / 32; ks++) {
+#pragma unroll
+            for (int p = 0; p < kSlices; p++) {
+              const uint64_t ad = sdesc(sa + p * kASlice + ks * 32);
+#pragma unroll
+              for (int q = 0; q + p < kSlices; q++) {
+                const uint64_t bd = sdesc(sb + q * kBSlice + ks * 32);
+                mma_i8(tmem + (uint32_t)((p + q) * BN), ad, bd, (kin > 0 || ks > 0 || p > 0) ? 1u : 0u);
+              }
+            }
+          }
+          tc_commit(empty0 + 8 * s);   // frees the smem stage when these MMAs complete
+          if (kin == P.spc - 1 || kk == P.kstages - 1) tc_commit(tfull);
+          if (++s == kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else {   // ---------------- epilogue: TMEM -> FP64 recombination -> S
+    const int q4 = warp & 3;             // TMEM lane quarter this warp may access
+    const int rl = q4 * 32 + lane;       // tile row of this thread
+    const int nchunks = (P.kstages + P.spc - 1) / P.spc;
+    uint32_t c = 0;
+    for (long long t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+      int b, I, J, pass;
+      decode(P, t, b, I, J, pass);
+      const Blk& B = P.b[b];
+      const int n = B.n;
+      const int i = I * BM + rl;
+      const bool row_ok = i < n;
+      const int ei = row_ok ? P.expo[B.col0 + i] : 0;
+      double* Sb = reinterpret_cast<double*>(P.S + B.soff);
+      for (int ch = 0; ch < nchunks; ch++, c++) {
+        mbar_wait(tfull, c & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < BN / 8; cc++) {
+          uint32_t g[kSlices][8];
+#pragma unroll
+          for (int tt = 0; tt < kSlices; tt++)
+            tmem_ld8(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(tt * BN + cc * 8), g[tt]);
+          tmem_wait_ld();
+          if (!row_ok) continue;
+#pragma unroll
+          for (int e = 0; e < 8; e++) {
+            const int j = J * BN + cc * 8 + e;
+            if (j >= n || j > i) continue;
+            double v = (double)(int)g[0][e];
+#pragma unroll
+            for (int tt = 1; tt < kSlices; tt++) v = fma(v, 256.0, (double)(int)g[tt][e]);
+            double val = scalbn(v, ei + P.expo[B.col0 + j] - 60);
+            double* direct = Sb + 2 * ((long long)i * n + j) + pass;
+            if (ch > 0) val += *direct;
+            if (ch + 1 < nchunks) {
+              *direct = val;
+            } else if (i == j) {
+              *direct = pass ? 0.0 : val;
+            } else {
+              *direct = val;
+              Sb[2 * ((long long)j * n + i) + pass] = pass ? -val : val;
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+  }
+}
+
+// Column maxima of max(|Re|, |Im|) over samples (as ordered bit patterns of non-negative doubles).
+__global__ void oz_colmax(const double2* __restrict__ A, long long lda, long long c0, int n, long long K,
+                          int rows_per, unsigned long long* __restrict__ mx) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const long long k0 = (long long)blockIdx.y * rows_per, k1 = min(K, k0 + rows_per);
+  double m = 0.0;
+  for (long long k = k0; k < k1; k++) {
+    const double2 v = A[k * lda + c0 + j];
+    m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+  }
+  atomicMax(mx + j, (unsigned long long)__double_as_longlong(m));
+}
+
+__device__ __forceinline__ void put_digits(long long x, uint64_t (&pk)[kSlices], int r) {
+#pragma unroll
+  for (int p = kSlices - 1; p >= 1; p--) {
+    const int d = (int)(signed char)(x & 0xFF);
+    pk[p] |= (uint64_t)(uint8_t)d << (8 * r);
+    x = (x - d) >> 8;
+  }
+  pk[0] |= (uint64_t)(uint8_t)(int)x << (8 * r);
+}
+
+// Digits of 32 columns x 64 samples, written as K-major int8 rows
+// E[p][j][part * Kp + k], part 0 = Re A, 1 = Im A, 2 = -Re A.
+constexpr int kSplitRow = 80;   // smem bytes per staged 64-byte row (conflict-light, 16-B aligned)
+constexpr size_t kSplitSmem = (size_t)3 * kSlices * 32 * kSplitRow;
+__global__ void __launch_bounds__(256) oz_split(const double2* __restrict__ A, long long lda, long long c0, int n,
+                                                long long K, long long Kp, const unsigned long long* __restrict__ mx,
+                                                int8_t* __restrict__ E, int* __restrict__ expo) {
+  extern __shared__ uint8_t ssm[];
+  const int t = threadIdx.x, jl = t & 31, kg = t >> 5;
+  const int j = blockIdx.x * 32 + jl;
+  const long long k0 = (long long)blockIdx.y * 64;
+  int e = 0;
+  if (j < n) {
+    const double m = __longlong_as_double((long long)mx[j]);
+    if (m > 0.0) frexp(m, &e);
+    if (blockIdx.y == 0 && kg == 0) expo[j] = e;
+  }
+  uint64_t pk[3][kSlices];
+#pragma unroll
+  for (int a = 0; a < 3; a++)
+#pragma unroll
+    for (int p = 0; p < kSlices; p++) pk[a][p] = 0;
+#pragma unroll 2
+  for (int r = 0; r < 8; r++) {
+    const long long k = k0 + kg * 8 + r;
+    double2 v = make_double2(0.0, 0.0);
+    if (j < n && k < K) v = A[k * lda + c0 + j];
+    const long long xr = llrint(scalbn(v.x, 54 - e)), xi = llrint(scalbn(v.y, 54 - e));
+    put_digits(xr, pk[0], r);
+    put_digits(xi, pk[1], r);
+    put_digits(-xr, pk[2], r);
+  }
+#pragma unroll
+  for (int a = 0; a < 3; a++)
+#pragma unroll
+    for (int p = 0; p < kSlices; p++)
+      *reinterpret_cast<uint64_t*>(ssm + ((a * kSlices + p) * 32 + jl) * kSplitRow + kg * 8) = pk[a][p];
+  __syncthreads();
+  for (int c = t; c < 3 * kSlices * 32 * 4; c += 256) {
+    const int row = c >> 2, q = c & 3;
+    const int a = row / (kSlices * 32), rem = row % (kSlices * 32), p = rem / 32, jj = blockIdx.x * 32 + rem % 32;
+    if (jj >= n) continue;
+    const uint4 v = *reinterpret_cast<const uint4*>(ssm + row * kSplitRow + q * 16);
+    *reinterpret_cast<uint4*>(E + ((long long)p * n + jj) * (3 * Kp) + a * Kp + k0 + q * 16) = v;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+sr_status get_encode(EncodeFn& fn) {
+  static EncodeFn cached = nullptr;
+  if (!cached) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SR_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) {
+      set_error("cuTensorMapEncodeTiled unavailable");
+      return SR_ERR_CUDA;
+    }
+    cached = reinterpret_cast<EncodeFn>(p);
+  }
+  fn = cached;
+  return SR_OK;
+}
+
+sr_status make_map(CUtensorMap& m, void* base, long long Kp, long long ncols, int rows) {
+  EncodeFn enc;
+  SR_TRY(get_encode(enc));
+  const cuuint64_t dims[3] = {(cuuint64_t)(3 * Kp), (cuuint64_t)ncols, (cuuint64_t)kSlices};
+  const cuuint64_t strides[2] = {(cuuint64_t)(3 * Kp), (cuuint64_t)(3 * Kp * ncols)};
+  const cuuint32_t box[3] = {(cuuint32_t)BKB, (cuuint32_t)rows, (cuuint32_t)kSlices};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return SR_ERR_CUDA;
+  }
+  return SR_OK;
+}
+
+long long pad_k(long long ns) { return std::max<long long>(64, (ns + 63) / 64 * 64); }
+
+// Blocks are processed in groups whose digit slices fit a fixed budget (all blocks at once
+// when they fit; the buffer is reused group by group otherwise).
+constexpr size_t kSliceBudget = (size_t)6 << 30;
+size_t slice_bytes(long long Kp, long long ncols) { return (size_t)kSlices * 3 * Kp * ncols; }
+
+struct Group {
+  int b0, b1;
+  long long ncols;
+};
+std::vector<Group> plan(long long Kp, int nblk, const int64_t* offs, size_t& max_bytes) {
+  std::vector<Group> g;
+  max_bytes = 0;
+  int b = 0;
+  while (b < nblk) {
+    int e = b + 1;
+    while (e < nblk && slice_bytes(Kp, offs[e + 1] - offs[b]) <= kSliceBudget && e - b < kMaxBlk) e++;
+    g.push_back({b, e, offs[e] - offs[b]});
+    max_bytes = std::max(max_bytes, slice_bytes(Kp, offs[e] - offs[b]));
+    b = e;
+  }
+  return g;
+}
+
+}  // namespace
+
+size_t workspace_bytes(long long ns, int nblk, const int64_t* offs) {
+  const long long Kp = pad_k(ns);
+  size_t mb = 0;
+  std::vector<Group> g = plan(Kp, nblk, offs, mb);
+  long long mc = 0;
+  for (auto& x : g) mc = std::max(mc, x.ncols);
+  return round256(mb) + round256((size_t)mc * 8) + round256((size_t)mc * 4);
+}
+
+sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double2* A, long long lda, double2* S,
+                       void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (ws_bytes < workspace_bytes(ns, nblk, offs) || !ws) {
+    set_error("sr_block_qgt_i8: workspace too small");
+    return SR_ERR_WORKSPACE;
+  }
+  long long s_total = 0;
+  for (int b = 0; b < nblk; b++) s_total += (offs[b + 1] - offs[b]) * (offs[b + 1] - offs[b]);
+  if (ns == 0) {
+    SR_CUDA(cudaMemsetAsync(S, 0, (size_t)s_total * sizeof(double2), st));
+    return SR_OK;
+  }
+  const long long Kp = pad_k(ns);
+  size_t mb = 0;
+  std::vector<Group> groups = plan(Kp, nblk, offs, mb);
+  long long mc = 0;
+  for (auto& x : groups) mc = std::max(mc, x.ncols);
+  Arena a(ws, ws_bytes);
+  int8_t* E = a.take<int8_t>(mb);
+  unsigned long long* mx = a.take<unsigned long long>(mc);
+  int* expo = a.take<int>(mc);
+
+  static bool attr = false;
+  if (!attr) {
+    SR_CUDA(cudaFuncSetAttribute(gram_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+    SR_CUDA(cudaFuncSetAttribute(oz_split, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSplitSmem));
+    attr = true;
+  }
+  long long soff = 0;
+  for (const Group& G : groups) {
+    const long long c0 = offs[G.b0], nc = G.ncols;
+    SR_CUDA(cudaMemsetAsync(mx, 0, (size_t)nc * 8, st));
+    {
+      const int rows_per = 256;
+      dim3 g((unsigned)((nc + 255) / 256), (unsigned)((ns + rows_per - 1) / rows_per));
+      oz_colmax<<<g, 256, 0, st>>>(A, lda, c0, (int)nc, ns, rows_per, mx);
+      SR_LAUNCHED();
+    }
+    {
+      dim3 g((unsigned)((nc + 31) / 32), (unsigned)(Kp / 64));
+      oz_split<<<g, 256, kSplitSmem, st>>>(A, lda, c0, (int)nc, ns, Kp, mx, E, expo);
+      SR_LAUNCHED();
+    }
+    Params P{};
+    P.nblk = G.b1 - G.b0;
+    P.Kp = Kp;
+    P.kstages = (int)(2 * Kp / BKB);
+    P.spc = kChunkK / BKB;
+    P.S = S;
+    P.expo = expo;
+    long long tiles = 0;
+    for (int k = 0; k < P.nblk; k++) {
+      const int b = G.b0 + k;
+      Blk& B = P.b[k];
+      B.n = (int)(offs[b + 1] - offs[b]);
+      B.col0 = offs[b] - c0;
+      B.soff = soff;
+      soff += (long long)B.n * B.n;
+      B.RT = (B.n + BM - 1) / BM;
+      B.CT = (B.n + BN - 1) / BN;
+      B.tile_begin = tiles;
+      long long cnt = 0;
+      for (int i = 0; i < B.RT; i++) cnt += std::min(B.CT, 2 * i + 2);
+      tiles += 2 * cnt;
+    }
+    P.total_tiles = tiles;
+    CUtensorMap ma, mb2;
+    SR_TRY(make_map(ma, E, Kp, nc, BM));
+    SR_TRY(make_map(mb2, E, Kp, nc, BN));
+    const unsigned grid = (unsigned)std::min<long long>(tiles, kNumSMs);
+    gram_i8<<<grid, kThreads, kSmem, st>>>(ma, mb2, P);
+    SR_LAUNCHED();
+  }
+  return SR_OK;
+}
+
+}  // namespace oz
+}  // namespace sr

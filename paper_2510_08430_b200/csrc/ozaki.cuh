@@ -1,0 +1,20 @@
+// ozaki.cuh — stage (4) on the 5th-generation tensor cores (tcgen05 kind::i8), see ozaki.cu.
+#pragma once
+#include "common.cuh"
+
+namespace sr {
+namespace oz {
+
+constexpr int kSlices = 7;   // int8 digits per scaled value (54 bits, DESIGN.md §5 "Ozaki")
+
+// Workspace bytes of block_qgt_i8 for n_samples rows and the given block partition.
+size_t workspace_bytes(long long ns, int nblk, const int64_t* offs);
+
+// S_b = A_b^H A_b for every block (same contract as sr_block_qgt), computed from the int8
+// digit slices of the column-scaled A with tcgen05 kind::i8 MMAs accumulated exactly in
+// TMEM (int32) and recombined in FP64.
+sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double2* A, long long lda, double2* S,
+                       void* ws, size_t ws_bytes, cudaStream_t st);
+
+}  // namespace oz
+}  // namespace sr

@@ -1,0 +1,156 @@
+"""GPU parity of the int8 tcgen05 Gram engine (sr_block_qgt_i8, DESIGN.md §5 "Ozaki").
+
+Same contract and tolerance as sr_block_qgt: relative L2 1e-11 per block S_b against the
+CPU oracle (BASELINE.json north_star), exactly Hermitian as stored, real diagonal.  The
+cases span several 128 x 64 tiles with ragged edges, one-column blocks, a single sample,
+and n_samples above 8192 (more than one exact int32 accumulation chunk of K' = 16384).
+"""
+import numpy as np
+import pytest
+import torch
+
+import workloads
+from oracle import estimators, hamiltonian, network, solvers
+
+pytestmark = pytest.mark.gpu
+
+C128 = torch.complex128
+
+
+@pytest.fixture(scope="module")
+def sr():
+    import paper_2510_08430_b200 as pkg
+    pkg.load()
+    return pkg
+
+
+def dev():
+    return torch.device("cuda:0")
+
+
+def T(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dev())
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def packed_blocks(S, offs):
+    out, pos = [], 0
+    for b in range(len(offs) - 1):
+        n = offs[b + 1] - offs[b]
+        out.append(S[pos:pos + n * n].reshape(n, n))
+        pos += n * n
+    return out
+
+
+CASES = [
+    (512, (220, 420)),
+    (37, (64, 18, 130)),
+    (17, (1, 65, 128)),
+    (1, (40, 3)),
+    (300, (129, 64, 63, 257)),
+    (9000, (70, 131)),        # two int32 accumulation chunks
+    (20000, (33,)),           # three chunks, ragged K
+]
+
+
+@pytest.mark.parametrize("ns,sizes", CASES, ids=[f"ns{c[0]}_{'-'.join(map(str, c[1]))}" for c in CASES])
+def test_block_qgt_i8_parity(sr, ns, sizes):
+    rng = np.random.default_rng(ns + 7 * len(sizes))
+    n_p = sum(sizes)
+    offs = [0] + [int(x) for x in np.cumsum(sizes)]
+    O = rng.standard_normal((ns, n_p)) + 1j * rng.standard_normal((ns, n_p))
+    # columns of very different scale (the per-column exponents must carry them)
+    O *= np.exp(rng.uniform(-6, 6, n_p))[None, :]
+    A, _ = estimators.scaled_centered(O, np.zeros(ns))
+    S = torch.full((sum(n * n for n in sizes),), complex(np.nan, np.nan), dtype=C128, device=dev())
+    sr.sr_block_qgt_i8(T(A), offs, S)
+    got = packed_blocks(S.cpu().numpy(), offs)
+    ref = estimators.qgt_blocks(O, offs)
+    for g, r in zip(got, ref):
+        assert np.all(np.isfinite(g))
+        if np.linalg.norm(r) == 0:
+            assert np.all(g == 0)
+            continue
+        assert rel(g, r) < 1e-11
+        assert np.array_equal(g, g.conj().T)           # Hermitian as stored
+        assert np.all(np.diag(g).imag == 0)
+
+
+def test_block_qgt_i8_zero_column_and_outlier(sr):
+    """A zero column gives a zero row/column; one huge sample in a column is carried by that
+    column's exponent (error relative to the column maximum, R10)."""
+    rng = np.random.default_rng(3)
+    ns, n = 200, 96
+    A = rng.standard_normal((ns, n)) + 1j * rng.standard_normal((ns, n))
+    A[:, 5] = 0
+    A[17, 9] *= 1e6
+    S = torch.empty(n * n, dtype=C128, device=dev())
+    sr.sr_block_qgt_i8(T(A), [0, n], S)
+    g = S.cpu().numpy().reshape(n, n)
+    ref = A.conj().T @ A
+    assert np.all(g[5] == 0) and np.all(g[:, 5] == 0)
+    assert rel(g, ref) < 1e-11
+
+
+def test_block_qgt_i8_matches_fp64_engine(sr):
+    """configs[1] at full size (N_s = 4096, blocks 3280/6480/6480): the int8 engine against
+    the FP64 DMMA engine on the same A, block by block."""
+    w = workloads.CONFIGS[1]
+    rng = np.random.default_rng(11)
+    n_p = w.n_params
+    offs = [int(x) for x in sr.block_offsets(w.widths)]
+    A = (torch.randn(w.n_samples, n_p, dtype=torch.float64, device=dev(),
+                     generator=torch.Generator(dev()).manual_seed(5))
+         + 1j * torch.randn(w.n_samples, n_p, dtype=torch.float64, device=dev(),
+                            generator=torch.Generator(dev()).manual_seed(6)))
+    A = A.contiguous()
+    n_s = sum((offs[b + 1] - offs[b]) ** 2 for b in range(len(offs) - 1))
+    S8 = torch.empty(n_s, dtype=C128, device=dev())
+    S64 = torch.empty(n_s, dtype=C128, device=dev())
+    sr.sr_block_qgt_i8(A, offs, S8)
+    sr.sr_block_qgt(A, offs, S64)
+    pos = 0
+    for b in range(len(offs) - 1):
+        n = offs[b + 1] - offs[b]
+        d = torch.linalg.vector_norm(S8[pos:pos + n * n] - S64[pos:pos + n * n])
+        r = torch.linalg.vector_norm(S64[pos:pos + n * n])
+        assert (d / r).item() < 1e-13
+        pos += n * n
+    # sampled entries against plain FP64 dot products of the same columns
+    cols = rng.choice(offs[1], 8, replace=False)
+    Ac = A[:, torch.as_tensor(cols, device=dev())].cpu().numpy()
+    ref = Ac.conj().T @ Ac
+    blk0 = S8[:offs[1] ** 2].reshape(offs[1], offs[1])
+    got = blk0[torch.as_tensor(cols, device=dev())][:, torch.as_tensor(cols, device=dev())].cpu().numpy()
+    assert rel(got, ref) < 1e-12
+
+
+def test_step_with_int8_engine(sr):
+    """sr_step with the int8 Gram engine: dtheta within 1e-9 and S_b within 1e-11 of the oracle."""
+    w = workloads.CONFIGS[0]
+    spins, params = workloads.make_inputs(w)
+    ij, jj = sr.lattice.for_workload(w)
+    nb = len(jj)
+    ws = torch.empty(sr.sr_step_workspace_bytes(w.widths, w.n_samples, nb), dtype=torch.uint8, device=dev())
+    d = torch.empty(w.n_params, dtype=C128, device=dev())
+    en = torch.empty(1, dtype=C128, device=dev())
+    prev = sr.sr_set_gram_engine(sr.GRAM_INT8)
+    try:
+        sr.sr_step(w.widths, T(sr.model.pack(params)), T(spins), T(ij), T(jj), w.lam, d, en, ws)
+    finally:
+        sr.sr_set_gram_engine(prev)
+    O = network.jacobian(params, spins)
+    e = hamiltonian.local_energies(params, spins, hamiltonian.bonds_for(w))
+    off = network.layer_offsets(params)
+    blocks = estimators.qgt_blocks(O, off)
+    ref = solvers.block_solve(blocks, estimators.force(O, e), off, w.lam)
+    assert rel(d.cpu().numpy(), ref) < 1e-9
+    so = sr.sr_step_s_offset(w.widths, w.n_samples, nb)
+    n_s = sum(b.size for b in blocks)
+    S = ws[so:so + 16 * n_s].view(C128).cpu().numpy()
+    for g, r in zip(packed_blocks(S, sr.block_offsets(w.widths)), blocks):
+        assert rel(g, r) < 1e-11
