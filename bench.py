@@ -47,6 +47,18 @@ def block_sizes(w):
     return w.layer_sizes
 
 
+INT8_SLICES = 7                 # digit slices of sr_block_qgt_i8 (include/sr_block.h)
+INT8_PAIRS = INT8_SLICES * (INT8_SLICES + 1) // 2
+INT8_OVER_BF16 = 4.5 / 2.25     # nominal dense int8 : bf16 tensor rate (B200_PROFILING.md table)
+
+
+def gram_i8_ops(w, ns):
+    """Algorithmic int8 tensor ops of the digit-slice Gram: for each unique Hermitian entry
+    (i >= j) the real Re and Im dot products over K' = 2 N_s, INT8_PAIRS slice products
+    each, 2 ops per multiply-add."""
+    return sum(2 * (n * (n + 1) / 2) * (2 * ns) * INT8_PAIRS * 2 for n in block_sizes(w))
+
+
 def gram_flops(w, ns):
     """Algorithmic FP64 flops of the block QGT: n_b(n_b+1)/2 unique complex entries of each
     Hermitian S_b, N_s complex multiply-adds (8 real flops) each."""
@@ -131,10 +143,12 @@ def run_gpu(args):
     n_p, ns = w.n_params, w.n_samples
     offs = sr.block_offsets(w.widths)
 
+    engine = args.gram_engine
+    sr.sr_set_gram_engine(sr.GRAM_INT8 if engine == "int8" else sr.GRAM_FP64)   # for sr_step_host (e2e)
     if world > 1:
-        step = parallel.ShardedStep(w.widths, spins_all, ij, jj, w.lam, rank, world, dev)
+        step = parallel.ShardedStep(w.widths, spins_all, ij, jj, w.lam, rank, world, dev, gram_engine=engine)
     else:
-        step = parallel.LocalStep(w.widths, spins_all, ij, jj, w.lam, dev)
+        step = parallel.LocalStep(w.widths, spins_all, ij, jj, w.lam, dev, gram_engine=engine)
     theta = torch.from_numpy(theta_h).to(dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -146,11 +160,17 @@ def run_gpu(args):
     n_ev = len(step.STAGES) + 1
     n_stage_runs = max(1, min(args.steps, 3))
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(n_stage_runs)]
+    gram_kernel = "gram_i8" if engine == "int8" else "gram_tn"
+    sr.sr_kernel_time_ms(gram_kernel)
+    sr.sr_kernel_timer(True)                 # CUDA events around the Gram kernel's launches
     sr.sr_reset_launch_count()
     for k in range(n_stage_runs):
         step.run(theta, events=evs[k])
     torch.cuda.synchronize(dev)
+    sr.sr_kernel_timer(False)
     launches = sr.sr_launch_count() // n_stage_runs
+    gk_ms, gk_n = sr.sr_kernel_time_ms(gram_kernel)
+    gram_kernel_ms = gk_ms / max(gk_n, 1)
     stage_ms = {name: float(np.mean([evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(n_stage_runs)]))
                 for i, name in enumerate(step.STAGES)}
 
@@ -200,7 +220,33 @@ def run_gpu(args):
     gram_ms = stage_ms["block_qgt"]
     gflop = gram_flops(w, ns / world)
     achieved = gflop / (gram_ms * 1e-3) / 1e12
-    traffic = _ncu_traffic()
+    fp64_eq = gflop / (gram_kernel_ms * 1e-3) / 1e12
+    if engine == "int8":
+        ops = gram_i8_ops(w, ns / world)
+        peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * INT8_OVER_BF16
+        ach = ops / (gram_kernel_ms * 1e-3) / 1e12
+        roofline = {
+            "kernel": "sr::oz::gram_i8 (sr_block_qgt_i8: tcgen05.mma kind::i8, TMA, TMEM)", "bound": "tensor",
+            "achieved": ach, "peak": peak, "unit": "TFLOP/s", "op_dtype": "int8 (one multiply-add = 2 ops)",
+            "frac": ach / peak, "traffic": _ncu_traffic("gram_i8_traffic.json"),
+            "kernel_ms": gram_kernel_ms,
+            "algorithmic": (f"sum_b 2 (Re, Im) x n_b(n_b+1)/2 entries x K'=2 N_s x {INT8_PAIRS} slice pairs x 2 "
+                            f"= {ops:.4e} int8 ops per launch"),
+            "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained x 2 (nominal int8/bf16 ratio, "
+                            "B200_PROFILING.md); the burst figure x 2 is "
+                            f"{peaks['bf16_tflops'] * INT8_OVER_BF16:.0f}, the smem-resident tcgen05 "
+                            "microbenchmark 4763 (profiles/r01_tcgen05_rate.txt)"),
+            "fp64_equivalent": {"achieved_tflops": fp64_eq, "fp64_dmma_peak": FP64_PEAK_TFLOPS,
+                                "ratio_to_fp64_peak": fp64_eq / FP64_PEAK_TFLOPS,
+                                "algorithmic": f"sum_b 4 N_s n_b (n_b+1) = {gflop:.4e} flop"},
+        }
+    else:
+        roofline = {"kernel": "gram::tile_kernel<TN,HERM_STORE> (sr_block_qgt)", "bound": "tensor",
+                    "achieved": fp64_eq, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": fp64_eq / FP64_PEAK_TFLOPS, "traffic": _ncu_traffic("gram_traffic.json"),
+                    "kernel_ms": gram_kernel_ms,
+                    "algorithmic": f"sum_b 4 N_s n_b (n_b+1) = {gflop:.4e} flop per launch",
+                    "peak_source": FP64_PEAK_SOURCE}
     O_bytes = 16.0 * ns / world * n_p
     jac_ms = stage_ms["jacobian"]
     rec = {
@@ -218,14 +264,13 @@ def run_gpu(args):
         "data": "synthetic (seeded uniform S^z=0 spins, complex-normal weights; workloads.py)",
         "config": {"workload": w.name, "lattice": f"{w.lattice}{'x'.join(map(str, w.extent))}",
                    "widths": list(w.widths), "n_samples": ns, "n_params": n_p, "blocks": block_sizes(w),
-                   "lambda": w.lam, "parallelism": f"samples sharded x{world}" if world > 1 else "single GPU",
+                   "lambda": w.lam, "gram_engine": engine, "parallelism": f"samples sharded x{world}" if world > 1 else "single GPU",
                    "l2": f"inputs larger than L2 (O = {16.0 * ns * n_p / 1e9:.2f} GB per step vs 126 MB L2); no flush"},
-        "roofline": {"kernel": "gram::tile_kernel<TN,HERM_STORE> (sr_block_qgt)", "bound": "tensor",
-                     "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                     "algorithmic": f"sum_b 4 N_s n_b (n_b+1) = {gflop:.4e} flop per launch",
-                     "peak_source": FP64_PEAK_SOURCE},
+        "roofline": roofline,
         "stage_roofline": {
+            "block_qgt": {"engine": engine, "fp64_equivalent_tflops": achieved,
+                          "fp64_dmma_peak": FP64_PEAK_TFLOPS, "ratio": achieved / FP64_PEAK_TFLOPS,
+                          "includes": "column scaling + digit split + Gram" if engine == "int8" else "Gram"},
             "jacobian": {"bound": "hbm", "achieved_gbs": O_bytes / (jac_ms * 1e-3) / 1e9,
                          "peak_gbs": peaks["hbm_gbs"], "frac": O_bytes / (jac_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                          "algorithmic": "16 B x N_s x n_p written (O)"},
@@ -278,9 +323,9 @@ def run_e2e(sr, torch, w, theta_h, spins, ij, jj, dev, args):
             "api": "sr_step_host (C ABI, pinned host buffers, host-clock timed, stream synchronised per step)"}
 
 
-def _ncu_traffic():
+def _ncu_traffic(name):
     """dram bytes per launch of the Gram kernel from the committed ncu --set full capture."""
-    path = os.path.join(ROOT, "profiles", "gram_traffic.json")
+    path = os.path.join(ROOT, "profiles", name)
     try:
         with open(path) as f:
             d = json.load(f)
@@ -368,6 +413,8 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch stage by stage instead of one CUDA graph")
+    ap.add_argument("--gram-engine", default="int8", choices=["int8", "fp64"],
+                    help="stage (4) engine: int8 tcgen05 digit slices (default) or FP64 DMMA")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

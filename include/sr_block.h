@@ -19,7 +19,8 @@
  *   Pointers typed `double*` below that say "complex" point at 2*count doubles.
  * - Every pointer is a DEVICE pointer unless the argument says (host).  Device
  *   buffers are owned by the caller; the library never allocates or frees device
- *   memory, and keeps no state between calls.  Scratch comes in through a
+ *   memory, and keeps no state between calls apart from the process-wide Gram engine
+ *   choice (sr_set_gram_engine) and the optional kernel timer (sr_kernel_timer).  Scratch comes in through a
  *   `workspace` pointer whose size the matching *_workspace_bytes() query returns
  *   (256-byte aligned base required).
  * - `stream` is a cudaStream_t (NULL = legacy default stream).  All device work is
@@ -75,6 +76,15 @@ SR_API const char* sr_last_error(void);
  * (instrumentation for bench.py's gpu_launches; reset with sr_reset_launch_count). */
 SR_API int64_t sr_launch_count(void);
 SR_API void sr_reset_launch_count(void);
+
+/* Kernel timer (measurement support for bench.py).  While enabled, launches of the
+ * dominant kernels ("gram_i8" of sr_block_qgt_i8, "gram_tn" of sr_block_qgt) are
+ * bracketed by CUDA events on their launch stream (not while the stream is being
+ * captured into a graph).  sr_kernel_time_ms synchronises those events and returns the
+ * summed milliseconds of the launches of `kernel` recorded since the previous read
+ * (their count in *launches, may be NULL), then forgets them. */
+SR_API void sr_kernel_timer(int enable);
+SR_API double sr_kernel_time_ms(const char* kernel, int64_t* launches);
 
 /* ---------------------------------------------------------------- stage (1) ---
  * sr_jacobian — PAPER.md §2 Eq. 2 "O_i(x) = d_{theta_i} log psi_theta(x)".

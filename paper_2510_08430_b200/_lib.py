@@ -29,6 +29,8 @@ SIGNATURES = {
     "sr_last_error": (C.c_char_p, []),
     "sr_launch_count": (_i64, []),
     "sr_reset_launch_count": (None, []),
+    "sr_kernel_timer": (None, [_i32]),
+    "sr_kernel_time_ms": (_dbl, [C.c_char_p, _I64P]),
     "sr_jacobian_workspace_bytes": (_sz, [_i32, _I32P, _i64]),
     "sr_jacobian": (_i32, [_i32, _I32P, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _sz, _vp]),
     "sr_local_energy_workspace_bytes": (_sz, [_i32, _I32P, _i64, _i64]),
@@ -314,3 +316,14 @@ def sr_launch_count():
 
 def sr_reset_launch_count():
     load().sr_reset_launch_count()
+
+
+def sr_kernel_timer(enable):
+    load().sr_kernel_timer(1 if enable else 0)
+
+
+def sr_kernel_time_ms(kernel):
+    """(summed ms, launches) of `kernel` since the last read (see include/sr_block.h)."""
+    n = C.c_int64(0)
+    ms = load().sr_kernel_time_ms(kernel.encode(), C.byref(n))
+    return float(ms), int(n.value)

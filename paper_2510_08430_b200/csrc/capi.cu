@@ -17,6 +17,42 @@ void set_error(const std::string& m) { g_err = m; }
 void count_launch(int n) { g_launches += n; }
 int g_gram_engine = SR_GRAM_FP64;
 
+struct TimedLaunch {
+  std::string name;
+  cudaEvent_t a, b;
+};
+bool g_timer = false;
+std::vector<TimedLaunch> g_timed;
+std::vector<cudaEvent_t> g_event_pool;
+bool g_timer_open = false;
+
+cudaEvent_t timer_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+void timer_begin(const char* kernel, cudaStream_t st) {
+  g_timer_open = false;
+  if (!g_timer) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs != cudaStreamCaptureStatusNone) return;
+  TimedLaunch t{kernel, timer_event(), timer_event()};
+  cudaEventRecord(t.a, st);
+  g_timed.push_back(t);
+  g_timer_open = true;
+}
+void timer_end(cudaStream_t st) {
+  if (!g_timer_open) return;
+  cudaEventRecord(g_timed.back().b, st);
+  g_timer_open = false;
+}
+
 sr_status jacobian_impl(const NetDesc&, const double*, const int8_t*, long long, double*, double*, long long,
                         void*, size_t, cudaStream_t);
 size_t jacobian_ws(const NetDesc&, long long);
@@ -81,7 +117,10 @@ sr_status block_qgt_impl(long long ns, int nblk, const int64_t* offs, const doub
     gram::add_prob(ps, A + offs[b], lda, A + offs[b], lda, S + soff, n, (int)n, (int)n, ns, true);
     soff += n * n;
   }
-  return gram::launch<gram::TN, gram::HERM_STORE>(ps, st);
+  timer_begin("gram_tn", st);
+  const sr_status r = gram::launch<gram::TN, gram::HERM_STORE>(ps, st);
+  timer_end(st);
+  return r;
 }
 
 sr_status block_solve_impl(int nblk, const int64_t* offs, const double2* S, const double2* F, double lam,
@@ -300,6 +339,31 @@ SR_API sr_status sr_block_qgt_i8(int64_t n_samples, int n_blocks, const int64_t*
   SR_CHECK_ARG(A && S, "null pointer");
   return oz::block_qgt_i8(n_samples, n_blocks, block_offsets, reinterpret_cast<const double2*>(A), lda,
                           reinterpret_cast<double2*>(S), workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+SR_API void sr_kernel_timer(int enable) { g_timer = enable != 0; }
+
+SR_API double sr_kernel_time_ms(const char* kernel, int64_t* launches) {
+  double ms = 0.0;
+  int64_t n = 0;
+  std::vector<TimedLaunch> keep;
+  for (TimedLaunch& t : g_timed) {
+    if (kernel && t.name == kernel) {
+      float x = 0.f;
+      cudaEventSynchronize(t.b);
+      if (cudaEventElapsedTime(&x, t.a, t.b) == cudaSuccess) {
+        ms += x;
+        n++;
+      }
+      g_event_pool.push_back(t.a);
+      g_event_pool.push_back(t.b);
+    } else {
+      keep.push_back(t);
+    }
+  }
+  g_timed.swap(keep);
+  if (launches) *launches = n;
+  return ms;
 }
 
 SR_API int sr_set_gram_engine(int engine) {

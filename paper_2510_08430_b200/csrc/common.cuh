@@ -22,6 +22,9 @@ namespace sr {
 // ----------------------------------------------------------------------------
 void set_error(const std::string& msg);
 void count_launch(int n = 1);
+// Kernel timer (sr_kernel_timer): events around a launch on `st` when enabled.
+void timer_begin(const char* kernel, cudaStream_t st);
+void timer_end(cudaStream_t st);
 
 #define SR_CHECK_ARG(cond, msg)                 \
   do {                                          \

@@ -532,7 +532,9 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
     SR_TRY(make_map(ma, E, Kp, nc, BM));
     SR_TRY(make_map(mb2, E, Kp, nc, BN));
     const unsigned grid = (unsigned)std::min<long long>(tiles, kNumSMs);
+    timer_begin("gram_i8", st);
     gram_i8<<<grid, kThreads, kSmem, st>>>(ma, mb2, P);
+    timer_end(st);
     SR_LAUNCHED();
   }
   return SR_OK;

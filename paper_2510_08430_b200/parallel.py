@@ -8,7 +8,7 @@ ShardedStep, rank r of G, owning samples [r*N_s/G, (r+1)*N_s/G):
   1. sr_jacobian, sr_local_energy on the local rows                       (no exchange)
   2. sr_column_moments -> all_gather of the double-double moment rows     (2 n_p + 2 complex)
   3. sr_center_force_global sums the rows (double-double), centres -> all_reduce(SUM) of F
-  4. sr_block_qgt on the local rows (partial S_b = A_b,local^H A_b,local),
+  4. sr_block_qgt_i8 (or sr_block_qgt) on the local rows (partial S_b = A_b,local^H A_b,local),
      reduce(SUM, dst=owner(b)) per block, owner(b) = b mod G
   5. owners: sr_block_solve of their blocks; dtheta all_reduce(SUM) (non-owners hold 0)
 The arithmetic is the C ABI's; this module only moves buffers.  `ops` is injectable so
@@ -27,16 +27,21 @@ STAGES = ("jacobian", "local_energy", "center_force", "block_qgt", "block_solve"
 class CudaOps:
     """The C-ABI stage calls with one shared, preallocated workspace."""
 
-    def __init__(self, widths, n_local, n_bonds, device):
+    def __init__(self, widths, n_local, n_bonds, device, gram_engine="int8"):
+        if gram_engine not in ("int8", "fp64"):
+            raise ValueError(f"gram_engine must be 'int8' or 'fp64', got {gram_engine!r}")
         lib = sr.load()
         L, wa = sr._widths(widths)
         n_p = sr.n_params(widths)
         offs = sr.block_offsets(widths)
+        self.gram_engine = gram_engine
         need = max(
             lib.sr_jacobian_workspace_bytes(L, wa, n_local),
             lib.sr_local_energy_workspace_bytes(L, wa, n_local, n_bonds),
             lib.sr_center_force_workspace_bytes(n_local, n_p),
             lib.sr_block_solve_workspace_bytes(len(offs) - 1, sr._offsets(offs)),
+            lib.sr_block_qgt_i8_workspace_bytes(n_local, len(offs) - 1, sr._offsets(offs))
+            if gram_engine == "int8" else 0,
         )
         self.ws = torch.empty(int(need), dtype=torch.uint8, device=device)
 
@@ -57,7 +62,10 @@ class CudaOps:
                                   workspace=self.ws)
 
     def block_qgt(self, A, offs, S):
-        sr.sr_block_qgt(A, offs, S)
+        if self.gram_engine == "int8":
+            sr.sr_block_qgt_i8(A, offs, S, workspace=self.ws)
+        else:
+            sr.sr_block_qgt(A, offs, S)
 
     def block_solve(self, offs, S, F, lam, dtheta, info=None):
         sr.sr_block_solve(offs, S, F, lam, dtheta, info=info, workspace=self.ws)
@@ -110,11 +118,11 @@ class LocalStep:
 
     STAGES = STAGES
 
-    def __init__(self, widths, spins, bij, bj, lam, device, ops=None):
+    def __init__(self, widths, spins, bij, bj, lam, device, ops=None, gram_engine="int8"):
         self.lam = lam
         self.device = torch.device(device)
         self.buf = _Buffers(widths, spins, bij, bj, self.device)
-        self.ops = ops or CudaOps(widths, spins.shape[0], len(bj), self.device)
+        self.ops = ops or CudaOps(widths, spins.shape[0], len(bj), self.device, gram_engine)
 
     def run(self, theta, events=None):
         b, o = self.buf, self.ops
@@ -152,7 +160,8 @@ class ShardedStep:
 
     STAGES = STAGES
 
-    def __init__(self, widths, spins_all, bij, bj, lam, rank, world, device, ops=None, group=None):
+    def __init__(self, widths, spins_all, bij, bj, lam, rank, world, device, ops=None, group=None,
+                 gram_engine="int8"):
         self.lam = lam
         self.rank, self.world = rank, world
         self.group = group
@@ -160,7 +169,7 @@ class ShardedStep:
         lo, hi = shard_range(self.n_total, rank, world)
         self.device = torch.device(device)
         self.buf = _Buffers(widths, spins_all[lo:hi], bij, bj, self.device)
-        self.ops = ops or CudaOps(widths, hi - lo, len(bj), self.device)
+        self.ops = ops or CudaOps(widths, hi - lo, len(bj), self.device, gram_engine)
         self.moments = torch.empty(2 * self.buf.n_p + 2, dtype=torch.complex128, device=self.device)
         self.moments_all = torch.empty(world, 2 * self.buf.n_p + 2, dtype=torch.complex128, device=self.device)
         self.owned = [b for b in range(len(self.buf.offs) - 1) if block_owner(b, world) == rank]
