@@ -16,6 +16,7 @@ thread_local int64_t g_launches = 0;
 void set_error(const std::string& m) { g_err = m; }
 void count_launch(int n) { g_launches += n; }
 int g_gram_engine = SR_GRAM_FP64;
+int gram_engine() { return g_gram_engine; }
 
 struct TimedLaunch {
   std::string name;

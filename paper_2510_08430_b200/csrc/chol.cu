@@ -17,11 +17,13 @@
 // y_{<p} -= L_p,<p^H x_p) and dtheta = -x.
 #include "chol.cuh"
 #include "gram.cuh"
+#include "ozaki.cuh"
 
 namespace sr {
 namespace {
 
 constexpr int NB = 64;
+constexpr int kStrip = 4;   // panels per strip (deferred trailing update with K = 256)
 
 __global__ void chol_init(CholSet cs, double lam, int inplace) {
   const int b = blockIdx.y;
@@ -48,98 +50,229 @@ __global__ void chol_init(CholSet cs, double lam, int inplace) {
     B.rhs[r] = r < n ? B.F[r] : make_double2(0.0, 0.0);
 }
 
-// One CTA per active block: factor the 64x64 diagonal tile of panel p (left-looking), its
-// inverse X = Linv_p (row by row) and y_p = Linv_p b_p.  Step c, one barrier:
-//   d_c     = A[c][c] - sum_{k<c} |L[c][k]|^2                      (every quad, redundantly)
-//   L[r][c] = (A[r][c] - sum_{k<c} L[r][k] conj(L[c][k])) / sqrt(d_c)   rows r > c
-//   X[c][j] = -(sum_{j<=k<c} L[c][k] X[k][j]) / sqrt(d_c)               j = r < c
-//   L[c][c] = sqrt(d_c), X[c][c] = 1/sqrt(d_c)                          quad r == c
-// Quad (r, q) = (t/4, t%4) splits each dot product over k = q mod 4 and reduces with two
-// shuffles.  Everything reads only entries finalised in earlier steps.
-constexpr int LDS = NB + 4;   // 1088-byte rows: conflict-free quad access
-constexpr size_t kDiagSmem = (size_t)2 * NB * LDS * sizeof(double2);
-__global__ void __launch_bounds__(256) chol_diag(CholSet cs, ActiveList act, int p) {
+// One CTA per block: factor the 64x64 diagonal tile of panel p, form its inverse
+// X = Linv_p and y_p = Linv_p b_p.  Blocked by 16 (the latency of a 64-step column
+// recursion with a block barrier per step is what limited the unblocked forms):
+//   for each 16-column block k (offset o = 16k):
+//     (a) warp 0 factors D_k = A[o:o+16, o:o+16] in registers, lane r = row r, columns
+//         broadcast by shuffles, 1/sqrt of each pivot kept in dinv;
+//     (b) rows r >= o+16 solve x D_k^H = A[r, o:o+16] (one thread per row, right-looking);
+//     (c) A[r][s] -= sum_m L[r][o+m] conj(L[s][o+m]) on the trailing lower triangle
+//         (2x2 register patches).
+//   inverse: X_kk = D_k^{-1} (warp k, lane j = column j), then by block distance d = 1..3:
+//     W_ik = sum_{j=k}^{i-1} L_ij X_jk and X_ik = -X_ii W_ik (i = k + d), 2x2 patches.
+constexpr int LDT = NB + 1;   // 1040-byte rows
+constexpr size_t kDiagSmem = (size_t)2 * NB * LDT * sizeof(double2);
+
+__device__ __forceinline__ void cfma_conjb(double2& acc, double2 a, double2 b) {   // acc += a conj(b)
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.y, b.x, acc.y);
+  acc.y = fma(-a.x, b.y, acc.y);
+}
+
+// (a) warp 0: D = L L^H for the 16x16 block at (o, o) of T, in place.
+__device__ __forceinline__ void factor16(double2* T, int o, int lane, double* dinv, int* bad) {
+  double2 d[16];
+  const int r = lane;
+#pragma unroll
+  for (int s = 0; s < 16; s++)
+    d[s] = (r < 16 && s <= r) ? T[(o + r) * LDT + o + s] : make_double2(0.0, 0.0);
+#pragma unroll
+  for (int c = 0; c < 16; c++) {
+    double piv = __shfl_sync(0xffffffffu, d[c].x, c);
+    if (!(piv > 0.0)) {
+      if (lane == 0 && *bad == 0) *bad = o + c + 1;
+      piv = 1.0;
+    }
+    const double isd = rsqrt(piv);
+    if (r == c) d[c] = make_double2(piv * isd, 0.0);
+    else if (r > c) d[c] = cscale(d[c], isd);
+    if (lane == 0) dinv[o + c] = isd;
+#pragma unroll
+    for (int s = 1; s < 16; s++) {
+      if (s <= c) continue;
+      double2 ls;
+      ls.x = __shfl_sync(0xffffffffu, d[c].x, s);
+      ls.y = __shfl_sync(0xffffffffu, d[c].y, s);
+      if (r >= s) {
+        double2 v = d[s];
+        v.x -= d[c].x * ls.x + d[c].y * ls.y;
+        v.y -= d[c].y * ls.x - d[c].x * ls.y;
+        d[s] = v;
+      }
+    }
+  }
+  if (r < 16) {
+#pragma unroll
+    for (int s = 0; s < 16; s++)
+      if (s <= r) T[(o + r) * LDT + o + s] = d[s];
+  }
+}
+
+// (b) row r: x D^H = A[r, o:o+16] with D = L[o:o+16, o:o+16] (diagonal real, 1/D_cc in dinv).
+__device__ __forceinline__ void trsm_row(double2* T, int o, int r, const double* dinv) {
+  double2 a[16];
+#pragma unroll
+  for (int m = 0; m < 16; m++) a[m] = T[r * LDT + o + m];
+#pragma unroll
+  for (int c = 0; c < 16; c++) {
+    a[c] = cscale(a[c], dinv[o + c]);
+#pragma unroll
+    for (int m = c + 1; m < 16; m++) {
+      const double2 dm = T[(o + m) * LDT + o + c];   // D[m][c]; a[m] -= x_c conj(D[m][c])
+      a[m].x -= a[c].x * dm.x + a[c].y * dm.y;
+      a[m].y -= a[c].y * dm.x - a[c].x * dm.y;
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < 16; m++) T[r * LDT + o + m] = a[m];
+}
+
+// Lower-triangle patch index e -> (pi, pj), pi >= pj.
+__device__ __forceinline__ void tri_patch(int e, int& pi, int& pj) {
+  pi = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+  while ((pi + 1) * (pi + 2) / 2 <= e) pi++;
+  while (pi * (pi + 1) / 2 > e) pi--;
+  pj = e - pi * (pi + 1) / 2;
+}
+
+// (c) trailing update of rows/cols [o+16, 64) by the 16 columns L[:, o:o+16].
+__device__ __forceinline__ void syrk16(double2* T, int o, int t) {
+  const int b0 = o + 16, P = (NB - b0) / 2, cnt = P * (P + 1) / 2;
+  for (int e = t; e < cnt; e += 256) {
+    int pi, pj;
+    tri_patch(e, pi, pj);
+    const int r0 = b0 + 2 * pi, s0 = b0 + 2 * pj;
+    double2 acc[2][2] = {{make_double2(0.0, 0.0), make_double2(0.0, 0.0)},
+                         {make_double2(0.0, 0.0), make_double2(0.0, 0.0)}};
+#pragma unroll 4
+    for (int m = 0; m < 16; m++) {
+      const double2 lr0 = T[r0 * LDT + o + m], lr1 = T[(r0 + 1) * LDT + o + m];
+      const double2 ls0 = T[s0 * LDT + o + m], ls1 = T[(s0 + 1) * LDT + o + m];
+      cfma_conjb(acc[0][0], lr0, ls0);
+      cfma_conjb(acc[0][1], lr0, ls1);
+      cfma_conjb(acc[1][0], lr1, ls0);
+      cfma_conjb(acc[1][1], lr1, ls1);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; u++)
+#pragma unroll
+      for (int v = 0; v < 2; v++)
+        if (r0 + u >= s0 + v) {
+          double2& x = T[(r0 + u) * LDT + s0 + v];
+          x = csub(x, acc[u][v]);
+        }
+  }
+}
+
+// X[o:o+16, o:o+16] = L[o:o+16, o:o+16]^{-1} (lane j < 16 = column j; zeros above the diagonal).
+__device__ __forceinline__ void inv16(const double2* T, double2* X, int o, int lane, const double* dinv) {
+  if (lane >= 16) return;
+  const int j = lane;
+  double2 b[16];
+#pragma unroll
+  for (int i = 0; i < 16; i++) b[i] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < 16; i++) {
+    const double2 x = cscale(b[i], dinv[o + i]);
+    X[(o + i) * LDT + o + j] = x;
+#pragma unroll
+    for (int m = i + 1; m < 16; m++) {
+      const double2 l = T[(o + m) * LDT + o + i];
+      b[m].x -= l.x * x.x - l.y * x.y;
+      b[m].y -= l.x * x.y + l.y * x.x;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, int p) {
   extern __shared__ double2 dsm[];
-  double2* T = dsm;              // [64][LDS]: A (lower), columns replaced by L as they finish
-  double2* X = dsm + NB * LDS;   // [64][LDS]: Linv rows
+  double2* T = dsm;              // [64][LDT]: A (lower) -> L
+  double2* X = dsm + NB * LDT;   // [64][LDT]: Linv (lower)
+  __shared__ double dinv[NB];
   __shared__ double2 bsh[NB];
-  const CholBlock& B = cs.b[act.idx[blockIdx.x]];
+  __shared__ int bad;
   const long long np = B.npad;
   double2* tile = B.Fm + (long long)p * NB * np + (long long)p * NB;
-  const int t = threadIdx.x, r = t >> 2, q = t & 3;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   for (int e = t; e < NB * NB; e += 256) {
-    const int rr = e >> 6, c = e & 63;
-    T[rr * LDS + c] = c <= rr ? tile[(long long)rr * np + c] : make_double2(0.0, 0.0);
-    X[rr * LDS + c] = make_double2(0.0, 0.0);
+    const int r = e >> 6, c = e & 63;
+    if (c <= r) T[r * LDT + c] = tile[(long long)r * np + c];
   }
   if (t < NB) bsh[t] = B.rhs[(long long)p * NB + t];
+  if (t == 0) bad = 0;
   __syncthreads();
-  for (int c = 0; c < NB; c++) {
-    // pivot: d = A[c][c] - sum_{k<c} |L[c][k]|^2
-    double dp0 = 0.0, dp1 = 0.0;
-    int k = q;
-    for (; k + 4 < c; k += 8) {
-      const double2 u = T[c * LDS + k], v = T[c * LDS + k + 4];
-      dp0 = fma(u.x, u.x, fma(u.y, u.y, dp0));
-      dp1 = fma(v.x, v.x, fma(v.y, v.y, dp1));
+  for (int k = 0; k < 4; k++) {
+    const int o = 16 * k;
+    if (warp == 0) factor16(T, o, lane, dinv, &bad);
+    __syncthreads();
+    if (k < 3) {
+      if (t < NB - o - 16) trsm_row(T, o, o + 16 + t, dinv);
+      __syncthreads();
+      syrk16(T, o, t);
+      __syncthreads();
     }
-    if (k < c) {
-      const double2 u = T[c * LDS + k];
-      dp0 = fma(u.x, u.x, fma(u.y, u.y, dp0));
-    }
-    double dsum = dp0 + dp1;
-    dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
-    dsum += __shfl_xor_sync(0xffffffffu, dsum, 2);
-    double d = T[c * LDS + c].x - dsum;
-    if (!(d > 0.0)) {
-      if (t == 0 && cs.info) atomicCAS(cs.info, 0, (int)(B.row_base + (long long)p * NB + c + 1));
-      d = 1.0;
-    }
-    const double isd = 1.0 / sqrt(d);
-    double2 s0 = make_double2(0.0, 0.0), s1 = s0;
-    if (r > c) {
-      // sum_{k<c} L[r][k] conj(L[c][k])
-      int kk = q;
-      for (; kk + 4 < c; kk += 8) {
-        cfma_conj(s0, T[c * LDS + kk], T[r * LDS + kk]);
-        cfma_conj(s1, T[c * LDS + kk + 4], T[r * LDS + kk + 4]);
+  }
+  if (t == 0 && bad && info) atomicCAS(info, 0, (int)(B.row_base + (long long)p * NB + bad));
+  if (warp < 4) inv16(T, X, 16 * warp, lane, dinv);
+  __syncthreads();
+  for (int d = 1; d < 4; d++) {
+    const int nbk = 4 - d;
+    const bool act = t < nbk * 64;
+    const int kb = t >> 6, ib = kb + d, pr = (t & 63) >> 3, pc = t & 7;
+    const int r0 = 16 * ib + 2 * pr, c0 = 16 * kb + 2 * pc;
+    double2 acc[2][2] = {{make_double2(0.0, 0.0), make_double2(0.0, 0.0)},
+                         {make_double2(0.0, 0.0), make_double2(0.0, 0.0)}};
+    if (act) {   // W_ik = sum_{m in blocks k..i-1} L[r][m] X[m][c]
+      for (int m = 16 * kb; m < 16 * ib; m++) {
+        const double2 l0 = T[r0 * LDT + m], l1 = T[(r0 + 1) * LDT + m];
+        const double2 x0 = X[m * LDT + c0], x1 = X[m * LDT + c0 + 1];
+        cfma(acc[0][0], l0, x0);
+        cfma(acc[0][1], l0, x1);
+        cfma(acc[1][0], l1, x0);
+        cfma(acc[1][1], l1, x1);
       }
-      if (kk < c) cfma_conj(s0, T[c * LDS + kk], T[r * LDS + kk]);
-    } else if (r < c) {
-      // sum_{r<=k<c} L[c][k] X[k][r]
-      int kk = r + q;
-      for (; kk + 4 < c; kk += 8) {
-        cfma(s0, T[c * LDS + kk], X[kk * LDS + r]);
-        cfma(s1, T[c * LDS + kk + 4], X[(kk + 4) * LDS + r]);
-      }
-      if (kk < c) cfma(s0, T[c * LDS + kk], X[kk * LDS + r]);
+#pragma unroll
+      for (int u = 0; u < 2; u++)
+#pragma unroll
+        for (int v = 0; v < 2; v++) X[(r0 + u) * LDT + c0 + v] = acc[u][v];
     }
-    double2 sum = cadd(s0, s1);
-    sum.x += __shfl_xor_sync(0xffffffffu, sum.x, 1);
-    sum.y += __shfl_xor_sync(0xffffffffu, sum.y, 1);
-    sum.x += __shfl_xor_sync(0xffffffffu, sum.x, 2);
-    sum.y += __shfl_xor_sync(0xffffffffu, sum.y, 2);
-    if (q == 0) {
-      if (r > c) {
-        T[r * LDS + c] = cscale(csub(T[r * LDS + c], sum), isd);
-      } else if (r < c) {
-        X[c * LDS + r] = make_double2(-sum.x * isd, -sum.y * isd);
-      } else {
-        T[c * LDS + c] = make_double2(d * isd, 0.0);   // sqrt(d)
-        X[c * LDS + c] = make_double2(isd, 0.0);
+    __syncthreads();
+    if (act) {   // X_ik = -X_ii W_ik (X_ii lower triangular)
+#pragma unroll
+      for (int u = 0; u < 2; u++)
+#pragma unroll
+        for (int v = 0; v < 2; v++) acc[u][v] = make_double2(0.0, 0.0);
+      for (int m = 16 * ib; m <= r0 + 1; m++) {
+        const double2 w0 = X[m * LDT + c0], w1 = X[m * LDT + c0 + 1];
+        const double2 x0 = m <= r0 ? X[r0 * LDT + m] : make_double2(0.0, 0.0);
+        const double2 x1 = X[(r0 + 1) * LDT + m];
+        cfma(acc[0][0], x0, w0);
+        cfma(acc[0][1], x0, w1);
+        cfma(acc[1][0], x1, w0);
+        cfma(acc[1][1], x1, w1);
       }
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int u = 0; u < 2; u++)
+#pragma unroll
+        for (int v = 0; v < 2; v++) X[(r0 + u) * LDT + c0 + v] = make_double2(-acc[u][v].x, -acc[u][v].y);
     }
     __syncthreads();
   }
   double2* linv = B.linv + (long long)p * NB * NB;
   for (int e = t; e < NB * NB; e += 256) {
-    const int rr = e >> 6, c = e & 63;
-    if (c <= rr) tile[(long long)rr * np + c] = T[rr * LDS + c];
-    linv[e] = X[rr * LDS + c];
+    const int r = e >> 6, c = e & 63;
+    if (c <= r) tile[(long long)r * np + c] = T[r * LDT + c];
+    linv[e] = c <= r ? X[r * LDT + c] : make_double2(0.0, 0.0);
   }
   {
+    const int r = t >> 2, q = t & 3;
     double2 y = make_double2(0.0, 0.0);
-    for (int c = q; c <= r; c += 4) cfma(y, X[r * LDS + c], bsh[c]);
+    for (int c = q; c <= r; c += 4) cfma(y, X[r * LDT + c], bsh[c]);
     y.x += __shfl_xor_sync(0xffffffffu, y.x, 1);
     y.y += __shfl_xor_sync(0xffffffffu, y.y, 1);
     y.x += __shfl_xor_sync(0xffffffffu, y.x, 2);
@@ -149,8 +282,7 @@ __global__ void __launch_bounds__(256) chol_diag(CholSet cs, ActiveList act, int
 }
 
 // b_i -= sum_c L[i][p*64 + c] y_p[c] for rows i >= (p+1)*64 (one warp per row).
-__global__ void chol_rhs_update(CholSet cs, ActiveList act, int p) {
-  const CholBlock& B = cs.b[act.idx[blockIdx.y]];
+__global__ void chol_rhs_update(const CholBlock B, int p) {
   const long long np = B.npad;
   const long long r0 = (long long)(p + 1) * NB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -172,11 +304,10 @@ __global__ void chol_rhs_update(CholSet cs, ActiveList act, int p) {
 // x_p = Linv_p^H y_p (into xout), then y_c -= sum_c' conj(L[p*64 + c'][c]) x_p[c'] for c < p*64.
 // Each CTA owns 64 columns; 256 threads = 64 columns x 4 row quarters, reduced in a fixed
 // order through shared memory (deterministic).
-__global__ void __launch_bounds__(256) chol_back(CholSet cs, ActiveList act, int p) {
+__global__ void __launch_bounds__(256) chol_back(const CholBlock B, int p) {
   __shared__ double2 ys[NB];
   __shared__ double2 xs[NB];
   __shared__ double2 red[4][NB];
-  const CholBlock& B = cs.b[act.idx[blockIdx.y]];
   const long long np = B.npad;
   const int t = threadIdx.x;
   if (t < NB) ys[t] = B.rhs[(long long)p * NB + t];
@@ -235,6 +366,8 @@ void carve_chol(Arena& a, CholSet& cs, const long long* sizes, int nblk) {
     B.rhs = a.take<double2>(B.npad);
     B.xout = a.take<double2>(B.npad);
     B.linv = a.take<double2>((size_t)B.P * NB * NB);
+    B.tws_bytes = oz::trail_workspace_bytes(B.npad, (long long)kStrip * NB);
+    B.tws = a.take<char>(B.tws_bytes);
   }
 }
 
@@ -243,19 +376,18 @@ namespace {
 // Factorisation + substitutions of ONE block on one stream (two-level blocking, see header).
 sr_status solve_block(CholSet& cs, int b, cudaStream_t st) {
   const CholBlock& B = cs.b[b];
-  ActiveList act;
-  act.n = 1;
-  act.idx[0] = b;
   // Two-level blocking: strips of kStrip panels.  Inside a strip each panel p is factored
   // (chol_diag), its column solved (TRSM), the RHS updated, and only the strip's own later
   // columns updated (K = 64); the rest of the trailing matrix receives one deferred update
   // per strip with K = 64 * kStrip, which is where the flops are (4x the arithmetic
   // intensity of a per-panel update, 4x fewer passes over the trailing matrix).
-  constexpr int kStrip = 4;
+  const bool i8 = gram_engine() == SR_GRAM_INT8;
   for (int p0 = 0; p0 < B.P; p0 += kStrip) {
     const int pend = std::min(p0 + kStrip, B.P);
     for (int p = p0; p < pend; p++) {
-      chol_diag<<<1, 256, kDiagSmem, st>>>(cs, act, p);
+      timer_begin("chol_diag", st);
+      chol_diag<<<1, 256, kDiagSmem, st>>>(B, cs.info, p);
+      timer_end(st);
       SR_LAUNCHED();
       const long long m = B.npad - (long long)(p + 1) * NB;
       if (m <= 0) continue;
@@ -268,24 +400,40 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st) {
         gram::add_prob(inner, lrows, B.npad, lrows, B.npad, cblk, B.npad, (int)(B.npad - (long long)jj * NB), NB, NB,
                        false);
       }
+      timer_begin("chol_trsm", st);
       SR_TRY((gram::launch<gram::NH, gram::STORE>(trsm, st)));
+      timer_end(st);
       dim3 g((unsigned)std::min<long long>((m + 7) / 8, 4 * kNumSMs), 1);
-      chol_rhs_update<<<g, 256, 0, st>>>(cs, act, p);
+      timer_begin("chol_rhs", st);
+      chol_rhs_update<<<g, 256, 0, st>>>(B, p);
+      timer_end(st);
       SR_LAUNCHED();
-      SR_TRY((gram::launch<gram::NH, gram::SUB>(inner, st)));
+      timer_begin("chol_inner", st);
+      if (inner.count) SR_TRY((gram::launch<gram::NH, gram::SUB>(inner, st)));
+      timer_end(st);
     }
     const long long m = B.npad - (long long)pend * NB;
     if (m > 0) {   // deferred trailing update of the strip, K = 64 * (pend - p0)
-      gram::ProbSet trail{};
       const double2* lp = B.Fm + (long long)pend * NB * B.npad + (long long)p0 * NB;
       double2* trailing = B.Fm + (long long)pend * NB * B.npad + (long long)pend * NB;
-      gram::add_prob(trail, lp, B.npad, lp, B.npad, trailing, B.npad, (int)m, (int)m, (long long)(pend - p0) * NB, true);
-      SR_TRY((gram::launch<gram::NH, gram::SUB>(trail, st)));
+      if (i8) {   // int8 digit-slice tcgen05 engine (ozaki.cu), lower triangle
+        SR_TRY(oz::trail_update_i8(lp, B.npad, m, (long long)(pend - p0) * NB, trailing, B.npad, B.tws, B.tws_bytes,
+                                   0, st));
+      } else {
+        gram::ProbSet trail{};
+        gram::add_prob(trail, lp, B.npad, lp, B.npad, trailing, B.npad, (int)m, (int)m,
+                       (long long)(pend - p0) * NB, true);
+        timer_begin("trail_dmma", st);
+        SR_TRY((gram::launch<gram::NH, gram::SUB>(trail, st)));
+        timer_end(st);
+      }
     }
   }
   for (int p = B.P - 1; p >= 0; p--) {
     dim3 g((unsigned)std::max(1, p), 1);
-    chol_back<<<g, 256, 0, st>>>(cs, act, p);
+    timer_begin("chol_back", st);
+    chol_back<<<g, 256, 0, st>>>(B, p);
+    timer_end(st);
     SR_LAUNCHED();
   }
   return SR_OK;

@@ -14,6 +14,8 @@ struct CholBlock {
   double2* rhs;       // [npad]: b, then y, then the back-substitution residual
   double2* xout;      // [npad]: x
   double2* linv;      // [P][64][64]: inverses of the diagonal tiles
+  void* tws;          // int8 trailing-update workspace (digit slices of one strip)
+  size_t tws_bytes;
   long long n, npad, row_base;
   int P;
 };
@@ -24,10 +26,6 @@ struct CholSet {
   CholBlock b[kMaxBlocks];
 };
 
-struct ActiveList {
-  int n;
-  int idx[kMaxBlocks];
-};
 
 // Carves Fm/rhs/xout/linv for blocks of the given sizes (S, F, out set by the caller).
 void carve_chol(Arena& a, CholSet& cs, const long long* sizes, int nblk);

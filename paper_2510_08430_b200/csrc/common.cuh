@@ -25,6 +25,8 @@ void count_launch(int n = 1);
 // Kernel timer (sr_kernel_timer): events around a launch on `st` when enabled.
 void timer_begin(const char* kernel, cudaStream_t st);
 void timer_end(cudaStream_t st);
+// Process-wide engine for the dense contractions (sr_set_gram_engine).
+int gram_engine();
 
 #define SR_CHECK_ARG(cond, msg)                 \
   do {                                          \

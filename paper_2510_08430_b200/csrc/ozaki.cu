@@ -54,17 +54,20 @@ constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN 
 
 struct Blk {
   long long col0;        // first row of this block in the slice matrix (column of A within the group)
-  long long soff;        // element offset of S_b
+  double2* C;            // output: S_b (MODE_HERM, ld n) or the matrix updated in place (MODE_SUB)
+  long long ldc;
   long long tile_begin;  // first global tile index (tiles come in Re/Im pairs)
   int n, RT, CT;
 };
+// Epilogues: MODE_HERM writes S = G with its conjugate mirror (stage 4); MODE_SUB applies
+// C -= G to the lower triangle i >= j (Cholesky trailing update, chol.cu).
+enum { MODE_HERM = 0, MODE_SUB = 1 };
 struct Params {
   int nblk;
   int kstages;           // K' / BKB
   int spc;               // stages per exact accumulation chunk
   long long Kp;          // padded sample count (bytes per slice-row segment)
   long long total_tiles;
-  double2* S;
   const int* expo;
   Blk b[kMaxBlk];
 };
@@ -129,6 +132,12 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
+// v * 2^k: one multiply when 2^k is a normal double, scalbn otherwise.
+__device__ __forceinline__ double pow2_scale(double v, int k) {
+  if (k >= -1022 && k <= 1023) return v * __longlong_as_double((long long)(k + 1023) << 52);
+  return scalbn(v, k);
+}
+
 // Global tile t -> (block, row panel I, column panel J, pass).  Within a block the lower
 // triangle tiles (J <= 2I + 1, i.e. some i >= j) are rasterised in bands of kBand row
 // panels, column-major inside a band, and come in (Re, Im) pairs sharing the A panel.
@@ -168,6 +177,7 @@ __device__ __forceinline__ void decode(const Params& P, long long t, int& b, int
   I = J = 0;   // unreachable for t < total_tiles
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     gram_i8(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b, const Params P) {
   extern __shared__ uint8_t smem_raw[];
@@ -272,7 +282,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int i = I * BM + rl;
       const bool row_ok = i < n;
       const int ei = row_ok ? P.expo[B.col0 + i] : 0;
-      double* Sb = reinterpret_cast<double*>(P.S + B.soff);
+      double* Cb = reinterpret_cast<double*>(B.C);
+      const long long ldc = B.ldc;
+      if (MODE == MODE_SUB) {
+        // C -= G on the lower triangle by fire-and-forget reductions in L2 (red.global.add.f64):
+        // no read latency in the epilogue, and each element receives exactly one addend per
+        // launch (Re pass -> .x, Im pass -> .y), so the result is deterministic.
+        mbar_wait(tfull, c & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < BN / 8; cc++) {
+          uint32_t g[kSlices][8];
+#pragma unroll
+          for (int tt = 0; tt < kSlices; tt++)
+            tmem_ld8(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(tt * BN + cc * 8), g[tt]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 8; e++) {
+            const int j = J * BN + cc * 8 + e;
+            if (!row_ok || j >= n || j > i) continue;
+            double v = (double)(int)g[0][e];
+#pragma unroll
+            for (int tt = 1; tt < kSlices; tt++) v = fma(v, 256.0, (double)(int)g[tt][e]);
+            atomicAdd(Cb + 2 * ((long long)i * ldc + j) + pass, -pow2_scale(v, ei + P.expo[B.col0 + j] - 60));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
+        c++;
+        continue;
+      }
       for (int ch = 0; ch < nchunks; ch++, c++) {
         mbar_wait(tfull, c & 1);
         tc_fence_after();
@@ -291,8 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             double v = (double)(int)g[0][e];
 #pragma unroll
             for (int tt = 1; tt < kSlices; tt++) v = fma(v, 256.0, (double)(int)g[tt][e]);
-            double val = scalbn(v, ei + P.expo[B.col0 + j] - 60);
-            double* direct = Sb + 2 * ((long long)i * n + j) + pass;
+            double val = pow2_scale(v, ei + P.expo[B.col0 + j] - 60);
+            double* direct = Cb + 2 * ((long long)i * ldc + j) + pass;
             if (ch > 0) val += *direct;
             if (ch + 1 < nchunks) {
               *direct = val;
@@ -300,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               *direct = pass ? 0.0 : val;
             } else {
               *direct = val;
-              Sb[2 * ((long long)j * n + i) + pass] = pass ? -val : val;
+              Cb[2 * ((long long)j * ldc + i) + pass] = pass ? -val : val;
             }
           }
         }
@@ -388,6 +428,45 @@ __global__ void __launch_bounds__(256) oz_split(const double2* __restrict__ A, l
   }
 }
 
+// Digits of the rows of L (row-major along K, ld ldl) for C -= L L^H: row i plays the role
+// of a column of A = L^H (A_ki = conj(L_ik)), so the parts are [Re L | -Im L | -Re L].
+// One warp per row: row maximum by shuffles, then 8 consecutive k per lane per pass.
+__global__ void __launch_bounds__(256) oz_split_rows(const double2* __restrict__ L, long long ldl, int m, int K,
+                                                     int Kp, int8_t* __restrict__ E, int* __restrict__ expo) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (i >= m) return;
+  const double2* row = L + (long long)i * ldl;
+  double mx = 0.0;
+  for (int k = lane; k < K; k += 32) mx = fmax(mx, fmax(fabs(row[k].x), fabs(row[k].y)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);
+  if (lane == 0) expo[i] = e;
+  for (int k0 = lane * 8; k0 < Kp; k0 += 256) {
+    uint64_t pk[3][kSlices];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int p = 0; p < kSlices; p++) pk[a][p] = 0;
+#pragma unroll 2
+    for (int r = 0; r < 8; r++) {
+      const int k = k0 + r;
+      const double2 v = k < K ? row[k] : make_double2(0.0, 0.0);
+      const long long xr = llrint(scalbn(v.x, 54 - e)), xi = llrint(scalbn(-v.y, 54 - e));
+      put_digits(xr, pk[0], r);
+      put_digits(xi, pk[1], r);
+      put_digits(-xr, pk[2], r);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int p = 0; p < kSlices; p++)
+        *reinterpret_cast<uint64_t*>(E + ((long long)p * m + i) * (3LL * Kp) + (long long)a * Kp + k0) = pk[a][p];
+  }
+}
+
 // ---------------------------------------------------------------- host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -427,6 +506,24 @@ sr_status make_map(CUtensorMap& m, void* base, long long Kp, long long ncols, in
 }
 
 long long pad_k(long long ns) { return std::max<long long>(64, (ns + 63) / 64 * 64); }
+
+sr_status set_attrs() {
+  static bool attr = false;
+  if (!attr) {
+    SR_CUDA(cudaFuncSetAttribute(gram_i8<MODE_HERM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+    SR_CUDA(cudaFuncSetAttribute(gram_i8<MODE_SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+    SR_CUDA(cudaFuncSetAttribute(oz_split, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSplitSmem));
+    attr = true;
+  }
+  return SR_OK;
+}
+
+long long lower_tiles(int n) {
+  const int RT = (n + BM - 1) / BM, CT = (n + BN - 1) / BN;
+  long long cnt = 0;
+  for (int i = 0; i < RT; i++) cnt += std::min(CT, 2 * i + 2);
+  return cnt;
+}
 
 // Blocks are processed in groups whose digit slices fit a fixed budget (all blocks at once
 // when they fit; the buffer is reused group by group otherwise).
@@ -484,12 +581,7 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
   unsigned long long* mx = a.take<unsigned long long>(mc);
   int* expo = a.take<int>(mc);
 
-  static bool attr = false;
-  if (!attr) {
-    SR_CUDA(cudaFuncSetAttribute(gram_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
-    SR_CUDA(cudaFuncSetAttribute(oz_split, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSplitSmem));
-    attr = true;
-  }
+  SR_TRY(set_attrs());
   long long soff = 0;
   for (const Group& G : groups) {
     const long long c0 = offs[G.b0], nc = G.ncols;
@@ -510,7 +602,6 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
     P.Kp = Kp;
     P.kstages = (int)(2 * Kp / BKB);
     P.spc = kChunkK / BKB;
-    P.S = S;
     P.expo = expo;
     long long tiles = 0;
     for (int k = 0; k < P.nblk; k++) {
@@ -518,14 +609,13 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
       Blk& B = P.b[k];
       B.n = (int)(offs[b + 1] - offs[b]);
       B.col0 = offs[b] - c0;
-      B.soff = soff;
+      B.C = S + soff;
+      B.ldc = B.n;
       soff += (long long)B.n * B.n;
       B.RT = (B.n + BM - 1) / BM;
       B.CT = (B.n + BN - 1) / BN;
       B.tile_begin = tiles;
-      long long cnt = 0;
-      for (int i = 0; i < B.RT; i++) cnt += std::min(B.CT, 2 * i + 2);
-      tiles += 2 * cnt;
+      tiles += 2 * lower_tiles(B.n);
     }
     P.total_tiles = tiles;
     CUtensorMap ma, mb2;
@@ -533,10 +623,59 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
     SR_TRY(make_map(mb2, E, Kp, nc, BN));
     const unsigned grid = (unsigned)std::min<long long>(tiles, kNumSMs);
     timer_begin("gram_i8", st);
-    gram_i8<<<grid, kThreads, kSmem, st>>>(ma, mb2, P);
+    gram_i8<MODE_HERM><<<grid, kThreads, kSmem, st>>>(ma, mb2, P);
     timer_end(st);
     SR_LAUNCHED();
   }
+  return SR_OK;
+}
+
+size_t trail_workspace_bytes(long long m, long long K) {
+  const long long Kp = pad_k(K);
+  return round256((size_t)kSlices * 3 * Kp * m) + round256((size_t)m * 4);
+}
+
+sr_status trail_update_i8(const double2* L, long long ldl, long long m, long long K, double2* C, long long ldc,
+                          void* ws, size_t ws_bytes, int max_ctas, cudaStream_t st) {
+  if (m <= 0 || K <= 0) return SR_OK;
+  const long long Kp = pad_k(K);
+  if (2 * Kp > kChunkK || m >= (1LL << 31) / kSlices) {
+    set_error("trail_update_i8: K or m too large");
+    return SR_ERR_INVALID;
+  }
+  if (ws_bytes < trail_workspace_bytes(m, K)) {
+    set_error("trail_update_i8: workspace too small");
+    return SR_ERR_WORKSPACE;
+  }
+  SR_TRY(set_attrs());
+  Arena a(ws, ws_bytes);
+  int8_t* E = a.take<int8_t>((size_t)kSlices * 3 * Kp * m);
+  int* expo = a.take<int>(m);
+  oz_split_rows<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(L, ldl, (int)m, (int)K, (int)Kp, E, expo);
+  SR_LAUNCHED();
+  Params P{};
+  P.nblk = 1;
+  P.Kp = Kp;
+  P.kstages = (int)(2 * Kp / BKB);
+  P.spc = kChunkK / BKB;
+  P.expo = expo;
+  Blk& B = P.b[0];
+  B.col0 = 0;
+  B.C = C;
+  B.ldc = ldc;
+  B.n = (int)m;
+  B.RT = (B.n + BM - 1) / BM;
+  B.CT = (B.n + BN - 1) / BN;
+  B.tile_begin = 0;
+  P.total_tiles = 2 * lower_tiles(B.n);
+  CUtensorMap ma, mb;
+  SR_TRY(make_map(ma, E, Kp, m, BM));
+  SR_TRY(make_map(mb, E, Kp, m, BN));
+  const unsigned grid = (unsigned)std::min<long long>(P.total_tiles, max_ctas > 0 ? max_ctas : kNumSMs);
+  timer_begin("trail_i8", st);
+  gram_i8<MODE_SUB><<<grid, kThreads, kSmem, st>>>(ma, mb, P);
+  timer_end(st);
+  SR_LAUNCHED();
   return SR_OK;
 }
 

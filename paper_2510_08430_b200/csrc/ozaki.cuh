@@ -16,5 +16,13 @@ size_t workspace_bytes(long long ns, int nblk, const int64_t* offs);
 sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double2* A, long long lda, double2* S,
                        void* ws, size_t ws_bytes, cudaStream_t st);
 
+// Cholesky trailing update C[i][j] -= sum_k L[i][k] conj(L[j][k]) for i >= j < m (lower
+// triangle only; C row-major with leading dimension ldc, L row-major along k with ldl),
+// by the same digit-slice tcgen05 engine.  K <= 8192.  max_ctas caps the persistent grid
+// (0 = one CTA per SM).
+size_t trail_workspace_bytes(long long m, long long K);
+sr_status trail_update_i8(const double2* L, long long ldl, long long m, long long K, double2* C, long long ldc,
+                          void* ws, size_t ws_bytes, int max_ctas, cudaStream_t st);
+
 }  // namespace oz
 }  // namespace sr

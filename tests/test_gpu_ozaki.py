@@ -154,3 +154,50 @@ def test_step_with_int8_engine(sr):
     S = ws[so:so + 16 * n_s].view(C128).cpu().numpy()
     for g, r in zip(packed_blocks(S, sr.block_offsets(w.widths)), blocks):
         assert rel(g, r) < 1e-11
+
+
+@pytest.fixture
+def int8_engine(sr):
+    prev = sr.sr_set_gram_engine(sr.GRAM_INT8)
+    yield
+    sr.sr_set_gram_engine(prev)
+
+
+@pytest.mark.parametrize("lam", [1e-3, 1.0])
+@pytest.mark.parametrize("ns,sizes", [(512, (220, 420)), (100, (64, 18, 130)), (300, (250,)), (700, (1000,)),
+                                      (2000, (1300, 257))])
+def test_block_solve_int8_trailing_updates(sr, int8_engine, ns, sizes, lam):
+    """sr_block_solve with the Cholesky trailing updates (K = 256 strips) on the int8 engine:
+    dtheta within 1e-9 of the oracle (the same bar as the FP64 path)."""
+    rng = np.random.default_rng(ns + 1)
+    n_p = sum(sizes)
+    offs = [0] + [int(x) for x in np.cumsum(sizes)]
+    O = rng.standard_normal((ns, n_p)) + 1j * rng.standard_normal((ns, n_p))
+    e = rng.standard_normal(ns) + 1j * rng.standard_normal(ns)
+    blocks = estimators.qgt_blocks(O, offs)
+    F = estimators.force(O, e)
+    Sp = np.concatenate([b.ravel() for b in blocks])
+    d = torch.empty(n_p, dtype=C128, device=dev())
+    info = torch.full((1,), -5, dtype=torch.int32, device=dev())
+    sr.sr_block_solve(offs, T(Sp), T(F), lam, d, info=info)
+    ref = solvers.block_solve(blocks, F, offs, lam)
+    assert info.item() == 0
+    assert rel(d.cpu().numpy(), ref) < 1e-9
+
+
+def test_full_and_ntk_int8(sr, int8_engine):
+    """Comparison paths with the int8 trailing updates: full-QGT and NTK solves agree with the
+    oracle and with each other (push-through identity)."""
+    w = workloads.CONFIGS[0]
+    spins, params = workloads.make_inputs(w)
+    O = network.jacobian(params, spins)
+    e = hamiltonian.local_energies(params, spins, hamiltonian.bonds_for(w))
+    A, et = estimators.scaled_centered(O, e)
+    F = estimators.force(O, e)
+    d_full = torch.empty(w.n_params, dtype=C128, device=dev())
+    d_ntk = torch.empty(w.n_params, dtype=C128, device=dev())
+    sr.sr_full_qgt_solve(T(A), T(F), w.lam, d_full)
+    sr.sr_ntk_solve(T(A), T(et), w.lam, d_ntk)
+    ref = solvers.full_solve(estimators.qgt_full(O), F, w.lam)
+    assert rel(d_full.cpu().numpy(), ref) < 1e-9
+    assert rel(d_ntk.cpu().numpy(), ref) < 1e-9
