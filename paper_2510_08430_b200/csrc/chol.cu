@@ -9,12 +9,15 @@
 //   chol_diag        factor the 64x64 diagonal tile in shared memory, form its inverse
 //                    Linv_p, and y_p = Linv_p b_p (forward substitution folded in)
 //   trsm (engine)    L_ip = A_ip Linv_p^H for every row tile i > p      (DMMA, NH/STORE)
-//   chol_rhs_update  b_i -= L_ip y_p
+//   (chol_diag also subtracts the strip's earlier panels from its own 64 rows of b)
 //   inner (engine)   A_ij -= L_ip L_jp^H for the strip's later columns j (DMMA, NH/SUB)
-// and after every strip of 4 panels one deferred trailing update with K = 256:
+// and after every strip of 4 panels chol_rhs_update (b_i -= L_i,strip y_strip for the rows
+// below) and one deferred trailing update with K = 256:
 //   trail (engine)   A_ij -= L_i,strip L_j,strip^H for i >= j beyond the strip (NH/SUB)
 // then back substitution L^H x = y panel by panel (x_p = Linv_p^H y_p, then
 // y_{<p} -= L_p,<p^H x_p) and dtheta = -x.
+#include <cstdlib>
+
 #include "chol.cuh"
 #include "gram.cuh"
 #include "ozaki.cuh"
@@ -71,7 +74,9 @@ __device__ __forceinline__ void cfma_conjb(double2& acc, double2 a, double2 b) {
   acc.y = fma(-a.x, b.y, acc.y);
 }
 
-// (a) warp 0: D = L L^H for the 16x16 block at (o, o) of T, in place.
+// (a) warp 0: D = L L^H for the 16x16 block at (o, o) of T, in place.  Lane r < 16 holds
+// row r; step c scales column c, publishes it to T and applies the rank-1 update to the
+// later columns of its row, reading L[s][c] back as shared-memory broadcasts.
 __device__ __forceinline__ void factor16(double2* T, int o, int lane, double* dinv, int* bad) {
   double2 d[16];
   const int r = lane;
@@ -80,7 +85,12 @@ __device__ __forceinline__ void factor16(double2* T, int o, int lane, double* di
     d[s] = (r < 16 && s <= r) ? T[(o + r) * LDT + o + s] : make_double2(0.0, 0.0);
 #pragma unroll
   for (int c = 0; c < 16; c++) {
-    double piv = __shfl_sync(0xffffffffu, d[c].x, c);
+    // pivot through shared memory: shuffles in this (warp-uniform but not provably
+    // convergent) branch would compile to WARPSYNC.COLLECTIVE sequences
+    if (r == c) dinv[o + c] = d[c].x;
+    __syncwarp();
+    double piv = dinv[o + c];
+    __syncwarp();
     if (!(piv > 0.0)) {
       if (lane == 0 && *bad == 0) *bad = o + c + 1;
       piv = 1.0;
@@ -88,14 +98,14 @@ __device__ __forceinline__ void factor16(double2* T, int o, int lane, double* di
     const double isd = rsqrt(piv);
     if (r == c) d[c] = make_double2(piv * isd, 0.0);
     else if (r > c) d[c] = cscale(d[c], isd);
+    if (r < 16 && r >= c) T[(o + r) * LDT + o + c] = d[c];
     if (lane == 0) dinv[o + c] = isd;
+    __syncwarp();
 #pragma unroll
     for (int s = 1; s < 16; s++) {
       if (s <= c) continue;
-      double2 ls;
-      ls.x = __shfl_sync(0xffffffffu, d[c].x, s);
-      ls.y = __shfl_sync(0xffffffffu, d[c].y, s);
-      if (r >= s) {
+      const double2 ls = T[(o + s) * LDT + o + c];   // L[s][c]
+      if (r >= s && r < 16) {
         double2 v = d[s];
         v.x -= d[c].x * ls.x + d[c].y * ls.y;
         v.y -= d[c].y * ls.x - d[c].x * ls.y;
@@ -103,30 +113,36 @@ __device__ __forceinline__ void factor16(double2* T, int o, int lane, double* di
       }
     }
   }
-  if (r < 16) {
-#pragma unroll
-    for (int s = 0; s < 16; s++)
-      if (s <= r) T[(o + r) * LDT + o + s] = d[s];
-  }
 }
 
-// (b) row r: x D^H = A[r, o:o+16] with D = L[o:o+16, o:o+16] (diagonal real, 1/D_cc in dinv).
-__device__ __forceinline__ void trsm_row(double2* T, int o, int r, const double* dinv) {
-  double2 a[16];
+// (b) rows below the block solve x D^H = A[r, o:o+16] with D = L[o:o+16, o:o+16]
+// (diagonal real, 1/D_cc in dinv): a quad per row, lane q holding entries m = q mod 4;
+// step c: x_c = a_c / D_cc from the owner lane, shuffled inside the quad, then
+// a_m -= x_c conj(D[m][c]) for m > c.
+__device__ __forceinline__ void trsm_quad(double2* T, int o, int r, int q, const double* dinv) {
+  double2 a[4];
 #pragma unroll
-  for (int m = 0; m < 16; m++) a[m] = T[r * LDT + o + m];
+  for (int k = 0; k < 4; k++) a[k] = T[r * LDT + o + 4 * k + q];
 #pragma unroll
   for (int c = 0; c < 16; c++) {
-    a[c] = cscale(a[c], dinv[o + c]);
+    if (q == (c & 3)) {   // owner: x_c final, published in place
+      a[c >> 2] = cscale(a[c >> 2], dinv[o + c]);
+      T[r * LDT + o + c] = a[c >> 2];
+    }
+    __syncwarp();
+    const double2 x = T[r * LDT + o + c];
 #pragma unroll
-    for (int m = c + 1; m < 16; m++) {
-      const double2 dm = T[(o + m) * LDT + o + c];   // D[m][c]; a[m] -= x_c conj(D[m][c])
-      a[m].x -= a[c].x * dm.x + a[c].y * dm.y;
-      a[m].y -= a[c].y * dm.x - a[c].x * dm.y;
+    for (int k = 0; k < 4; k++) {
+      const int m = 4 * k + q;
+      if (m > c) {
+        const double2 dm = T[(o + m) * LDT + o + c];
+        a[k].x -= x.x * dm.x + x.y * dm.y;
+        a[k].y -= x.y * dm.x - x.x * dm.y;
+      }
     }
   }
 #pragma unroll
-  for (int m = 0; m < 16; m++) T[r * LDT + o + m] = a[m];
+  for (int k = 0; k < 4; k++) T[r * LDT + o + 4 * k + q] = a[k];
 }
 
 // Lower-triangle patch index e -> (pi, pj), pi >= pj.
@@ -186,7 +202,7 @@ __device__ __forceinline__ void inv16(const double2* T, double2* X, int o, int l
   }
 }
 
-__global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, int p) {
+__global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, int p, int p0) {
   extern __shared__ double2 dsm[];
   double2* T = dsm;              // [64][LDT]: A (lower) -> L
   double2* X = dsm + NB * LDT;   // [64][LDT]: Linv (lower)
@@ -200,7 +216,17 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
     const int r = e >> 6, c = e & 63;
     if (c <= r) T[r * LDT + c] = tile[(long long)r * np + c];
   }
-  if (t < NB) bsh[t] = B.rhs[(long long)p * NB + t];
+  {   // b_p -= sum over the strip's earlier panels q in [p0, p) of L_pq y_q (rows of panel p)
+    const int r = t >> 2, q = t & 3;
+    const double2* lrow = B.Fm + ((long long)p * NB + r) * np;
+    double2 s2 = make_double2(0.0, 0.0);
+    for (long long c = (long long)p0 * NB + q; c < (long long)p * NB; c += 4) cfma(s2, lrow[c], B.rhs[c]);
+    s2.x += __shfl_xor_sync(0xffffffffu, s2.x, 1);
+    s2.y += __shfl_xor_sync(0xffffffffu, s2.y, 1);
+    s2.x += __shfl_xor_sync(0xffffffffu, s2.x, 2);
+    s2.y += __shfl_xor_sync(0xffffffffu, s2.y, 2);
+    if (q == 0) bsh[r] = csub(B.rhs[(long long)p * NB + r], s2);
+  }
   if (t == 0) bad = 0;
   __syncthreads();
   for (int k = 0; k < 4; k++) {
@@ -208,7 +234,7 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
     if (warp == 0) factor16(T, o, lane, dinv, &bad);
     __syncthreads();
     if (k < 3) {
-      if (t < NB - o - 16) trsm_row(T, o, o + 16 + t, dinv);
+      if (t < 4 * (NB - o - 16)) trsm_quad(T, o, o + 16 + (t >> 2), t & 3, dinv);
       __syncthreads();
       syrk16(T, o, t);
       __syncthreads();
@@ -281,17 +307,15 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
   }
 }
 
-// b_i -= sum_c L[i][p*64 + c] y_p[c] for rows i >= (p+1)*64 (one warp per row).
-__global__ void chol_rhs_update(const CholBlock B, int p) {
+// b_i -= sum_{c in [c0, c1)} L[i][c] y[c] for rows i >= c1 (the strip's panels applied to the
+// right-hand side of every later row at once; one warp per row).
+__global__ void chol_rhs_update(const CholBlock B, long long c0, long long c1) {
   const long long np = B.npad;
-  const long long r0 = (long long)(p + 1) * NB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double2* y = B.rhs + (long long)p * NB;
-  const double2 y0 = y[lane], y1 = y[lane + 32];
-  for (long long r = r0 + (long long)blockIdx.x * 8 + warp; r < np; r += (long long)gridDim.x * 8) {
-    const double2* row = B.Fm + r * np + (long long)p * NB;
-    double2 s = cmul(row[lane], y0);
-    cfma(s, row[lane + 32], y1);
+  for (long long r = c1 + (long long)blockIdx.x * 8 + warp; r < np; r += (long long)gridDim.x * 8) {
+    const double2* row = B.Fm + r * np;
+    double2 s = make_double2(0.0, 0.0);
+    for (long long c = c0 + lane; c < c1; c += 32) cfma(s, row[c], B.rhs[c]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
@@ -373,6 +397,19 @@ void carve_chol(Arena& a, CholSet& cs, const long long* sizes, int nblk) {
 
 namespace {
 
+// Persistent-grid cap of the int8 trailing update: with several blocks in flight, leave SMs
+// for the other blocks' latency-bound panel chains (SR_TRAIL_CTAS overrides, for tuning).
+int trail_ctas(int nblocks) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("SR_TRAIL_CTAS");
+    env = e ? atoi(e) : -1;
+  }
+  if (env >= 0) return env;
+  (void)nblocks;
+  return 0;   // measured: capping the grid slows the 3-block solve (trailing throughput bound)
+}
+
 // Factorisation + substitutions of ONE block on one stream (two-level blocking, see header).
 sr_status solve_block(CholSet& cs, int b, cudaStream_t st) {
   const CholBlock& B = cs.b[b];
@@ -386,7 +423,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st) {
     const int pend = std::min(p0 + kStrip, B.P);
     for (int p = p0; p < pend; p++) {
       timer_begin("chol_diag", st);
-      chol_diag<<<1, 256, kDiagSmem, st>>>(B, cs.info, p);
+      chol_diag<<<1, 256, kDiagSmem, st>>>(B, cs.info, p, p0);
       timer_end(st);
       SR_LAUNCHED();
       const long long m = B.npad - (long long)(p + 1) * NB;
@@ -403,22 +440,24 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st) {
       timer_begin("chol_trsm", st);
       SR_TRY((gram::launch<gram::NH, gram::STORE>(trsm, st)));
       timer_end(st);
-      dim3 g((unsigned)std::min<long long>((m + 7) / 8, 4 * kNumSMs), 1);
-      timer_begin("chol_rhs", st);
-      chol_rhs_update<<<g, 256, 0, st>>>(B, p);
-      timer_end(st);
-      SR_LAUNCHED();
       timer_begin("chol_inner", st);
       if (inner.count) SR_TRY((gram::launch<gram::NH, gram::SUB>(inner, st)));
       timer_end(st);
     }
     const long long m = B.npad - (long long)pend * NB;
+    if (m > 0) {   // the strip's y applied to the right-hand side of all later rows
+      dim3 g((unsigned)std::min<long long>((m + 7) / 8, 4 * kNumSMs), 1);
+      timer_begin("chol_rhs", st);
+      chol_rhs_update<<<g, 256, 0, st>>>(B, (long long)p0 * NB, (long long)pend * NB);
+      timer_end(st);
+      SR_LAUNCHED();
+    }
     if (m > 0) {   // deferred trailing update of the strip, K = 64 * (pend - p0)
       const double2* lp = B.Fm + (long long)pend * NB * B.npad + (long long)p0 * NB;
       double2* trailing = B.Fm + (long long)pend * NB * B.npad + (long long)pend * NB;
       if (i8) {   // int8 digit-slice tcgen05 engine (ozaki.cu), lower triangle
         SR_TRY(oz::trail_update_i8(lp, B.npad, m, (long long)(pend - p0) * NB, trailing, B.npad, B.tws, B.tws_bytes,
-                                   0, st));
+                                   trail_ctas(cs.count), st));
       } else {
         gram::ProbSet trail{};
         gram::add_prob(trail, lp, B.npad, lp, B.npad, trailing, B.npad, (int)m, (int)m,

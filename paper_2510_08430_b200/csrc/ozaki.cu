@@ -45,7 +45,8 @@ constexpr int kStageBytes = kSlices * (kASlice + kBSlice);   // 86016
 constexpr int kChunkK = 16384;            // K' per exact int32 accumulation
 constexpr int kBand = 8;                  // row panels per rasterisation band
 constexpr int kMaxBlk = 24;
-constexpr int kThreads = 192;             // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
+constexpr int kEpiWarps = 8;              // two per TMEM lane quarter, 32 columns each
+constexpr int kThreads = 64 + 32 * kEpiWarps;   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2.. epilogue
 constexpr size_t kSmem = (size_t)kStages * kStageBytes + 1024 + 256;
 // tcgen05 instruction descriptor: D s32 (bits 4-5 = 2), A/B signed int8 (bits 7-9, 10-12 = 1),
 // both K-major, N >> 3 at bit 17, M >> 4 at bit 24.
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(empty0 + 8 * s, 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 4);
+    mbar_init(tempty, kEpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm_a) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm_b) : "memory");
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {   // ---------------- epilogue: TMEM -> FP64 recombination -> S
     const int q4 = warp & 3;             // TMEM lane quarter this warp may access
     const int rl = q4 * 32 + lane;       // tile row of this thread
+    const int c0 = ((warp - 2) >> 2) * (BN / 2);   // first of this warp's 32 tile columns
     const int nchunks = (P.kstages + P.spc - 1) / P.spc;
     uint32_t c = 0;
     for (long long t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
@@ -284,69 +286,71 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ei = row_ok ? P.expo[B.col0 + i] : 0;
       double* Cb = reinterpret_cast<double*>(B.C);
       const long long ldc = B.ldc;
-      if (MODE == MODE_SUB) {
-        // C -= G on the lower triangle by fire-and-forget reductions in L2 (red.global.add.f64):
-        // no read latency in the epilogue, and each element receives exactly one addend per
-        // launch (Re pass -> .x, Im pass -> .y), so the result is deterministic.
-        mbar_wait(tfull, c & 1);
-        tc_fence_after();
-#pragma unroll 1
-        for (int cc = 0; cc < BN / 8; cc++) {
-          uint32_t g[kSlices][8];
-#pragma unroll
-          for (int tt = 0; tt < kSlices; tt++)
-            tmem_ld8(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(tt * BN + cc * 8), g[tt]);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 8; e++) {
-            const int j = J * BN + cc * 8 + e;
-            if (!row_ok || j >= n || j > i) continue;
-            double v = (double)(int)g[0][e];
-#pragma unroll
-            for (int tt = 1; tt < kSlices; tt++) v = fma(v, 256.0, (double)(int)g[tt][e]);
-            atomicAdd(Cb + 2 * ((long long)i * ldc + j) + pass, -pow2_scale(v, ei + P.expo[B.col0 + j] - 60));
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty);
-        c++;
-        continue;
-      }
       for (int ch = 0; ch < nchunks; ch++, c++) {
         mbar_wait(tfull, c & 1);
         tc_fence_after();
-#pragma unroll 1
-        for (int cc = 0; cc < BN / 8; cc++) {
+        // Phase 1: TMEM -> registers, the seven digit-diagonal sums combined by Horner
+        // (exact int32 -> FP64), then TMEM is released so the next tile's MMAs overlap
+        // phase 2 (scaling and the global writes).
+        double vals[BN / 2];
+#pragma unroll
+        for (int cc = 0; cc < BN / 16; cc++) {
           uint32_t g[kSlices][8];
 #pragma unroll
           for (int tt = 0; tt < kSlices; tt++)
-            tmem_ld8(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(tt * BN + cc * 8), g[tt]);
+            tmem_ld8(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(tt * BN + c0 + cc * 8), g[tt]);
           tmem_wait_ld();
-          if (!row_ok) continue;
 #pragma unroll
           for (int e = 0; e < 8; e++) {
-            const int j = J * BN + cc * 8 + e;
-            if (j >= n || j > i) continue;
             double v = (double)(int)g[0][e];
 #pragma unroll
             for (int tt = 1; tt < kSlices; tt++) v = fma(v, 256.0, (double)(int)g[tt][e]);
-            double val = pow2_scale(v, ei + P.expo[B.col0 + j] - 60);
-            double* direct = Cb + 2 * ((long long)i * ldc + j) + pass;
-            if (ch > 0) val += *direct;
-            if (ch + 1 < nchunks) {
-              *direct = val;
-            } else if (i == j) {
-              *direct = pass ? 0.0 : val;
-            } else {
-              *direct = val;
-              Cb[2 * ((long long)j * ldc + i) + pass] = pass ? -val : val;
-            }
+            vals[cc * 8 + e] = v;
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty);
+        // Phase 2 (column exponents fetched once per lane, broadcast by shuffles)
+        const int jl = J * BN + c0 + lane;
+        const int ej_lane = jl < n ? P.expo[B.col0 + jl] : 0;
+        const int jb = J * BN + c0;
+        double* dp = Cb + 2 * ((long long)i * ldc + jb) + pass;   // C[i][j], j = jb + e
+        double* mp = Cb + 2 * ((long long)jb * ldc + i) + pass;   // C[j][i]
+        const long long mstep = 2 * ldc;
+#pragma unroll
+        for (int e = 0; e < BN / 2; e++, mp += mstep) {
+          const int ej = __shfl_sync(0xffffffffu, ej_lane, e);
+          const int j = jb + e;
+          if (!row_ok || j >= n || j > i) continue;
+          const double val = pow2_scale(vals[e], ei + ej - 60);
+          if (MODE == MODE_SUB) {
+            // C -= G on the lower triangle by a fire-and-forget reduction in L2
+            // (red.global.add.f64): each element receives exactly one addend per launch
+            // (Re pass -> .x, Im pass -> .y), so the result is deterministic.
+            atomicAdd(dp + 2 * e, -val);
+            continue;
+          }
+          if (nchunks == 1) {
+            if (i == j) {
+              dp[2 * e] = pass ? 0.0 : val;
+            } else {
+              dp[2 * e] = val;
+              *mp = pass ? -val : val;
+            }
+            continue;
+          }
+          double acc = val;
+          if (ch > 0) acc += dp[2 * e];
+          if (ch + 1 < nchunks) {
+            dp[2 * e] = acc;
+          } else if (i == j) {
+            dp[2 * e] = pass ? 0.0 : acc;
+          } else {
+            dp[2 * e] = acc;
+            *mp = pass ? -acc : acc;
+          }
+        }
       }
     }
   }
