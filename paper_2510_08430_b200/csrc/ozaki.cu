@@ -43,6 +43,11 @@ constexpr int kBSlice = BN * BKB;         // 4 KB
 constexpr int kAStage = kSlices * kASlice;
 constexpr int kStageBytes = kSlices * (kASlice + kBSlice);   // 86016
 constexpr int kChunkK = 16384;            // K' per exact int32 accumulation
+#ifndef SR_OZ_A_TMEM
+#define SR_OZ_A_TMEM 0   // measured slower: 23.4 vs 20.2 ms at configs[1] (profiles/r01_tcgen05_rate.txt)
+#endif
+constexpr bool kATmem = SR_OZ_A_TMEM;     // operand A staged into TMEM by tcgen05.cp
+constexpr uint32_t kACol = kSlices * BN;  // TMEM columns [448, 504): the A digits of one K step
 constexpr int kBand = 8;                  // row panels per rasterisation band
 constexpr int kMaxBlk = 24;
 constexpr int kEpiWarps = 8;              // two per TMEM lane quarter, 32 columns each
@@ -113,6 +118,15 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
                : "memory");
+}
+__device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(
+          d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(kIdesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc_) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;\n" ::"r"(taddr), "l"(sdesc_));
 }
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
   asm volatile(
@@ -251,13 +265,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sa = smem_base + s * kStageBytes, sb = sa + kAStage;
 #pragma unroll
           for (int ks = 0; ks < BKB / 32; ks++) {
+            if (kATmem) {
+              // A digits of this K step -> TMEM (7 x 128 lanes x 32 bytes = 56 columns), so the
+              // MMAs read only B through the shared-memory port.  tcgen05.cp and tcgen05.mma
+              // from this thread execute in issue order: the copy of step ks+1 cannot
+              // overtake the MMAs of step ks that read the same columns.
+#pragma unroll
+              for (int p = 0; p < kSlices; p++) tmem_cp_128x256b(tmem + kACol + 8 * p, sdesc(sa + p * kASlice + ks * 32));
+            }
 #pragma unroll
             for (int p = 0; p < kSlices; p++) {
               const uint64_t ad = sdesc(sa + p * kASlice + ks * 32);
 #pragma unroll
               for (int q = 0; q + p < kSlices; q++) {
                 const uint64_t bd = sdesc(sb + q * kBSlice + ks * 32);
-                mma_i8(tmem + (uint32_t)((p + q) * BN), ad, bd, (kin > 0 || ks > 0 || p > 0) ? 1u : 0u);
+                const uint32_t acc = (kin > 0 || ks > 0 || p > 0) ? 1u : 0u;
+                if (kATmem) mma_i8_ts(tmem + (uint32_t)((p + q) * BN), tmem + kACol + 8 * p, bd, acc);
+                else mma_i8(tmem + (uint32_t)((p + q) * BN), ad, bd, acc);
               }
             }
           }
