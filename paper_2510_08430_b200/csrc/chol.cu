@@ -14,8 +14,8 @@
 // and after every strip of 4 panels chol_rhs_update (b_i -= L_i,strip y_strip for the rows
 // below) and one deferred trailing update with K = 256:
 //   trail (engine)   A_ij -= L_i,strip L_j,strip^H for i >= j beyond the strip (NH/SUB)
-// then back substitution L^H x = y panel by panel (x_p = Linv_p^H y_p, then
-// y_{<p} -= L_p,<p^H x_p) and dtheta = -x.
+// then back substitution L^H x = y strip by strip (x_p = Linv_p^H y_p inside the strip,
+// then y_{<strip} -= L_strip,<^H x_strip) and dtheta = -x.
 #include <cstdlib>
 
 #include "chol.cuh"
@@ -325,42 +325,64 @@ __global__ void chol_rhs_update(const CholBlock B, long long c0, long long c1) {
   }
 }
 
-// x_p = Linv_p^H y_p (into xout), then y_c -= sum_c' conj(L[p*64 + c'][c]) x_p[c'] for c < p*64.
-// Each CTA owns 64 columns; 256 threads = 64 columns x 4 row quarters, reduced in a fixed
-// order through shared memory (deterministic).
-__global__ void __launch_bounds__(256) chol_back(const CholBlock B, int p) {
-  __shared__ double2 ys[NB];
+// Back substitution L^H x = y by strips of panels [p0, pend), two launches per strip:
+// chol_back_strip (one CTA): for p = pend-1 .. p0: x_p = Linv_p^H y_p, then
+//   y_q -= L_pq^H x_p for the strip's earlier panels q in [p0, p);
+// chol_back_rest (one CTA per 64 columns c < 64 p0): y_c -= sum_{r in strip} conj(L[r][c]) x_r.
+// Reductions run in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) chol_back_strip(const CholBlock B, int p0, int pend) {
+  __shared__ double2 ys[kStrip][NB];
   __shared__ double2 xs[NB];
+  const long long np = B.npad;
+  const int t = threadIdx.x, c = t >> 2, q4 = t & 3;
+  for (int e = t; e < (pend - p0) * NB; e += 256) ys[e >> 6][e & 63] = B.rhs[(long long)p0 * NB + e];
+  __syncthreads();
+  for (int p = pend - 1; p >= p0; p--) {
+    const double2* linv = B.linv + (long long)p * NB * NB;
+    double2 sx = make_double2(0.0, 0.0);
+    for (int r = c + q4; r < NB; r += 4) cfma_conj(sx, linv[r * NB + c], ys[p - p0][r]);
+    sx.x += __shfl_xor_sync(0xffffffffu, sx.x, 1);
+    sx.y += __shfl_xor_sync(0xffffffffu, sx.y, 1);
+    sx.x += __shfl_xor_sync(0xffffffffu, sx.x, 2);
+    sx.y += __shfl_xor_sync(0xffffffffu, sx.y, 2);
+    if (q4 == 0) {
+      xs[c] = sx;
+      B.xout[(long long)p * NB + c] = sx;
+    }
+    __syncthreads();
+    for (int q = p0; q < p; q++) {   // y_q[c] -= sum_r conj(L[p*64+r][q*64+c]) x_p[r]
+      const double2* lp = B.Fm + (long long)p * NB * np + (long long)q * NB + c;
+      double2 sy = make_double2(0.0, 0.0);
+      for (int r = q4; r < NB; r += 4) cfma_conj(sy, lp[(long long)r * np], xs[r]);
+      sy.x += __shfl_xor_sync(0xffffffffu, sy.x, 1);
+      sy.y += __shfl_xor_sync(0xffffffffu, sy.y, 1);
+      sy.x += __shfl_xor_sync(0xffffffffu, sy.x, 2);
+      sy.y += __shfl_xor_sync(0xffffffffu, sy.y, 2);
+      if (q4 == 0) ys[q - p0][c] = csub(ys[q - p0][c], sy);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) chol_back_rest(const CholBlock B, int p0, int pend) {
+  __shared__ double2 xs[kStrip * NB];
   __shared__ double2 red[4][NB];
   const long long np = B.npad;
-  const int t = threadIdx.x;
-  if (t < NB) ys[t] = B.rhs[(long long)p * NB + t];
+  const int t = threadIdx.x, cl = t & 63, rq = t >> 6;
+  const int nr = (pend - p0) * NB;
+  for (int e = t; e < nr; e += 256) xs[e] = B.xout[(long long)p0 * NB + e];
   __syncthreads();
-  const double2* linv = B.linv + (long long)p * NB * NB;
-  {
-    const int c = t >> 2, q = t & 3;
+  const long long ncol = (long long)p0 * NB;
+  for (long long cb = (long long)blockIdx.x * NB; cb < ncol; cb += (long long)gridDim.x * NB) {
+    const long long c = cb + cl;
     double2 s = make_double2(0.0, 0.0);
-    for (int r = c + q; r < NB; r += 4) cfma_conj(s, linv[r * NB + c], ys[r]);
-    s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
-    s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
-    s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
-    s.y += __shfl_xor_sync(0xffffffffu, s.y, 2);
-    if (q == 0) xs[c] = s;
-  }
-  __syncthreads();
-  if (blockIdx.x == 0 && t < NB) B.xout[(long long)p * NB + t] = xs[t];
-  const long long ncol = (long long)p * NB;
-  const int cl = t & 63, rq = t >> 6;
-  for (long long c0 = (long long)blockIdx.x * NB; c0 < ncol; c0 += (long long)gridDim.x * NB) {
-    const long long c = c0 + cl;
-    double2 s = make_double2(0.0, 0.0);
-    const double2* col = B.Fm + ((long long)p * NB + rq * 16) * np + c;
+    const double2* col = B.Fm + ((long long)p0 * NB) * np + c;
 #pragma unroll 4
-    for (int r = 0; r < 16; r++) cfma_conj(s, col[(long long)r * np], xs[rq * 16 + r]);
+    for (int r = rq; r < nr; r += 4) cfma_conj(s, col[(long long)r * np], xs[r]);
     red[rq][cl] = s;
     __syncthreads();
     if (rq == 0) {
-      double2 v = cadd(cadd(red[0][cl], red[1][cl]), cadd(red[2][cl], red[3][cl]));
+      const double2 v = cadd(cadd(red[0][cl], red[1][cl]), cadd(red[2][cl], red[3][cl]));
       B.rhs[c] = csub(B.rhs[c], v);
     }
     __syncthreads();
@@ -468,12 +490,16 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st) {
       }
     }
   }
-  for (int p = B.P - 1; p >= 0; p--) {
-    dim3 g((unsigned)std::max(1, p), 1);
+  for (int p0 = (B.P - 1) / kStrip * kStrip; p0 >= 0; p0 -= kStrip) {
+    const int pend = std::min(p0 + kStrip, B.P);
     timer_begin("chol_back", st);
-    chol_back<<<g, 256, 0, st>>>(B, p);
-    timer_end(st);
+    chol_back_strip<<<1, 256, 0, st>>>(B, p0, pend);
     SR_LAUNCHED();
+    if (p0 > 0) {
+      chol_back_rest<<<(unsigned)std::min(p0, 4 * kNumSMs), 256, 0, st>>>(B, p0, pend);
+      SR_LAUNCHED();
+    }
+    timer_end(st);
   }
   return SR_OK;
 }
