@@ -75,22 +75,23 @@ __device__ __forceinline__ void cfma_conjb(double2& acc, double2 a, double2 b) {
 }
 
 // (a) warp 0: D = L L^H for the 16x16 block at (o, o) of T, in place.  Lane r < 16 holds
-// row r; step c scales column c, publishes it to T and applies the rank-1 update to the
-// later columns of its row, reading L[s][c] back as shared-memory broadcasts.
+// row r; step c scales column c, publishes it to T (one __syncwarp) and applies the
+// rank-1 update to the later columns of its row, reading L[s][c] back as shared-memory
+// broadcasts.  Every lane also keeps the running diagonal dg[s] = A_ss - sum_k |L_sk|^2
+// (the same arithmetic as the owner's update of its own diagonal entry), so each step's
+// pivot is available locally without a broadcast.
 __device__ __forceinline__ void factor16(double2* T, int o, int lane, double* dinv, int* bad) {
   double2 d[16];
+  double dg[16];
   const int r = lane;
 #pragma unroll
-  for (int s = 0; s < 16; s++)
+  for (int s = 0; s < 16; s++) {
     d[s] = (r < 16 && s <= r) ? T[(o + r) * LDT + o + s] : make_double2(0.0, 0.0);
+    dg[s] = T[(o + s) * LDT + o + s].x;
+  }
 #pragma unroll
   for (int c = 0; c < 16; c++) {
-    // pivot through shared memory: shuffles in this (warp-uniform but not provably
-    // convergent) branch would compile to WARPSYNC.COLLECTIVE sequences
-    if (r == c) dinv[o + c] = d[c].x;
-    __syncwarp();
-    double piv = dinv[o + c];
-    __syncwarp();
+    double piv = dg[c];
     if (!(piv > 0.0)) {
       if (lane == 0 && *bad == 0) *bad = o + c + 1;
       piv = 1.0;
@@ -105,6 +106,7 @@ __device__ __forceinline__ void factor16(double2* T, int o, int lane, double* di
     for (int s = 1; s < 16; s++) {
       if (s <= c) continue;
       const double2 ls = T[(o + s) * LDT + o + c];   // L[s][c]
+      dg[s] -= ls.x * ls.x + ls.y * ls.y;
       if (r >= s && r < 16) {
         double2 v = d[s];
         v.x -= d[c].x * ls.x + d[c].y * ls.y;
