@@ -392,6 +392,21 @@ EnWs carve_en(Arena& a, const NetDesc& net, long long ns, long long nb) {
 
 }  // namespace
 
+template <int RB>
+sr_status launch_jac(const NetDesc& net, const double2* theta, const JacWs& w, const int8_t* spins, long long ns,
+                     double* log_psi, unsigned grid, size_t sm, cudaStream_t st) {
+  SR_TRY(set_smem(jac_forward<RB>, sm));
+  SR_TRY(set_smem(jac_backward<RB>, sm));
+  jac_forward<RB><<<grid, kThreads, sm, st>>>(net, theta, w.wt, spins, ns, w.hs, w.ts,
+                                              reinterpret_cast<double2*>(log_psi));
+  SR_LAUNCHED();
+  if (net.L > 1) {
+    jac_backward<RB><<<grid, kThreads, sm, st>>>(net, theta, w.ts, ns);
+    SR_LAUNCHED();
+  }
+  return SR_OK;
+}
+
 sr_status jacobian_impl(const NetDesc& net, const double* theta_d, const int8_t* spins, long long ns,
                         double* log_psi, double* O, long long ldo, void* ws, size_t ws_bytes,
                         cudaStream_t st) {
@@ -405,29 +420,18 @@ sr_status jacobian_impl(const NetDesc& net, const double* theta_d, const int8_t*
   const double2* theta = reinterpret_cast<const double2*>(theta_d);
   transpose_weights<<<64, kThreads, 0, st>>>(net, theta, w.wt);
   SR_LAUNCHED();
-  const int rb = rows_per_tile(net);
+  // Row tile: the largest of 32/16/8 rows (shared-memory bound by the widths) that still
+  // gives two waves of CTAs over the 148 SMs (configs[1]: 4096 rows -> 8 rows, 512 CTAs).
+  int rb = rows_per_tile(net);
+  while (rb > 8 && (ns + rb - 1) / rb < 2 * kNumSMs) rb /= 2;
   const size_t sm = tile_smem(net, rb);
   const unsigned grid = (unsigned)((ns + rb - 1) / rb);
   if (rb == 32) {
-    SR_TRY(set_smem(jac_forward<32>, sm));
-    SR_TRY(set_smem(jac_backward<32>, sm));
-    jac_forward<32><<<grid, kThreads, sm, st>>>(net, theta, w.wt, spins, ns, w.hs, w.ts,
-                                                reinterpret_cast<double2*>(log_psi));
-    SR_LAUNCHED();
-    if (net.L > 1) {
-      jac_backward<32><<<grid, kThreads, sm, st>>>(net, theta, w.ts, ns);
-      SR_LAUNCHED();
-    }
+    SR_TRY(launch_jac<32>(net, theta, w, spins, ns, log_psi, grid, sm, st));
+  } else if (rb == 16) {
+    SR_TRY(launch_jac<16>(net, theta, w, spins, ns, log_psi, grid, sm, st));
   } else {
-    SR_TRY(set_smem(jac_forward<16>, sm));
-    SR_TRY(set_smem(jac_backward<16>, sm));
-    jac_forward<16><<<grid, kThreads, sm, st>>>(net, theta, w.wt, spins, ns, w.hs, w.ts,
-                                                reinterpret_cast<double2*>(log_psi));
-    SR_LAUNCHED();
-    if (net.L > 1) {
-      jac_backward<16><<<grid, kThreads, sm, st>>>(net, theta, w.ts, ns);
-      SR_LAUNCHED();
-    }
+    SR_TRY(launch_jac<8>(net, theta, w, spins, ns, log_psi, grid, sm, st));
   }
   dim3 og((unsigned)ns, (unsigned)net.L);
   jac_outer<<<og, kThreads, 0, st>>>(net, spins, w.hs, w.ts, ns, reinterpret_cast<double2*>(O), ldo);
