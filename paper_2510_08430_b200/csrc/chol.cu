@@ -19,13 +19,16 @@
 #include <cstdlib>
 
 #include "chol.cuh"
+#include "chol_diag.cuh"
 #include "gram.cuh"
 #include "ozaki.cuh"
 
 namespace sr {
 namespace {
 
-constexpr int NB = 64;
+using cholk::NB;
+using cholk::chol_diag;
+using cholk::kDiagSmem;
 constexpr int kStrip = 4;   // panels per strip (deferred trailing update with K = 256)
 
 __global__ void chol_init(CholSet cs, double lam, int inplace) {
@@ -51,262 +54,6 @@ __global__ void chol_init(CholSet cs, double lam, int inplace) {
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < np;
        r += (long long)gridDim.x * blockDim.x)
     B.rhs[r] = r < n ? B.F[r] : make_double2(0.0, 0.0);
-}
-
-// One CTA per block: factor the 64x64 diagonal tile of panel p, form its inverse
-// X = Linv_p and y_p = Linv_p b_p.  Blocked by 16 (the latency of a 64-step column
-// recursion with a block barrier per step is what limited the unblocked forms):
-//   for each 16-column block k (offset o = 16k):
-//     (a) warp 0 factors D_k = A[o:o+16, o:o+16] in registers, lane r = row r, columns
-//         broadcast by shuffles, 1/sqrt of each pivot kept in dinv;
-//     (b) rows r >= o+16 solve x D_k^H = A[r, o:o+16] (one thread per row, right-looking);
-//     (c) A[r][s] -= sum_m L[r][o+m] conj(L[s][o+m]) on the trailing lower triangle
-//         (2x2 register patches).
-//   inverse: X_kk = D_k^{-1} (warp k, lane j = column j), then by block distance d = 1..3:
-//     W_ik = sum_{j=k}^{i-1} L_ij X_jk and X_ik = -X_ii W_ik (i = k + d), 2x2 patches.
-constexpr int LDT = NB + 1;   // 1040-byte rows
-constexpr size_t kDiagSmem = (size_t)2 * NB * LDT * sizeof(double2);
-
-__device__ __forceinline__ void cfma_conjb(double2& acc, double2 a, double2 b) {   // acc += a conj(b)
-  acc.x = fma(a.x, b.x, acc.x);
-  acc.x = fma(a.y, b.y, acc.x);
-  acc.y = fma(a.y, b.x, acc.y);
-  acc.y = fma(-a.x, b.y, acc.y);
-}
-
-// (a) warp 0: D = L L^H for the 16x16 block at (o, o) of T, in place.  Lane r < 16 holds
-// row r; step c scales column c, publishes it to T (one __syncwarp) and applies the
-// rank-1 update to the later columns of its row, reading L[s][c] back as shared-memory
-// broadcasts.  Every lane also keeps the running diagonal dg[s] = A_ss - sum_k |L_sk|^2
-// (the same arithmetic as the owner's update of its own diagonal entry), so each step's
-// pivot is available locally without a broadcast.
-__device__ __forceinline__ void factor16(double2* T, int o, int lane, double* dinv, int* bad) {
-  double2 d[16];
-  double dg[16];
-  const int r = lane;
-#pragma unroll
-  for (int s = 0; s < 16; s++) {
-    d[s] = (r < 16 && s <= r) ? T[(o + r) * LDT + o + s] : make_double2(0.0, 0.0);
-    dg[s] = T[(o + s) * LDT + o + s].x;
-  }
-#pragma unroll
-  for (int c = 0; c < 16; c++) {
-    double piv = dg[c];
-    if (!(piv > 0.0)) {
-      if (lane == 0 && *bad == 0) *bad = o + c + 1;
-      piv = 1.0;
-    }
-    const double isd = rsqrt(piv);
-    if (r == c) d[c] = make_double2(piv * isd, 0.0);
-    else if (r > c) d[c] = cscale(d[c], isd);
-    if (r < 16 && r >= c) T[(o + r) * LDT + o + c] = d[c];
-    if (lane == 0) dinv[o + c] = isd;
-    __syncwarp();
-#pragma unroll
-    for (int s = 1; s < 16; s++) {
-      if (s <= c) continue;
-      const double2 ls = T[(o + s) * LDT + o + c];   // L[s][c]
-      dg[s] -= ls.x * ls.x + ls.y * ls.y;
-      if (r >= s && r < 16) {
-        double2 v = d[s];
-        v.x -= d[c].x * ls.x + d[c].y * ls.y;
-        v.y -= d[c].y * ls.x - d[c].x * ls.y;
-        d[s] = v;
-      }
-    }
-  }
-}
-
-// (b) rows below the block solve x D^H = A[r, o:o+16] with D = L[o:o+16, o:o+16]
-// (diagonal real, 1/D_cc in dinv): a quad per row, lane q holding entries m = q mod 4;
-// step c: x_c = a_c / D_cc from the owner lane, shuffled inside the quad, then
-// a_m -= x_c conj(D[m][c]) for m > c.
-__device__ __forceinline__ void trsm_quad(double2* T, int o, int r, int q, const double* dinv) {
-  double2 a[4];
-#pragma unroll
-  for (int k = 0; k < 4; k++) a[k] = T[r * LDT + o + 4 * k + q];
-#pragma unroll
-  for (int c = 0; c < 16; c++) {
-    if (q == (c & 3)) {   // owner: x_c final, published in place
-      a[c >> 2] = cscale(a[c >> 2], dinv[o + c]);
-      T[r * LDT + o + c] = a[c >> 2];
-    }
-    __syncwarp();
-    const double2 x = T[r * LDT + o + c];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const int m = 4 * k + q;
-      if (m > c) {
-        const double2 dm = T[(o + m) * LDT + o + c];
-        a[k].x -= x.x * dm.x + x.y * dm.y;
-        a[k].y -= x.y * dm.x - x.x * dm.y;
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < 4; k++) T[r * LDT + o + 4 * k + q] = a[k];
-}
-
-// Lower-triangle patch index e -> (pi, pj), pi >= pj.
-__device__ __forceinline__ void tri_patch(int e, int& pi, int& pj) {
-  pi = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
-  while ((pi + 1) * (pi + 2) / 2 <= e) pi++;
-  while (pi * (pi + 1) / 2 > e) pi--;
-  pj = e - pi * (pi + 1) / 2;
-}
-
-// (c) trailing update of rows/cols [o+16, 64) by the 16 columns L[:, o:o+16].
-__device__ __forceinline__ void syrk16(double2* T, int o, int t) {
-  const int b0 = o + 16, P = (NB - b0) / 2, cnt = P * (P + 1) / 2;
-  for (int e = t; e < cnt; e += 256) {
-    int pi, pj;
-    tri_patch(e, pi, pj);
-    const int r0 = b0 + 2 * pi, s0 = b0 + 2 * pj;
-    double2 acc[2][2] = {{make_double2(0.0, 0.0), make_double2(0.0, 0.0)},
-                         {make_double2(0.0, 0.0), make_double2(0.0, 0.0)}};
-#pragma unroll 4
-    for (int m = 0; m < 16; m++) {
-      const double2 lr0 = T[r0 * LDT + o + m], lr1 = T[(r0 + 1) * LDT + o + m];
-      const double2 ls0 = T[s0 * LDT + o + m], ls1 = T[(s0 + 1) * LDT + o + m];
-      cfma_conjb(acc[0][0], lr0, ls0);
-      cfma_conjb(acc[0][1], lr0, ls1);
-      cfma_conjb(acc[1][0], lr1, ls0);
-      cfma_conjb(acc[1][1], lr1, ls1);
-    }
-#pragma unroll
-    for (int u = 0; u < 2; u++)
-#pragma unroll
-      for (int v = 0; v < 2; v++)
-        if (r0 + u >= s0 + v) {
-          double2& x = T[(r0 + u) * LDT + s0 + v];
-          x = csub(x, acc[u][v]);
-        }
-  }
-}
-
-// X[o:o+16, o:o+16] = L[o:o+16, o:o+16]^{-1} (lane j < 16 = column j; zeros above the diagonal).
-__device__ __forceinline__ void inv16(const double2* T, double2* X, int o, int lane, const double* dinv) {
-  if (lane >= 16) return;
-  const int j = lane;
-  double2 b[16];
-#pragma unroll
-  for (int i = 0; i < 16; i++) b[i] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-#pragma unroll
-  for (int i = 0; i < 16; i++) {
-    const double2 x = cscale(b[i], dinv[o + i]);
-    X[(o + i) * LDT + o + j] = x;
-#pragma unroll
-    for (int m = i + 1; m < 16; m++) {
-      const double2 l = T[(o + m) * LDT + o + i];
-      b[m].x -= l.x * x.x - l.y * x.y;
-      b[m].y -= l.x * x.y + l.y * x.x;
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, int p, int p0) {
-  extern __shared__ double2 dsm[];
-  double2* T = dsm;              // [64][LDT]: A (lower) -> L
-  double2* X = dsm + NB * LDT;   // [64][LDT]: Linv (lower)
-  __shared__ double dinv[NB];
-  __shared__ double2 bsh[NB];
-  __shared__ int bad;
-  const long long np = B.npad;
-  double2* tile = B.Fm + (long long)p * NB * np + (long long)p * NB;
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  for (int e = t; e < NB * NB; e += 256) {
-    const int r = e >> 6, c = e & 63;
-    if (c <= r) T[r * LDT + c] = tile[(long long)r * np + c];
-  }
-  {   // b_p -= sum over the strip's earlier panels q in [p0, p) of L_pq y_q (rows of panel p)
-    const int r = t >> 2, q = t & 3;
-    const double2* lrow = B.Fm + ((long long)p * NB + r) * np;
-    double2 s2 = make_double2(0.0, 0.0);
-    for (long long c = (long long)p0 * NB + q; c < (long long)p * NB; c += 4) cfma(s2, lrow[c], B.rhs[c]);
-    s2.x += __shfl_xor_sync(0xffffffffu, s2.x, 1);
-    s2.y += __shfl_xor_sync(0xffffffffu, s2.y, 1);
-    s2.x += __shfl_xor_sync(0xffffffffu, s2.x, 2);
-    s2.y += __shfl_xor_sync(0xffffffffu, s2.y, 2);
-    if (q == 0) bsh[r] = csub(B.rhs[(long long)p * NB + r], s2);
-  }
-  if (t == 0) bad = 0;
-  __syncthreads();
-  for (int k = 0; k < 4; k++) {
-    const int o = 16 * k;
-    if (warp == 0) factor16(T, o, lane, dinv, &bad);
-    __syncthreads();
-    if (k < 3) {
-      if (t < 4 * (NB - o - 16)) trsm_quad(T, o, o + 16 + (t >> 2), t & 3, dinv);
-      __syncthreads();
-      syrk16(T, o, t);
-      __syncthreads();
-    }
-  }
-  if (t == 0 && bad && info) atomicCAS(info, 0, (int)(B.row_base + (long long)p * NB + bad));
-  if (warp < 4) inv16(T, X, 16 * warp, lane, dinv);
-  __syncthreads();
-  for (int d = 1; d < 4; d++) {
-    const int nbk = 4 - d;
-    const bool act = t < nbk * 64;
-    const int kb = t >> 6, ib = kb + d, pr = (t & 63) >> 3, pc = t & 7;
-    const int r0 = 16 * ib + 2 * pr, c0 = 16 * kb + 2 * pc;
-    double2 acc[2][2] = {{make_double2(0.0, 0.0), make_double2(0.0, 0.0)},
-                         {make_double2(0.0, 0.0), make_double2(0.0, 0.0)}};
-    if (act) {   // W_ik = sum_{m in blocks k..i-1} L[r][m] X[m][c]
-      for (int m = 16 * kb; m < 16 * ib; m++) {
-        const double2 l0 = T[r0 * LDT + m], l1 = T[(r0 + 1) * LDT + m];
-        const double2 x0 = X[m * LDT + c0], x1 = X[m * LDT + c0 + 1];
-        cfma(acc[0][0], l0, x0);
-        cfma(acc[0][1], l0, x1);
-        cfma(acc[1][0], l1, x0);
-        cfma(acc[1][1], l1, x1);
-      }
-#pragma unroll
-      for (int u = 0; u < 2; u++)
-#pragma unroll
-        for (int v = 0; v < 2; v++) X[(r0 + u) * LDT + c0 + v] = acc[u][v];
-    }
-    __syncthreads();
-    if (act) {   // X_ik = -X_ii W_ik (X_ii lower triangular)
-#pragma unroll
-      for (int u = 0; u < 2; u++)
-#pragma unroll
-        for (int v = 0; v < 2; v++) acc[u][v] = make_double2(0.0, 0.0);
-      for (int m = 16 * ib; m <= r0 + 1; m++) {
-        const double2 w0 = X[m * LDT + c0], w1 = X[m * LDT + c0 + 1];
-        const double2 x0 = m <= r0 ? X[r0 * LDT + m] : make_double2(0.0, 0.0);
-        const double2 x1 = X[(r0 + 1) * LDT + m];
-        cfma(acc[0][0], x0, w0);
-        cfma(acc[0][1], x0, w1);
-        cfma(acc[1][0], x1, w0);
-        cfma(acc[1][1], x1, w1);
-      }
-    }
-    __syncthreads();
-    if (act) {
-#pragma unroll
-      for (int u = 0; u < 2; u++)
-#pragma unroll
-        for (int v = 0; v < 2; v++) X[(r0 + u) * LDT + c0 + v] = make_double2(-acc[u][v].x, -acc[u][v].y);
-    }
-    __syncthreads();
-  }
-  double2* linv = B.linv + (long long)p * NB * NB;
-  for (int e = t; e < NB * NB; e += 256) {
-    const int r = e >> 6, c = e & 63;
-    if (c <= r) tile[(long long)r * np + c] = T[r * LDT + c];
-    linv[e] = c <= r ? X[r * LDT + c] : make_double2(0.0, 0.0);
-  }
-  {
-    const int r = t >> 2, q = t & 3;
-    double2 y = make_double2(0.0, 0.0);
-    for (int c = q; c <= r; c += 4) cfma(y, X[r * LDT + c], bsh[c]);
-    y.x += __shfl_xor_sync(0xffffffffu, y.x, 1);
-    y.y += __shfl_xor_sync(0xffffffffu, y.y, 1);
-    y.x += __shfl_xor_sync(0xffffffffu, y.x, 2);
-    y.y += __shfl_xor_sync(0xffffffffu, y.y, 2);
-    if (q == 0) B.rhs[(long long)p * NB + r] = y;
-  }
 }
 
 // b_i -= sum_{c in [c0, c1)} L[i][c] y[c] for rows i >= c1 (the strip's panels applied to the
