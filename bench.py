@@ -223,7 +223,10 @@ def run_gpu(args):
     fp64_eq = gflop / (gram_kernel_ms * 1e-3) / 1e12
     if engine == "int8":
         ops = gram_i8_ops(w, ns / world)
-        peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * INT8_OVER_BF16
+        # The kernel is timed alone (its own CUDA-event pair) and runs near the maximum SM clock
+        # (see "clocks"), so the burst figure applies; the sustained one is reported beside it.
+        peak = peaks["bf16_tflops"] * INT8_OVER_BF16
+        peak_sus = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * INT8_OVER_BF16
         ach = ops / (gram_kernel_ms * 1e-3) / 1e12
         roofline = {
             "kernel": "sr::oz::gram_i8 (sr_block_qgt_i8: tcgen05.mma kind::i8, TMA, TMEM)", "bound": "tensor",
@@ -232,10 +235,10 @@ def run_gpu(args):
             "kernel_ms": gram_kernel_ms,
             "algorithmic": (f"sum_b 2 (Re, Im) x n_b(n_b+1)/2 entries x K'=2 N_s x {INT8_PAIRS} slice pairs x 2 "
                             f"= {ops:.4e} int8 ops per launch"),
-            "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained x 2 (nominal int8/bf16 ratio, "
-                            "B200_PROFILING.md); the burst figure x 2 is "
-                            f"{peaks['bf16_tflops'] * INT8_OVER_BF16:.0f}, the smem-resident tcgen05 "
-                            "microbenchmark 4763 (profiles/r01_tcgen05_rate.txt)"),
+            "peak_source": ("MEASURED_PEAKS.json bf16_tflops (burst) x 2, the nominal dense int8 : bf16 "
+                            "ratio (4.5 : 2.25 PFLOP/s, B200_PROFILING.md)"),
+            "frac_of_sustained": ach / peak_sus, "sustained_peak": peak_sus,
+            "frac_of_tcgen05_microbenchmark": ach / 4763.0,
             "fp64_equivalent": {"achieved_tflops": fp64_eq, "fp64_dmma_peak": FP64_PEAK_TFLOPS,
                                 "ratio_to_fp64_peak": fp64_eq / FP64_PEAK_TFLOPS,
                                 "algorithmic": f"sum_b 4 N_s n_b (n_b+1) = {gflop:.4e} flop"},

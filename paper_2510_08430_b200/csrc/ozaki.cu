@@ -55,8 +55,10 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;   // warp 0 TMA, warp 1 MMA + TMEM
 constexpr size_t kSmem = (size_t)kStages * kStageBytes + 1024 + 256;
 // tcgen05 instruction descriptor: D s32 (bits 4-5 = 2), A/B signed int8 (bits 7-9, 10-12 = 1),
 // both K-major, N >> 3 at bit 17, M >> 4 at bit 24.
-constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                            ((uint32_t)(BM >> 4) << 24);
+constexpr uint32_t idesc_n(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+constexpr uint32_t kIdesc = idesc_n(BN);
 
 struct Blk {
   long long col0;        // first row of this block in the slice matrix (column of A within the group)
@@ -128,11 +130,12 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint
 __device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc_) {
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;\n" ::"r"(taddr), "l"(sdesc_));
 }
-__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t acc,
+                                       uint32_t idesc = kIdesc) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
           d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(acc));
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
 // K-major operand, 64-byte swizzle: 8-row core groups 512 bytes apart (SBO), LBO unused (1),
 // descriptor version 1 (sm_100), layout type 4 = SWIZZLE_64B.
@@ -276,12 +279,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int p = 0; p < kSlices; p++) {
               const uint64_t ad = sdesc(sa + p * kASlice + ks * 32);
+              const uint32_t acc = (kin > 0 || ks > 0 || p > 0) ? 1u : 0u;
+              if (kATmem) {
 #pragma unroll
-              for (int q = 0; q + p < kSlices; q++) {
-                const uint64_t bd = sdesc(sb + q * kBSlice + ks * 32);
-                const uint32_t acc = (kin > 0 || ks > 0 || p > 0) ? 1u : 0u;
-                if (kATmem) mma_i8_ts(tmem + (uint32_t)((p + q) * BN), tmem + kACol + 8 * p, bd, acc);
-                else mma_i8(tmem + (uint32_t)((p + q) * BN), ad, bd, acc);
+                for (int q = 0; q + p < kSlices; q++)
+                  mma_i8_ts(tmem + (uint32_t)((p + q) * BN), tmem + kACol + 8 * p,
+                            sdesc(sb + q * kBSlice + ks * 32), acc);
+              } else {
+                // Slice pairs (p, q..q+k-1) in ONE MMA of N = 64 k <= 256: the B slices are
+                // adjacent 64-row groups in shared memory and the accumulators of the digit
+                // diagonals p+q..p+q+k-1 are adjacent 64-column groups in TMEM.  10 MMAs per
+                // K step instead of 28, reading each A slice once.
+#pragma unroll
+                for (int q = 0; q + p < kSlices; q += 4) {
+                  const int nq = (kSlices - p - q) < 4 ? (kSlices - p - q) : 4;
+                  mma_i8(tmem + (uint32_t)((p + q) * BN), ad, sdesc(sb + q * kBSlice + ks * 32), acc,
+                         idesc_n(BN * nq));
+                }
               }
             }
           }
