@@ -186,7 +186,7 @@ SR_API sr_status sr_block_qgt_i8(int64_t n_samples, int n_blocks,
  * SR_GRAM_FP64 = FP64 DMMA tensor cores (sr_block_qgt), SR_GRAM_INT8 = int8 tcgen05 digit
  * slices (sr_block_qgt_i8; for the trailing updates the rows of each L_21 strip are
  * scaled and split the same way).  Process-wide; returns the previous setting, or -1 for
- * an unknown engine (setting unchanged). */
+ * an unknown engine (setting unchanged).  Default: SR_GRAM_INT8. */
 #define SR_GRAM_FP64 0
 #define SR_GRAM_INT8 1
 SR_API int sr_set_gram_engine(int engine);

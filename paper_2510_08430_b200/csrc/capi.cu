@@ -15,7 +15,7 @@ thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
 void set_error(const std::string& m) { g_err = m; }
 void count_launch(int n) { g_launches += n; }
-int g_gram_engine = SR_GRAM_FP64;
+int g_gram_engine = SR_GRAM_INT8;   // default: int8 tcgen05 digit slices (R10)
 int gram_engine() { return g_gram_engine; }
 
 struct TimedLaunch {
