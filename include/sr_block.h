@@ -181,7 +181,7 @@ SR_API sr_status sr_block_qgt_i8(int64_t n_samples, int n_blocks,
                                  double* S, void* workspace, size_t workspace_bytes, void* stream);
 
 /* sr_set_gram_engine — engine of the dense contractions: sr_step's stage (4) and the
- * deferred trailing updates (A_22 -= L_21 L_21^H, K = 256) of every Cholesky
+ * deferred trailing updates (A_22 -= L_21 L_21^H, K = 512) of every Cholesky
  * factorisation (sr_block_solve, sr_full_qgt_solve, sr_ntk_solve, sr_step).
  * SR_GRAM_FP64 = FP64 DMMA tensor cores (sr_block_qgt), SR_GRAM_INT8 = int8 tcgen05 digit
  * slices (sr_block_qgt_i8; for the trailing updates the rows of each L_21 strip are

@@ -11,8 +11,8 @@
 //   trsm (engine)    L_ip = A_ip Linv_p^H for every row tile i > p      (DMMA, NH/STORE)
 //   (chol_diag also subtracts the strip's earlier panels from its own 64 rows of b)
 //   inner (engine)   A_ij -= L_ip L_jp^H for the strip's later columns j (DMMA, NH/SUB)
-// and after every strip of 4 panels chol_rhs_update (b_i -= L_i,strip y_strip for the rows
-// below) and one deferred trailing update with K = 256:
+// and after every strip of kStrip panels chol_rhs_update (b_i -= L_i,strip y_strip for the rows
+// below) and one deferred trailing update with K = 64 kStrip:
 //   trail (engine)   A_ij -= L_i,strip L_j,strip^H for i >= j beyond the strip (NH/SUB)
 // then back substitution L^H x = y strip by strip (x_p = Linv_p^H y_p inside the strip,
 // then y_{<strip} -= L_strip,<^H x_strip) and dtheta = -x.
@@ -26,10 +26,13 @@
 namespace sr {
 namespace {
 
+#ifndef SR_KSTRIP
+#define SR_KSTRIP 8   // measured best of 2, 4, 8, 12, 16 at configs[1] (3-block solve 25.9 -> 24.0 ms)
+#endif
 using cholk::NB;
 using cholk::chol_diag;
 using cholk::kDiagSmem;
-constexpr int kStrip = 4;   // panels per strip (deferred trailing update with K = 256)
+constexpr int kStrip = SR_KSTRIP;   // panels per strip (deferred trailing update with K = 64 kStrip)
 
 __global__ void chol_init(CholSet cs, double lam, int inplace) {
   const int b = blockIdx.y;
