@@ -8,8 +8,8 @@
 //   1. column scaling: every column j of A (a parameter) gets an exponent E_j with
 //      max_k max(|Re A_kj|, |Im A_kj|) < 2^E_j, and X_kj = rint(A_kj 2^(54 - E_j)) is an
 //      integer with |X| < 2^54 (rounding error <= 2^-55 of the column maximum);
-//   2. digits: X = sum_{p=0..6} d_p 256^(6-p), d_1..d_6 in [-128, 127] (balanced base-256),
-//      |d_0| <= 64 — seven int8 slices;
+//   2. digits: X = sum_{p=0..6} d_p 256^(6-p), d_p in [-128, 127], |d_0| <= 64 — seven int8
+//      slices (the bytes of X + 128 sum 256^p, shifted by 128: digit_bytes / digits8);
 //   3. real embedding: Re S = C^T C and Im S = C^T D over K' = 2 N_s, with
 //      C = [Re A; Im A] and D = [Im A; -Re A] (so S = A^H A exactly);
 //   4. products: G_t = sum_{p+q=t} C_p^T Y_q (Y = C or D) for t = 0..6, each an exact int32
@@ -413,14 +413,38 @@ __global__ void oz_colmax(const double2* __restrict__ A, long long lda, long lon
   atomicMax(mx + j, (unsigned long long)__double_as_longlong(m));
 }
 
-__device__ __forceinline__ void put_digits(long long x, uint64_t (&pk)[kSlices], int r) {
+// Signed base-256 digits from bytes: with C = 128 sum_{p<7} 256^p (> 2^54 > |X|),
+// U = X + C lies in [0, 2^56) and X = sum_p (u_p - 128) 256^(6-p) for the bytes u_p of U, so
+// the int8 digits are the bytes of U xor 0x80...80 — d_p in [-128, 127], |d_0| <= 64 as
+// for balanced digits.  digits8 takes eight values and returns pk[p] = digit p of value r in
+// byte r: an 8x8 byte transpose (32 byte permutes) instead of per-digit integer arithmetic.
+constexpr unsigned long long kDigitBias = 0x0080808080808080ULL;   // C
+__device__ __forceinline__ uint64_t digit_bytes(long long x) {
+  return ((unsigned long long)x + kDigitBias) ^ kDigitBias;   // bytes 0..6 = digits 6..0
+}
+__device__ __forceinline__ void transpose4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t& o0,
+                                           uint32_t& o1, uint32_t& o2, uint32_t& o3) {
+  const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
+  const uint32_t t2 = __byte_perm(c, d, 0x5140), t3 = __byte_perm(c, d, 0x7362);
+  o0 = __byte_perm(t0, t2, 0x5410);
+  o1 = __byte_perm(t0, t2, 0x7632);
+  o2 = __byte_perm(t1, t3, 0x5410);
+  o3 = __byte_perm(t1, t3, 0x7632);
+}
+__device__ __forceinline__ void digits8(const uint64_t (&u)[8], uint64_t (&pk)[kSlices]) {
+  uint32_t lo[8], hi[8];   // transposed rows: byte j of every value, values 0-3 | 4-7
+  uint32_t T[8][2];
 #pragma unroll
-  for (int p = kSlices - 1; p >= 1; p--) {
-    const int d = (int)(signed char)(x & 0xFF);
-    pk[p] |= (uint64_t)(uint8_t)d << (8 * r);
-    x = (x - d) >> 8;
+  for (int r = 0; r < 8; r++) {
+    lo[r] = (uint32_t)u[r];
+    hi[r] = (uint32_t)(u[r] >> 32);
   }
-  pk[0] |= (uint64_t)(uint8_t)(int)x << (8 * r);
+  transpose4(lo[0], lo[1], lo[2], lo[3], T[0][0], T[1][0], T[2][0], T[3][0]);   // bytes 0-3, values 0-3
+  transpose4(lo[4], lo[5], lo[6], lo[7], T[0][1], T[1][1], T[2][1], T[3][1]);   // bytes 0-3, values 4-7
+  transpose4(hi[0], hi[1], hi[2], hi[3], T[4][0], T[5][0], T[6][0], T[7][0]);   // bytes 4-7, values 0-3
+  transpose4(hi[4], hi[5], hi[6], hi[7], T[4][1], T[5][1], T[6][1], T[7][1]);   // bytes 4-7, values 4-7
+#pragma unroll
+  for (int p = 0; p < kSlices; p++) pk[p] = (uint64_t)T[6 - p][0] | ((uint64_t)T[6 - p][1] << 32);
 }
 
 // Digits of 32 columns x 64 samples, written as K-major int8 rows
@@ -441,19 +465,21 @@ __global__ void __launch_bounds__(256) oz_split(const double2* __restrict__ A, l
     if (blockIdx.y == 0 && kg == 0) expo[j] = e;
   }
   uint64_t pk[3][kSlices];
+  {
+    uint64_t ur[8], ui[8], un[8];
 #pragma unroll
-  for (int a = 0; a < 3; a++)
-#pragma unroll
-    for (int p = 0; p < kSlices; p++) pk[a][p] = 0;
-#pragma unroll 2
-  for (int r = 0; r < 8; r++) {
-    const long long k = k0 + kg * 8 + r;
-    double2 v = make_double2(0.0, 0.0);
-    if (j < n && k < K) v = A[k * lda + c0 + j];
-    const long long xr = llrint(scalbn(v.x, 54 - e)), xi = llrint(scalbn(v.y, 54 - e));
-    put_digits(xr, pk[0], r);
-    put_digits(xi, pk[1], r);
-    put_digits(-xr, pk[2], r);
+    for (int r = 0; r < 8; r++) {
+      const long long k = k0 + kg * 8 + r;
+      double2 v = make_double2(0.0, 0.0);
+      if (j < n && k < K) v = A[k * lda + c0 + j];
+      const long long xr = llrint(scalbn(v.x, 54 - e)), xi = llrint(scalbn(v.y, 54 - e));
+      ur[r] = digit_bytes(xr);
+      ui[r] = digit_bytes(xi);
+      un[r] = digit_bytes(-xr);
+    }
+    digits8(ur, pk[0]);
+    digits8(ui, pk[1]);
+    digits8(un, pk[2]);
   }
 #pragma unroll
   for (int a = 0; a < 3; a++)
@@ -488,18 +514,20 @@ __global__ void __launch_bounds__(256) oz_split_rows(const double2* __restrict__
   if (lane == 0) expo[i] = e;
   for (int k0 = lane * 8; k0 < Kp; k0 += 256) {
     uint64_t pk[3][kSlices];
+    {
+      uint64_t ur[8], ui[8], un[8];
 #pragma unroll
-    for (int a = 0; a < 3; a++)
-#pragma unroll
-      for (int p = 0; p < kSlices; p++) pk[a][p] = 0;
-#pragma unroll 2
-    for (int r = 0; r < 8; r++) {
-      const int k = k0 + r;
-      const double2 v = k < K ? row[k] : make_double2(0.0, 0.0);
-      const long long xr = llrint(scalbn(v.x, 54 - e)), xi = llrint(scalbn(-v.y, 54 - e));
-      put_digits(xr, pk[0], r);
-      put_digits(xi, pk[1], r);
-      put_digits(-xr, pk[2], r);
+      for (int r = 0; r < 8; r++) {
+        const int k = k0 + r;
+        const double2 v = k < K ? row[k] : make_double2(0.0, 0.0);
+        const long long xr = llrint(scalbn(v.x, 54 - e)), xi = llrint(scalbn(-v.y, 54 - e));
+        ur[r] = digit_bytes(xr);
+        ui[r] = digit_bytes(xi);
+        un[r] = digit_bytes(-xr);
+      }
+      digits8(ur, pk[0]);
+      digits8(ui, pk[1]);
+      digits8(un, pk[2]);
     }
 #pragma unroll
     for (int a = 0; a < 3; a++)
