@@ -91,8 +91,12 @@ __global__ void __launch_bounds__(256) chol_back_strip(const CholBlock B, int p0
   __syncthreads();
   for (int p = pend - 1; p >= p0; p--) {
     const double2* linv = B.linv + (long long)p * NB * NB;
-    double2 sx = make_double2(0.0, 0.0);
-    for (int r = c + q4; r < NB; r += 4) cfma_conj(sx, linv[r * NB + c], ys[p - p0][r]);
+    // Linv_p is lower triangular: entries r < c are zero, so the full 16-term sums are exact;
+    // 4 independent partial sums keep 4 loads in flight.
+    double2 sa[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+#pragma unroll
+    for (int i = 0; i < 16; i++) cfma_conj(sa[i & 3], linv[(4 * i + q4) * NB + c], ys[p - p0][4 * i + q4]);
+    double2 sx = cadd(cadd(sa[0], sa[1]), cadd(sa[2], sa[3]));
     sx.x += __shfl_xor_sync(0xffffffffu, sx.x, 1);
     sx.y += __shfl_xor_sync(0xffffffffu, sx.y, 1);
     sx.x += __shfl_xor_sync(0xffffffffu, sx.x, 2);
@@ -104,8 +108,11 @@ __global__ void __launch_bounds__(256) chol_back_strip(const CholBlock B, int p0
     __syncthreads();
     for (int q = p0; q < p; q++) {   // y_q[c] -= sum_r conj(L[p*64+r][q*64+c]) x_p[r]
       const double2* lp = B.Fm + (long long)p * NB * np + (long long)q * NB + c;
-      double2 sy = make_double2(0.0, 0.0);
-      for (int r = q4; r < NB; r += 4) cfma_conj(sy, lp[(long long)r * np], xs[r]);
+      double2 sb[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
+                       make_double2(0.0, 0.0)};
+#pragma unroll
+      for (int i = 0; i < 16; i++) cfma_conj(sb[i & 3], lp[(long long)(4 * i + q4) * np], xs[4 * i + q4]);
+      double2 sy = cadd(cadd(sb[0], sb[1]), cadd(sb[2], sb[3]));
       sy.x += __shfl_xor_sync(0xffffffffu, sy.x, 1);
       sy.y += __shfl_xor_sync(0xffffffffu, sy.y, 1);
       sy.x += __shfl_xor_sync(0xffffffffu, sy.x, 2);
