@@ -66,8 +66,13 @@ __global__ void chol_rhs_update(const CholBlock B, long long c0, long long c1) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (long long r = c1 + (long long)blockIdx.x * 8 + warp; r < np; r += (long long)gridDim.x * 8) {
     const double2* row = B.Fm + r * np;
-    double2 s = make_double2(0.0, 0.0);
-    for (long long c = c0 + lane; c < c1; c += 32) cfma(s, row[c], B.rhs[c]);
+    double2 sa[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    for (long long c = c0 + lane; c < c1; c += 128) {   // c1 - c0 is a multiple of 64
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (c + 32 * u < c1) cfma(sa[u], row[c + 32 * u], B.rhs[c + 32 * u]);
+    }
+    double2 s = cadd(cadd(sa[0], sa[1]), cadd(sa[2], sa[3]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
@@ -134,10 +139,13 @@ __global__ void __launch_bounds__(256) chol_back_rest(const CholBlock B, int p0,
   const long long ncol = (long long)p0 * NB;
   for (long long cb = (long long)blockIdx.x * NB; cb < ncol; cb += (long long)gridDim.x * NB) {
     const long long c = cb + cl;
-    double2 s = make_double2(0.0, 0.0);
+    double2 sa[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
     const double2* col = B.Fm + ((long long)p0 * NB) * np + c;
-#pragma unroll 4
-    for (int r = rq; r < nr; r += 4) cfma_conj(s, col[(long long)r * np], xs[r]);
+    for (int r0 = rq; r0 < nr; r0 += 16) {   // nr is a multiple of 64
+#pragma unroll
+      for (int u = 0; u < 4; u++) cfma_conj(sa[u], col[(long long)(r0 + 4 * u) * np], xs[r0 + 4 * u]);
+    }
+    const double2 s = cadd(cadd(sa[0], sa[1]), cadd(sa[2], sa[3]));
     red[rq][cl] = s;
     __syncthreads();
     if (rq == 0) {

@@ -206,10 +206,13 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
   {   // b_p -= sum over the strip's earlier panels q in [p0, p) of L_pq y_q (rows of panel p)
     const int r = t >> 2, q = t & 3;
     const double2* lrow = B.Fm + ((long long)p * NB + r) * np;
-    double2 s2 = make_double2(0.0, 0.0);
-    const int c0 = p0 * NB + q, c1 = p * NB;
-#pragma unroll 8
-    for (int c = c0; c < c1; c += 4) cfma(s2, lrow[c], B.rhs[c]);
+    double2 sa[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    const int c0 = p0 * NB + q, c1 = p * NB;   // c1 - c0 + q is a multiple of 64
+    for (int c = c0; c < c1; c += 16) {
+#pragma unroll
+      for (int u = 0; u < 4; u++) cfma(sa[u], lrow[c + 4 * u], B.rhs[c + 4 * u]);
+    }
+    double2 s2 = cadd(cadd(sa[0], sa[1]), cadd(sa[2], sa[3]));
     s2.x += __shfl_xor_sync(0xffffffffu, s2.x, 1);
     s2.y += __shfl_xor_sync(0xffffffffu, s2.y, 1);
     s2.x += __shfl_xor_sync(0xffffffffu, s2.x, 2);
