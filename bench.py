@@ -123,6 +123,20 @@ def dist_env():
     return int(os.environ.get("RANK", "0")), ws, int(os.environ.get("LOCAL_RANK", "0"))
 
 
+def _quiet_fd1(fn):
+    """Run fn() with the process-level stdout (fd 1) sent to /dev/null."""
+    sys.stdout.flush()
+    saved, devnull = os.dup(1), os.open(os.devnull, os.O_WRONLY)
+    os.dup2(devnull, 1)
+    try:
+        return fn()
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
+        os.close(devnull)
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def run_gpu(args):
     import torch
@@ -134,8 +148,14 @@ def run_gpu(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    sharded = world > 1 or args.sharded
+    if sharded:
+        # keep stdout to the one JSON line: the NCCL communicator set-up prints a version banner
+        # on fd 1, so it runs with fd 1 pointed at /dev/null
+        def _init():
+            dist.init_process_group("nccl", device_id=dev)
+            dist.barrier()
+        _quiet_fd1(_init)
     w = workloads.BY_NAME[args.workload]
     spins_all, params = workloads.make_inputs(w)
     ij, jj = sr.lattice.for_workload(w)
@@ -145,7 +165,7 @@ def run_gpu(args):
 
     engine = args.gram_engine
     sr.sr_set_gram_engine(sr.GRAM_INT8 if engine == "int8" else sr.GRAM_FP64)   # for sr_step_host (e2e)
-    if world > 1:
+    if sharded:
         step = parallel.ShardedStep(w.widths, spins_all, ij, jj, w.lam, rank, world, dev, gram_engine=engine)
     else:
         step = parallel.LocalStep(w.widths, spins_all, ij, jj, w.lam, dev, gram_engine=engine)
@@ -174,19 +194,19 @@ def run_gpu(args):
     stage_ms = {name: float(np.mean([evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(n_stage_runs)]))
                 for i, name in enumerate(step.STAGES)}
 
-    use_graph = world == 1 and not args.no_graph
+    use_graph = not sharded and not args.no_graph
     if use_graph:
         step.capture(theta)                  # the whole step as one CUDA graph
         for _ in range(args.warmup):
             step.replay()
     torch.cuda.synchronize(dev)
-    if world > 1:
+    if sharded:
         dist.barrier()
 
     clocks = ClockSampler(local)
     clocks.start()
     torch.cuda.synchronize(dev)
-    if world > 1:
+    if sharded:
         dist.barrier()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(stream)
@@ -197,22 +217,23 @@ def run_gpu(args):
             step.run(theta)
     stop.record(stream)
     torch.cuda.synchronize(dev)
-    if world > 1:
+    if sharded:
         dist.barrier()
     clk = clocks.stop()
     total_ms = start.elapsed_time(stop)
-    if world > 1:
+    if sharded:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
 
     # e2e: the same step through sr_step_host (host buffers in and out, every step)
-    e2e = None
-    if world == 1:
+    if sharded:
+        e2e = run_e2e_sharded(torch, dist, step, theta_h, dev, args)
+    else:
         e2e = run_e2e(sr, torch, w, theta_h, spins_all, ij, jj, dev, args)
 
     if rank != 0:
-        if world > 1:
+        if sharded:
             dist.destroy_process_group()
         return
     ms_per_step = total_ms / args.steps
@@ -267,7 +288,7 @@ def run_gpu(args):
         "data": "synthetic (seeded uniform S^z=0 spins, complex-normal weights; workloads.py)",
         "config": {"workload": w.name, "lattice": f"{w.lattice}{'x'.join(map(str, w.extent))}",
                    "widths": list(w.widths), "n_samples": ns, "n_params": n_p, "blocks": block_sizes(w),
-                   "lambda": w.lam, "gram_engine": engine, "parallelism": f"samples sharded x{world}" if world > 1 else "single GPU",
+                   "lambda": w.lam, "gram_engine": engine, "parallelism": f"samples sharded x{world} (NCCL)" if sharded else "single GPU",
                    "l2": f"inputs larger than L2 (O = {16.0 * ns * n_p / 1e9:.2f} GB per step vs 126 MB L2); no flush"},
         "roofline": roofline,
         "stage_roofline": {
@@ -297,8 +318,36 @@ def run_gpu(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rec["cpu_baseline"] = cpu_baseline(w)
     print(json.dumps(rec), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
+
+
+def run_e2e_sharded(torch, dist, step, theta_h, dev, args):
+    """e2e of the sharded step through the public Python API: every step copies theta from
+    pinned host memory, runs parallel.ShardedStep (C ABI + NCCL) and reads dtheta back;
+    host clock between barriers, max over ranks.  (The spins shard stays resident: the
+    samples are the rank's data, not a per-step input.)"""
+    th = torch.from_numpy(theta_h).pin_memory()
+    dth = torch.empty(theta_h.shape[0], dtype=torch.complex128).pin_memory()
+    theta = torch.empty(theta_h.shape[0], dtype=torch.complex128, device=dev)
+
+    def one():
+        theta.copy_(th, non_blocking=True)
+        d, _ = step.run(theta)
+        dth.copy_(d, non_blocking=True)
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(1, args.warmup)):
+        one()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    return {"value": args.steps / float(dt.item()), "unit": "steps/s", "h2d_bytes_per_step": int(th.numel() * 16),
+            "d2h_bytes_per_step": int(dth.numel() * 16),
+            "api": "parallel.ShardedStep.run (C ABI + NCCL), pinned theta in, dtheta out, host-clock timed"}
 
 
 def run_e2e(sr, torch, w, theta_h, spins, ij, jj, dev, args):
@@ -416,6 +465,8 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch stage by stage instead of one CUDA graph")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the sample-sharded NCCL step even on one rank (tests the multi-GPU path)")
     ap.add_argument("--gram-engine", default="int8", choices=["int8", "fp64"],
                     help="stage (4) engine: int8 tcgen05 digit slices (default) or FP64 DMMA")
     args = ap.parse_args()

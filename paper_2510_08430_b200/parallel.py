@@ -9,7 +9,7 @@ ShardedStep, rank r of G, owning samples [r*N_s/G, (r+1)*N_s/G):
   2. sr_column_moments -> all_gather of the double-double moment rows     (2 n_p + 2 complex)
   3. sr_center_force_global sums the rows (double-double), centres -> all_reduce(SUM) of F
   4. sr_block_qgt_i8 (or sr_block_qgt) on the local rows (partial S_b = A_b,local^H A_b,local),
-     reduce(SUM, dst=owner(b)) per block, owner(b) = b mod G
+     reduce(SUM, dst=owner(b)) per block; owners hold contiguous, cost-balanced block ranges
   5. owners: sr_block_solve of their blocks; dtheta all_reduce(SUM) (non-owners hold 0)
 The arithmetic is the C ABI's; this module only moves buffers.  `ops` is injectable so
 the collective pattern can be exercised on CPU with gloo (tests/test_parallel_gloo.py).
@@ -27,7 +27,7 @@ STAGES = ("jacobian", "local_energy", "center_force", "block_qgt", "block_solve"
 class CudaOps:
     """The C-ABI stage calls with one shared, preallocated workspace."""
 
-    def __init__(self, widths, n_local, n_bonds, device, gram_engine="int8"):
+    def __init__(self, widths, n_local, n_bonds, device, gram_engine="int8", solve_offsets=None):
         if gram_engine not in ("int8", "fp64"):
             raise ValueError(f"gram_engine must be 'int8' or 'fp64', got {gram_engine!r}")
         lib = sr.load()
@@ -39,7 +39,9 @@ class CudaOps:
             lib.sr_jacobian_workspace_bytes(L, wa, n_local),
             lib.sr_local_energy_workspace_bytes(L, wa, n_local, n_bonds),
             lib.sr_center_force_workspace_bytes(n_local, n_p),
-            lib.sr_block_solve_workspace_bytes(len(offs) - 1, sr._offsets(offs)),
+            # a sharded step's owner solves only its own contiguous range of blocks
+            lib.sr_block_solve_workspace_bytes(len(solve_offsets) - 1, sr._offsets(solve_offsets))
+            if solve_offsets is not None else lib.sr_block_solve_workspace_bytes(len(offs) - 1, sr._offsets(offs)),
             lib.sr_block_qgt_i8_workspace_bytes(n_local, len(offs) - 1, sr._offsets(offs))
             if gram_engine == "int8" else 0,
         )
@@ -78,8 +80,42 @@ def shard_range(n, rank, world):
     return lo, lo + base + (1 if rank < rem else 0)
 
 
-def block_owner(b, world):
-    return b % world
+def block_ranges(sizes, world):
+    """Contiguous owner ranges of layer blocks: rank r owns blocks [lo_r, hi_r), balanced by the
+    Cholesky cost sum n_b^3 (greedy against the remaining average), so an owner's blocks are
+    one contiguous stretch of S, F and dtheta, solved together in one sr_block_solve call
+    (concurrent streams).  Every rank gets a block while blocks last; extra ranks own none."""
+    nb = len(sizes)
+    cost = [float(n) ** 3 for n in sizes]
+    ranges, lo = [], 0
+    for r in range(world):
+        left = world - r
+        if lo >= nb:
+            ranges.append((nb, nb))
+            continue
+        if left == 1:
+            ranges.append((lo, nb))
+            lo = nb
+            continue
+        target = sum(cost[lo:]) / left
+        hi, acc = lo + 1, cost[lo]
+        max_hi = nb - (left - 1) if nb - lo >= left else lo + 1
+        while hi < max_hi and acc + cost[hi] / 2 <= target:
+            acc += cost[hi]
+            hi += 1
+        ranges.append((lo, hi))
+        lo = hi
+    return ranges
+
+
+def block_owner(b, world, sizes=None):
+    """Owner rank of block b (sizes given: the contiguous cost-balanced ranges; else b mod world)."""
+    if sizes is None:
+        return b % world
+    for r, (lo, hi) in enumerate(block_ranges(sizes, world)):
+        if lo <= b < hi:
+            return r
+    raise ValueError(b)
 
 
 class _Buffers:
@@ -169,10 +205,15 @@ class ShardedStep:
         lo, hi = shard_range(self.n_total, rank, world)
         self.device = torch.device(device)
         self.buf = _Buffers(widths, spins_all[lo:hi], bij, bj, self.device)
-        self.ops = ops or CudaOps(widths, hi - lo, len(bj), self.device, gram_engine)
+        offs = sr.block_offsets(widths)
+        self.sizes = [offs[b + 1] - offs[b] for b in range(len(offs) - 1)]
+        self.ranges = block_ranges(self.sizes, world)
+        olo, ohi = self.ranges[rank]
+        self.own_offs = [offs[b] - offs[olo] for b in range(olo, ohi + 1)] if ohi > olo else None
+        self.ops = ops or CudaOps(widths, hi - lo, len(bj), self.device, gram_engine, solve_offsets=self.own_offs)
         self.moments = torch.empty(2 * self.buf.n_p + 2, dtype=torch.complex128, device=self.device)
         self.moments_all = torch.empty(world, 2 * self.buf.n_p + 2, dtype=torch.complex128, device=self.device)
-        self.owned = [b for b in range(len(self.buf.offs) - 1) if block_owner(b, world) == rank]
+        self.owned = list(range(olo, ohi))
 
     def run(self, theta, events=None):
         import torch.distributed as dist
@@ -190,12 +231,15 @@ class ShardedStep:
         _rec(events, 3, st)
         o.block_qgt(b.O, b.offs, b.S)
         for blk in range(len(b.offs) - 1):
-            dist.reduce(b.s_block(blk), dst=block_owner(blk, self.world), group=g)
+            dist.reduce(b.s_block(blk), dst=block_owner(blk, self.world, self.sizes), group=g)
         _rec(events, 4, st)
         b.dtheta.zero_()
-        for blk in self.owned:
-            lo, hi = b.offs[blk], b.offs[blk + 1]
-            o.block_solve([0, hi - lo], b.s_block(blk), b.F[lo:hi], self.lam, b.dtheta[lo:hi])
+        if self.owned:   # this rank's contiguous blocks in one call (concurrent streams)
+            olo, ohi = self.owned[0], self.owned[-1] + 1
+            lo, hi = b.offs[olo], b.offs[ohi]
+            spos = sum(n * n for n in self.sizes[:olo])
+            slen = sum(n * n for n in self.sizes[olo:ohi])
+            o.block_solve(self.own_offs, b.S[spos:spos + slen], b.F[lo:hi], self.lam, b.dtheta[lo:hi])
         dist.all_reduce(b.dtheta, group=g)
         _rec(events, 5, st)
         return b.dtheta, b.energy

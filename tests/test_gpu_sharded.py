@@ -1,0 +1,61 @@
+"""The sample-sharded step (parallel.ShardedStep: C ABI stages + NCCL collectives) on a real
+GPU, as a one-rank NCCL process group: same dtheta and energy as the single-GPU step and as
+the oracle (BASELINE.json north_star: the NCCL reduce of the per-block partial S_b to its
+owner, the owner's solve and the dtheta all-reduce).  The world-size-2 orchestration is
+covered on CPU by tests/test_parallel_gloo.py."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+import workloads
+from oracle import estimators, hamiltonian, network, solvers
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.fixture(scope="module")
+def nccl_group():
+    if dist.is_initialized():
+        yield
+        return
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    yield
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_sharded_step_matches_local_and_oracle(nccl_group, cfg):
+    import paper_2510_08430_b200 as sr
+    from paper_2510_08430_b200 import parallel
+    w = workloads.CONFIGS[cfg]
+    spins, params = workloads.make_inputs(w)
+    ij, jj = sr.lattice.for_workload(w)
+    dev = torch.device("cuda:0")
+    theta = torch.from_numpy(sr.model.pack(params)).to(dev)
+    local = parallel.LocalStep(w.widths, spins, ij, jj, w.lam, dev)
+    d_local, e_local = (x.clone() for x in local.run(theta))
+    shard = parallel.ShardedStep(w.widths, spins, ij, jj, w.lam, 0, 1, dev)
+    d_shard, e_shard = shard.run(theta)
+    torch.cuda.synchronize()
+    rel = (torch.linalg.vector_norm(d_shard - d_local) / torch.linalg.vector_norm(d_local)).item()
+    assert rel < 1e-11
+    assert abs(e_shard.item() - e_local.item()) <= 1e-13 * abs(e_local.item())
+    if cfg == 0:   # small enough for the oracle
+        O = network.jacobian(params, spins)
+        e = hamiltonian.local_energies(params, spins, hamiltonian.bonds_for(w))
+        off = network.layer_offsets(params)
+        ref = solvers.block_solve(estimators.qgt_blocks(O, off), estimators.force(O, e), off, w.lam)
+        got = d_shard.cpu().numpy()
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-9

@@ -35,6 +35,18 @@ def test_shard_ranges_and_owners():
             sizes = [b - a for a, b in rs]
             assert max(sizes) - min(sizes) <= 1
     assert [block_owner(b, 8) for b in range(8)] == list(range(8))    # configs[4]: one block per GPU
+    from paper_2510_08430_b200.parallel import block_ranges
+    sizes4 = [16160] + [25760] * 7
+    assert block_ranges(sizes4, 8) == [(b, b + 1) for b in range(8)]
+    assert [block_owner(b, 8, sizes4) for b in range(8)] == list(range(8))
+    for sizes in ([3280, 6480, 6480], [5328] + [20880] * 3, [12928] + [16512] * 5, [640], sizes4):
+        for g in (1, 2, 3, 4, 8):
+            rs = block_ranges(sizes, g)
+            assert len(rs) == g and rs[0][0] == 0 and rs[-1][1] == len(sizes)
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(g - 1))          # contiguous cover
+            owned = [hi - lo for lo, hi in rs]
+            assert all(o >= 1 for o in owned[:min(g, len(sizes))])             # a block per rank while they last
+    assert block_ranges([3280, 6480, 6480], 2) == [(0, 2), (2, 3)]
 
 
 def test_workload_inputs_are_seeded_and_in_sector():

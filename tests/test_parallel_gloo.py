@@ -7,6 +7,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -62,8 +63,13 @@ class OracleOps:
             pos += n * n
 
     def block_solve(self, offs, S, F, lam, dtheta, info=None):
-        n = offs[1] - offs[0]
-        dtheta.copy_(torch.from_numpy(solvers.full_solve(S.reshape(n, n).numpy(), F.numpy(), lam)))
+        pos = 0
+        for b in range(len(offs) - 1):
+            lo, hi = offs[b], offs[b + 1]
+            n = hi - lo
+            x = solvers.full_solve(S[pos:pos + n * n].reshape(n, n).numpy(), F[lo:hi].numpy(), lam)
+            dtheta[lo:hi].copy_(torch.from_numpy(x))
+            pos += n * n
 
 
 def _worker(rank, world, port, result_path):
@@ -91,9 +97,11 @@ def _free_port():
     return p
 
 
-def test_sharded_step_equals_unsharded_oracle(tmp_path):
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_sharded_step_equals_unsharded_oracle(tmp_path, world):
+    """world 1: one owner of both blocks; 2: one block each; 3: a rank without a block."""
     out = str(tmp_path / "d.npy")
-    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     got = np.load(out)
     w = workloads.CONFIGS[0].with_samples(64)
     spins, params = workloads.make_inputs(w)
