@@ -11,6 +11,8 @@
 //   (z_0(x') = z_0(x) - 2 s_i W_0[:,i] - 2 s_j W_0[:,j]), the remaining layers run
 //   densely on the row tile in shared memory, and each row contributes
 //   2 J_b exp(ln psi(x') - ln psi(x)); rows of one sample are reduced in bond order.
+#include <cstdlib>
+
 #include "net.cuh"
 
 namespace sr {
@@ -313,8 +315,8 @@ __global__ void __launch_bounds__(kThreads) energy_eval(NetDesc net, const doubl
     }
     __syncthreads();
     for (int l = 1; l < net.L; l++) {
-      dense_rows<RB>(wt + net.toff[l], theta + net.boff[l], net.w[l], net.w[l + 1], cur, ld,
-                     [&](int r, int j, double2 z) { nxt[r * ld + j] = lncosh(z); });
+      auto epi = [&](int r, int j, double2 z) { nxt[r * ld + j] = lncosh(z); };
+      dense_rows<RB, decltype(epi), 8>(wt + net.toff[l], theta + net.boff[l], net.w[l], net.w[l + 1], cur, ld, epi);
       __syncthreads();
       double2* tmp = cur;
       cur = nxt;
@@ -473,19 +475,27 @@ sr_status local_energy_impl(const NetDesc& net, const double* theta_d, long long
   SR_LAUNCHED();
   energy_rows<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(spins, ns, net.w[0], nb, bij, w.off, w.rows);
   SR_LAUNCHED();
-  const int rb = rows_per_tile(net);
+  // 16-row tiles: more CTAs per SM to hide the L2 latency of the weight stream (measured
+  // faster than 32 rows); SR_ENERGY_RB overrides for tuning.
+  int rb = 16;
+  if (const char* e = getenv("SR_ENERGY_RB")) rb = atoi(e) == 32 ? 32 : atoi(e) == 8 ? 8 : 16;
   const size_t sm = tile_smem(net, rb);
   const long long max_tiles = (ns * nb + rb - 1) / rb;
-  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(max_tiles, 4LL * kNumSMs));
+  const unsigned grid =
+      (unsigned)std::max<long long>(1, std::min<long long>(max_tiles, (rb == 32 ? 4LL : 8LL) * kNumSMs));
   const double2* lp = reinterpret_cast<const double2*>(log_psi);
   if (rb == 32) {
     SR_TRY(set_smem(energy_eval<32>, sm));
     energy_eval<32><<<grid, kThreads, sm, st>>>(net, theta, w.wt, spins, bij, bond_j, w.z0, lp, w.off, ns, w.rows,
                                                 w.contrib);
-  } else {
+  } else if (rb == 16) {
     SR_TRY(set_smem(energy_eval<16>, sm));
     energy_eval<16><<<grid, kThreads, sm, st>>>(net, theta, w.wt, spins, bij, bond_j, w.z0, lp, w.off, ns, w.rows,
                                                 w.contrib);
+  } else {
+    SR_TRY(set_smem(energy_eval<8>, sm));
+    energy_eval<8><<<grid, kThreads, sm, st>>>(net, theta, w.wt, spins, bij, bond_j, w.z0, lp, w.off, ns, w.rows,
+                                               w.contrib);
   }
   SR_LAUNCHED();
   energy_reduce<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(w.diag, w.off, w.contrib, ns,

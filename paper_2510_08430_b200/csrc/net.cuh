@@ -29,7 +29,7 @@ sr_status make_net(int n_layers, const int32_t* widths, NetDesc* net);
 // M row-major [n_in][n_out] in global memory (L2-resident weights; coalesced across j).
 // Thread layout: 256 threads = 64 output lanes x 4 row groups; row r = group + 4q.
 // epi(r, j, z) is called for every r < RB, j < n_out.
-template <int RB, typename Epi>
+template <int RB, typename Epi, int UNROLL = 4>
 __device__ __forceinline__ void dense_rows(const double2* __restrict__ M, const double2* __restrict__ bias,
                                            int n_in, int n_out, const double2* hin, int ldin, Epi epi) {
   constexpr int RQ = RB / 4;
@@ -43,7 +43,7 @@ __device__ __forceinline__ void dense_rows(const double2* __restrict__ M, const 
 #pragma unroll
     for (int q = 0; q < RQ; q++) acc[q] = b0;
     const double2* mcol = M + (jv ? j : 0);
-#pragma unroll 4
+#pragma unroll UNROLL
     for (int i = 0; i < n_in; i++) {
       double2 wv = jv ? __ldg(mcol + (long long)i * n_out) : make_double2(0.0, 0.0);
 #pragma unroll
