@@ -136,8 +136,11 @@ __device__ __forceinline__ double2 lncosh(double2 z) {
   if (fabs(z.x) < 20.0) {
     double sa, ca, sb, cb;
     sincos(0.5 * z.y, &sb, &cb);
-    sa = sinh(0.5 * z.x);
-    ca = cosh(0.5 * z.x);
+    // sinh and cosh of x/2 from one expm1 (full relative accuracy for small x):
+    // em = e^(x/2) - 1, sinh = em (em + 2) / (2 (em + 1)), cosh = ((em + 1) + 1/(em + 1)) / 2
+    const double em = expm1(0.5 * z.x), ep = em + 1.0, iep = 1.0 / ep;
+    sa = 0.5 * em * (em + 2.0) * iep;
+    ca = 0.5 * (ep + iep);
     const double sr = sa * cb, si = ca * sb;   // sinh(z/2)
     return clog1p(make_double2(2.0 * (sr - si) * (sr + si), 4.0 * sr * si));
   }
