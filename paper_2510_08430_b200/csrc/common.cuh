@@ -171,6 +171,29 @@ __device__ __forceinline__ double2 ctanh(double2 z) {
   return neg ? make_double2(-t.x, -t.y) : t;
 }
 
+// lncosh(z) and tanh(z) together (Jacobian forward pass): for |Re z| < 20 both come from one
+// expm1 and one sincos of z/2 — tanh(z) = (sinh 2x + i sin 2y) / (cosh 2x + cos 2y) with the
+// double angles built from sinh/cosh(x/2) and sin/cos(y/2) by products; otherwise the
+// separate large-argument forms above.
+__device__ __forceinline__ void lncosh_tanh(double2 z, double2& h, double2& t) {
+  if (fabs(z.x) >= 20.0) {
+    h = lncosh(z);
+    t = ctanh(z);
+    return;
+  }
+  double sb, cb;
+  sincos(0.5 * z.y, &sb, &cb);
+  const double em = expm1(0.5 * z.x), ep = em + 1.0, iep = 1.0 / ep;
+  const double sa = 0.5 * em * (em + 2.0) * iep, ca = 0.5 * (ep + iep);   // sinh, cosh of x/2
+  const double sr = sa * cb, si = ca * sb;                                 // sinh(z/2)
+  h = clog1p(make_double2(2.0 * (sr - si) * (sr + si), 4.0 * sr * si));
+  const double shx = 2.0 * sa * ca, chx = 1.0 + 2.0 * sa * sa;            // sinh x, cosh x
+  const double sy = 2.0 * sb * cb, cy = (cb - sb) * (cb + sb);             // sin y, cos y
+  const double d = (1.0 + 2.0 * shx * shx) + (cy - sy) * (cy + sy);        // cosh 2x + cos 2y
+  const double id = 1.0 / d;
+  t = make_double2(2.0 * shx * chx * id, 2.0 * sy * cy * id);
+}
+
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
 

@@ -84,12 +84,13 @@ __global__ void __launch_bounds__(kThreads) jac_forward(NetDesc net, const doubl
     double2* tl = ts + net.aoff[l] * ns;
     dense_rows<RB>(wt + net.toff[l], theta + net.boff[l], net.w[l], fout, cur, ld,
                    [&](int r, int j, double2 z) {
-                     const double2 h = lncosh(z);
+                     double2 h, th;
+                     lncosh_tanh(z, h, th);
                      nxt[r * ld + j] = h;
                      const long long k = row0 + r;
                      if (k < ns) {
                        hl[k * fout + j] = h;
-                       tl[k * fout + j] = ctanh(z);
+                       tl[k * fout + j] = th;
                      }
                    });
     __syncthreads();
