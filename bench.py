@@ -190,7 +190,8 @@ def run_gpu(args):
     sr.sr_kernel_timer(False)
     launches = sr.sr_launch_count() // n_stage_runs
     gk_ms, gk_n = sr.sr_kernel_time_ms(gram_kernel)
-    gram_kernel_ms = gk_ms / max(gk_n, 1)
+    gram_kernel_ms = gk_ms / n_stage_runs        # all launches of one stage-(4) call (block groups)
+    gram_launches = gk_n // n_stage_runs
     stage_ms = {name: float(np.mean([evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(n_stage_runs)]))
                 for i, name in enumerate(step.STAGES)}
 
@@ -230,6 +231,8 @@ def run_gpu(args):
     if sharded:
         e2e = run_e2e_sharded(torch, dist, step, theta_h, dev, args)
     else:
+        del step                      # the e2e run allocates its own sr_step workspace
+        torch.cuda.empty_cache()
         e2e = run_e2e(sr, torch, w, theta_h, spins_all, ij, jj, dev, args)
 
     if rank != 0:
@@ -253,7 +256,7 @@ def run_gpu(args):
             "kernel": "sr::oz::gram_i8 (sr_block_qgt_i8: tcgen05.mma kind::i8, TMA, TMEM)", "bound": "tensor",
             "achieved": ach, "peak": peak, "unit": "TFLOP/s", "op_dtype": "int8 (one multiply-add = 2 ops)",
             "frac": ach / peak, "traffic": _ncu_traffic("gram_i8_traffic.json"),
-            "kernel_ms": gram_kernel_ms,
+            "kernel_ms": gram_kernel_ms, "kernel_launches": gram_launches,
             "algorithmic": (f"sum_b 2 (Re, Im) x n_b(n_b+1)/2 entries x K'=2 N_s x {INT8_PAIRS} slice pairs x 2 "
                             f"= {ops:.4e} int8 ops per launch"),
             "peak_source": ("MEASURED_PEAKS.json bf16_tflops (burst) x 2, the nominal dense int8 : bf16 "
