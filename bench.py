@@ -123,6 +123,16 @@ def dist_env():
     return int(os.environ.get("RANK", "0")), ws, int(os.environ.get("LOCAL_RANK", "0"))
 
 
+def config_of(w, world, engine, sharded):
+    """The workload description shared by both arms' JSON lines."""
+    return {"workload": w.name, "lattice": f"{w.lattice}{'x'.join(map(str, w.extent))}",
+            "widths": list(w.widths), "n_samples": w.n_samples, "n_params": w.n_params, "blocks": block_sizes(w),
+            "lambda": w.lam, "gram_engine": engine,
+            "parallelism": f"samples sharded x{world} (NCCL)" if sharded else "single GPU",
+            "l2": f"inputs larger than L2 (O = {16.0 * w.n_samples * w.n_params / 1e9:.2f} GB per step vs 126 MB L2); "
+                  "no flush"}
+
+
 def _quiet_fd1(fn):
     """Run fn() with the process-level stdout (fd 1) sent to /dev/null."""
     sys.stdout.flush()
@@ -289,10 +299,7 @@ def run_gpu(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded uniform S^z=0 spins, complex-normal weights; workloads.py)",
-        "config": {"workload": w.name, "lattice": f"{w.lattice}{'x'.join(map(str, w.extent))}",
-                   "widths": list(w.widths), "n_samples": ns, "n_params": n_p, "blocks": block_sizes(w),
-                   "lambda": w.lam, "gram_engine": engine, "parallelism": f"samples sharded x{world} (NCCL)" if sharded else "single GPU",
-                   "l2": f"inputs larger than L2 (O = {16.0 * ns * n_p / 1e9:.2f} GB per step vs 126 MB L2); no flush"},
+        "config": config_of(w, world, engine, sharded),
         "roofline": roofline,
         "stage_roofline": {
             "block_qgt": {"engine": engine, "fp64_equivalent_tflops": achieved,
@@ -452,7 +459,7 @@ def run_reference(args):
     rec = {"metric": METRIC, "value": args.steps / total, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-           "config": {"workload": w.name, "n_samples": w.n_samples, "n_params": w.n_params},
+           "config": config_of(w, world, args.gram_engine, world > 1),
            "cpu_baseline": {"value": args.steps / total, "unit": "steps/s", "cores": _threads(), "kind": "oracle",
                             "sample": sample},
            "e2e": {"value": args.steps / total, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
