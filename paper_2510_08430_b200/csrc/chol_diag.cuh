@@ -6,6 +6,9 @@
 #ifndef SR_DIAG_PROBE
 #define SR_DIAG_PROBE(i)
 #endif
+#ifndef SR_DIAG_BS
+#define SR_DIAG_BS 8   // diagonal sub-block of the single-warp factor (8 or 16)
+#endif
 
 namespace sr {
 namespace cholk {
@@ -13,14 +16,15 @@ namespace cholk {
 constexpr int NB = 64;
 
 // One CTA per block: factor the 64x64 diagonal tile of panel p, form its inverse
-// X = Linv_p and y_p = Linv_p b_p.  Blocked by 16 (the latency of a 64-step column
-// recursion with a block barrier per step is what limited the unblocked forms):
-//   for each 16-column block k (offset o = 16k):
-//     (a) warp 0 factors D_k = A[o:o+16, o:o+16] in registers, lane r = row r, columns
-//         broadcast by shuffles, 1/sqrt of each pivot kept in dinv;
-//     (b) rows r >= o+16 solve x D_k^H = A[r, o:o+16] (one thread per row, right-looking);
+// X = Linv_p and y_p = Linv_p b_p.  Blocked by BS = 8 (the latency of a 64-step column
+// recursion with a block barrier per step is what limited the unblocked forms; 8 beat 16,
+// tools/diag_probe.cu: 66.6k vs 75.3k cycles):
+//   for each BS-column block k (offset o = BS k):
+//     (a) warp 0 factors D_k = A[o:o+BS, o:o+BS] in registers, lane r = row r, columns
+//         broadcast through shared memory, 1/sqrt of each pivot kept in dinv;
+//     (b) rows r >= o+BS solve x D_k^H = A[r, o:o+BS] (a quad per row, right-looking);
 //     (c) A[r][s] -= sum_m L[r][o+m] conj(L[s][o+m]) on the trailing lower triangle
-//         (2x2 register patches).
+//         (2x2 register patches), overlapped with (a) of the next block.
 //   inverse: X_kk = D_k^{-1} (warp k, lane j = column j), then by block distance d = 1..3:
 //     W_ik = sum_{j=k}^{i-1} L_ij X_jk and X_ik = -X_ii W_ik (i = k + d), 2x2 patches.
 constexpr int LDT = NB + 1;   // 1040-byte rows
@@ -39,17 +43,18 @@ __device__ __forceinline__ void cfma_conjb(double2& acc, double2 a, double2 b) {
 // broadcasts.  Every lane also keeps the running diagonal dg[s] = A_ss - sum_k |L_sk|^2
 // (the same arithmetic as the owner's update of its own diagonal entry), so each step's
 // pivot is available locally without a broadcast.
-__device__ __forceinline__ void factor16(double2* T, int o, int lane, double* dinv, int* bad) {
-  double2 d[16];
-  double dg[16];
+template <int BS>
+__device__ __forceinline__ void factorb(double2* T, int o, int lane, double* dinv, int* bad) {
+  double2 d[BS];
+  double dg[BS];
   const int r = lane;
 #pragma unroll
-  for (int s = 0; s < 16; s++) {
-    d[s] = (r < 16 && s <= r) ? T[(o + r) * LDT + o + s] : make_double2(0.0, 0.0);
+  for (int s = 0; s < BS; s++) {
+    d[s] = (r < BS && s <= r) ? T[(o + r) * LDT + o + s] : make_double2(0.0, 0.0);
     dg[s] = T[(o + s) * LDT + o + s].x;
   }
 #pragma unroll
-  for (int c = 0; c < 16; c++) {
+  for (int c = 0; c < BS; c++) {
     double piv = dg[c];
     if (!(piv > 0.0)) {
       if (lane == 0 && *bad == 0) *bad = o + c + 1;
@@ -58,15 +63,15 @@ __device__ __forceinline__ void factor16(double2* T, int o, int lane, double* di
     const double isd = rsqrt(piv);
     if (r == c) d[c] = make_double2(piv * isd, 0.0);
     else if (r > c) d[c] = cscale(d[c], isd);
-    if (r < 16 && r >= c) T[(o + r) * LDT + o + c] = d[c];
+    if (r < BS && r >= c) T[(o + r) * LDT + o + c] = d[c];
     if (lane == 0) dinv[o + c] = isd;
     __syncwarp();
 #pragma unroll
-    for (int s = 1; s < 16; s++) {
+    for (int s = 1; s < BS; s++) {
       if (s <= c) continue;
       const double2 ls = T[(o + s) * LDT + o + c];   // L[s][c]
       dg[s] -= ls.x * ls.x + ls.y * ls.y;
-      if (r >= s && r < 16) {
+      if (r >= s && r < BS) {
         double2 v = d[s];
         v.x -= d[c].x * ls.x + d[c].y * ls.y;
         v.y -= d[c].y * ls.x - d[c].x * ls.y;
@@ -80,12 +85,13 @@ __device__ __forceinline__ void factor16(double2* T, int o, int lane, double* di
 // (diagonal real, 1/D_cc in dinv): a quad per row, lane q holding entries m = q mod 4;
 // step c: x_c = a_c / D_cc from the owner lane, shuffled inside the quad, then
 // a_m -= x_c conj(D[m][c]) for m > c.
+template <int BS>
 __device__ __forceinline__ void trsm_quad(double2* T, int o, int r, int q, const double* dinv) {
-  double2 a[4];
+  double2 a[BS / 4];
 #pragma unroll
-  for (int k = 0; k < 4; k++) a[k] = T[r * LDT + o + 4 * k + q];
+  for (int k = 0; k < BS / 4; k++) a[k] = T[r * LDT + o + 4 * k + q];
 #pragma unroll
-  for (int c = 0; c < 16; c++) {
+  for (int c = 0; c < BS; c++) {
     if (q == (c & 3)) {   // owner: x_c final, published in place
       a[c >> 2] = cscale(a[c >> 2], dinv[o + c]);
       T[r * LDT + o + c] = a[c >> 2];
@@ -93,7 +99,7 @@ __device__ __forceinline__ void trsm_quad(double2* T, int o, int r, int q, const
     __syncwarp();
     const double2 x = T[r * LDT + o + c];
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
+    for (int k = 0; k < BS / 4; k++) {
       const int m = 4 * k + q;
       if (m > c) {
         const double2 dm = T[(o + m) * LDT + o + c];
@@ -103,7 +109,7 @@ __device__ __forceinline__ void trsm_quad(double2* T, int o, int r, int q, const
     }
   }
 #pragma unroll
-  for (int k = 0; k < 4; k++) T[r * LDT + o + 4 * k + q] = a[k];
+  for (int k = 0; k < BS / 4; k++) T[r * LDT + o + 4 * k + q] = a[k];
 }
 
 // Lower-triangle patch index e -> (pi, pj), pi >= pj.
@@ -114,19 +120,20 @@ __device__ __forceinline__ void tri_patch(int e, int& pi, int& pj) {
   pj = e - pi * (pi + 1) / 2;
 }
 
-// (c) trailing update of rows/cols [o+16, 64) by the 16 columns L[:, o:o+16], by threads
-// t in [0, nt); with skip_next the 16x16 diagonal block at o+16 is left to syrk16_diag.
-__device__ __forceinline__ void syrk16(double2* T, int o, int t, int nt, bool skip_next) {
-  const int b0 = o + 16, P = (NB - b0) / 2, cnt = P * (P + 1) / 2;
+// (c) trailing update of rows/cols [o+BS, 64) by the BS columns L[:, o:o+BS], by threads
+// t in [0, nt); with skip_next the BS x BS diagonal block at o+BS is left to syrkb_diag.
+template <int BS>
+__device__ __forceinline__ void syrkb(double2* T, int o, int t, int nt, bool skip_next) {
+  const int b0 = o + BS, P = (NB - b0) / 2, cnt = P * (P + 1) / 2;
   for (int e = t; e < cnt; e += nt) {
     int pi, pj;
     tri_patch(e, pi, pj);
-    if (skip_next && pi < 8) continue;   // patch rows (and so columns) inside block o+16
+    if (skip_next && pi < BS / 2) continue;   // patch rows (and so columns) inside block o+BS
     const int r0 = b0 + 2 * pi, s0 = b0 + 2 * pj;
     double2 acc[2][2] = {{make_double2(0.0, 0.0), make_double2(0.0, 0.0)},
                          {make_double2(0.0, 0.0), make_double2(0.0, 0.0)}};
 #pragma unroll 4
-    for (int m = 0; m < 16; m++) {
+    for (int m = 0; m < BS; m++) {
       const double2 lr0 = T[r0 * LDT + o + m], lr1 = T[(r0 + 1) * LDT + o + m];
       const double2 ls0 = T[s0 * LDT + o + m], ls1 = T[(s0 + 1) * LDT + o + m];
       cfma_conjb(acc[0][0], lr0, ls0);
@@ -145,15 +152,16 @@ __device__ __forceinline__ void syrk16(double2* T, int o, int t, int nt, bool sk
   }
 }
 
-// Warp 0: the diagonal block at o+16 receives block o's update (136 lower entries).
-__device__ __forceinline__ void syrk16_diag(double2* T, int o, int lane) {
-  const int b0 = o + 16;
-  for (int e = lane; e < 136; e += 32) {
+// Warp 0: the diagonal block at o+BS receives block o's update (BS(BS+1)/2 lower entries).
+template <int BS>
+__device__ __forceinline__ void syrkb_diag(double2* T, int o, int lane) {
+  const int b0 = o + BS;
+  for (int e = lane; e < BS * (BS + 1) / 2; e += 32) {
     int r, c;
     tri_patch(e, r, c);
     double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int m = 0; m < 16; m++) cfma_conjb(acc, T[(b0 + r) * LDT + o + m], T[(b0 + c) * LDT + o + m]);
+    for (int m = 0; m < BS; m++) cfma_conjb(acc, T[(b0 + r) * LDT + o + m], T[(b0 + c) * LDT + o + m]);
     double2& x = T[(b0 + r) * LDT + b0 + c];
     x = csub(x, acc);
   }
@@ -222,25 +230,25 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
   if (t == 0) bad = 0;
   __syncthreads();
   SR_DIAG_PROBE(1);
-  // Block k: warp 0 applies block k-1's update to the diagonal block k and factors it while
-  // warps 1-7 apply block k-1's update to the rest of the trailing triangle (the SYRK is
-  // off the critical path); then every warp solves the rows below block k.
-  for (int k = 0; k < 4; k++) {
-    const int o = 16 * k;
+  // Block k (BS columns): warp 0 applies block k-1's update to the diagonal block k and
+  // factors it while warps 1-7 apply block k-1's update to the rest of the trailing
+  // triangle (the SYRK is off the critical path); then every warp solves the rows below.
+  constexpr int BS = SR_DIAG_BS;
+  static_assert(BS == 8 || BS == 16, "diagonal sub-block must be 8 or 16");
+  for (int k = 0; k < NB / BS; k++) {
+    const int o = BS * k;
     if (warp == 0) {
-      if (k > 0) syrk16_diag(T, o - 16, lane);
+      if (k > 0) syrkb_diag<BS>(T, o - BS, lane);
       __syncwarp();
-      factor16(T, o, lane, dinv, &bad);
+      factorb<BS>(T, o, lane, dinv, &bad);
     } else if (k > 0) {
-      syrk16(T, o - 16, t - 32, 224, true);
+      syrkb<BS>(T, o - BS, t - 32, 224, true);
     }
     __syncthreads();
-    SR_DIAG_PROBE(2 + 3 * k);
-    if (k < 3) {
-      if (t < 4 * (NB - o - 16)) trsm_quad(T, o, o + 16 + (t >> 2), t & 3, dinv);
+    SR_DIAG_PROBE(2 + 3 * (k * 4 / (NB / BS)));
+    if (k < NB / BS - 1) {
+      if (t < 4 * (NB - o - BS)) trsm_quad<BS>(T, o, o + BS + (t >> 2), t & 3, dinv);
       __syncthreads();
-      SR_DIAG_PROBE(3 + 3 * k);
-      SR_DIAG_PROBE(4 + 3 * k);
     }
   }
   if (t == 0 && bad && info) atomicCAS(info, 0, (int)(B.row_base + (long long)p * NB + bad));
