@@ -274,48 +274,60 @@ def test_step_and_step_host(sr):
     assert torch.equal(dh, d.cpu()) and torch.equal(eh, en.cpu())
 
 
-@pytest.mark.parametrize("cfg", [1, 2])
+@pytest.mark.parametrize("cfg", [1, 2, 3])
 def test_full_size_config(sr, cfg):
-    """BASELINE.json configs[1] (the bench workload) and configs[2] at full size in the bench's
-    launch configuration (parallel.LocalStep): sampled outputs against the oracle, the rest
-    through properties that hold at any size."""
+    """BASELINE.json configs[1] (the bench workload), configs[2] and configs[3] at full size in
+    the bench's launch configuration (parallel.LocalStep): sampled outputs against the oracle,
+    the rest through properties that hold at any size.
+
+    Stage (1) is checked against the oracle's O on sampled columns; stages (3)-(4) against the
+    oracle applied to the GPU's own O on those columns.  The split matters for configs[3],
+    whose deepest layers have |<O_i>|/std(O_i) ~ 1e9: the FP64 rounding of O itself (2e-15,
+    on either side) then moves Obar by ~1e-6 relative, so no two independently rounded FP64
+    computations of O agree on S_b there (reading R11); centring, Gram and solve
+    are still held to the north_star bars on identical inputs."""
     from paper_2510_08430_b200 import parallel
     w = workloads.CONFIGS[cfg]
     spins, params = workloads.make_inputs(w)
     ij, jj = sr.lattice.for_workload(w)
     step = parallel.LocalStep(w.widths, spins, ij, jj, w.lam, dev())
     theta = T(sr.model.pack(params))
+    b = step.buf
+    offs = b.offs
+    rng = np.random.default_rng(cfg)
+    cols = np.sort(np.concatenate([rng.choice(np.arange(offs[i], offs[i + 1]), 6, replace=False)
+                                   for i in range(len(offs) - 1)]))
+    tcols = torch.as_tensor(cols, device=dev())
+    # stage (1) alone: the GPU's O on the sampled columns (step buffers, before the step)
+    sr.sr_jacobian(w.widths, theta, b.spins, b.log_psi, b.O)
+    O_gpu = b.O[:, tcols].cpu().numpy()
     d1, en = step.run(theta)
     d1 = d1.clone()
     d2, _ = step.run(theta)
     assert torch.equal(d1, d2)                              # deterministic reductions
-    b = step.buf
-    rng = np.random.default_rng(cfg)
     ks = rng.choice(w.n_samples, 4, replace=False)
     bonds = hamiltonian.bonds_for(w)
-    # stage (1): sampled rows of O (the buffer now holds A = sqrt(w)(O - <O>); check log psi
-    # and E_loc directly, and O through A + the mean on sampled columns below)
     lp = b.log_psi.cpu().numpy()
     for k in ks:
         assert abs(np.exp(lp[k]) - np.exp(network.forward(params, spins[k])[0])) < 1e-12
     el = b.e_loc.cpu().numpy()
     el_ref = hamiltonian.local_energies(params, spins[ks], bonds)
     assert rel(el[ks], el_ref) < 1e-10
-    # stage (4): sampled S entries from oracle-built centred columns
-    offs = b.offs
-    cols = np.sort(np.concatenate([rng.choice(np.arange(offs[i], offs[i + 1]), 6, replace=False)
-                                   for i in range(len(offs) - 1)]))
+    # stage (1): sampled columns of O against the oracle's derivatives, column by column
     O_cols = np.stack([network.log_derivative_row(params, x)[cols] for x in spins])
-    A_cols, _ = estimators.scaled_centered(O_cols, np.zeros(w.n_samples))
-    A_gpu = b.O[:, torch.as_tensor(cols, device=dev())].cpu().numpy()
-    assert rel(A_gpu, A_cols) < 1e-11
-    blocks = [blk.reshape(offs[i + 1] - offs[i], -1) for i, blk in
-              enumerate(b.s_block(i) for i in range(len(offs) - 1))]
+    col_err = np.linalg.norm(O_gpu - O_cols, axis=0) / np.linalg.norm(O_cols, axis=0)
+    assert np.all(col_err < 1e-12)
+    # stage (3) on the GPU's O: A = (O - <O>)/sqrt(N_s) against the oracle's centring
+    A_ref, _ = estimators.scaled_centered(O_gpu, np.zeros(w.n_samples))
+    A_gpu = b.O[:, tcols].cpu().numpy()
+    assert rel(A_gpu, A_ref) < 1e-11
+    # stage (4): sampled entries of every S_b against the oracle's QGT of the same columns
+    blocks = [b.s_block(i).reshape(offs[i + 1] - offs[i], -1) for i in range(len(offs) - 1)]
     for i in range(len(offs) - 1):
         sel = [c for c in range(len(cols)) if offs[i] <= cols[c] < offs[i + 1]]
-        loc = cols[sel] - offs[i]
-        got = blocks[i][torch.as_tensor(loc, device=dev())][:, torch.as_tensor(loc, device=dev())].cpu().numpy()
-        ref = estimators.qgt_full(O_cols[:, sel])
+        loc = torch.as_tensor(cols[sel] - offs[i], device=dev())
+        got = blocks[i][loc][:, loc].cpu().numpy()
+        ref = estimators.qgt_full(O_gpu[:, sel])
         assert rel(got, ref) < 1e-11
         Sb = blocks[i]
         assert torch.equal(Sb, Sb.conj().T.resolve_conj())   # exactly Hermitian as stored
@@ -325,7 +337,6 @@ def test_full_size_config(sr, cfg):
     assert rel(b.F.cpu().numpy(), Fchk.cpu().numpy()) < 1e-10
     for i in range(len(offs) - 1):
         lo, hi = offs[i], offs[i + 1]
-        Sb = blocks[i]
-        r = Sb @ d1[lo:hi] + w.lam * d1[lo:hi] + b.F[lo:hi]
+        r = blocks[i] @ d1[lo:hi] + w.lam * d1[lo:hi] + b.F[lo:hi]
         assert (torch.linalg.vector_norm(r) / torch.linalg.vector_norm(b.F[lo:hi])).item() < 1e-9
     assert abs(en.item() - el.mean()) < 1e-12 * abs(el.mean())

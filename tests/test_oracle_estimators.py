@@ -103,21 +103,27 @@ def test_scaled_centered_factorisation():
     np.testing.assert_allclose(A @ A.conj().T, estimators.ntk(O, w), rtol=1e-12, atol=1e-15)
 
 
-def test_centering_is_exact_to_double_rounding_under_cancellation():
-    # columns nearly constant over samples (as the last-layer bias derivatives are): the
-    # centred values must equal the exactly computed (rational-arithmetic) ones up to one
-    # double rounding plus the longdouble rounding of the mean (2^-63 |<O>|), i.e. ~1e-13
-    # relative here, where a double-rounded mean would give ~1e-9
+@pytest.mark.parametrize("scale,n", [(1e-7, 33), (1e-9, 4096), (1e-12, 500)])
+def test_centering_is_exact_to_double_rounding_under_cancellation(scale, n):
+    # columns nearly constant over samples (as the deep-layer derivatives are: |<O>|/std up
+    # to ~1e9 at configs[3], ~1e12 here): the centred values must equal the exactly computed
+    # (rational-arithmetic) ones up to one double rounding (R7, R11), where a
+    # double-rounded mean would give errors of ~1e-4 relative and a 64-bit long-double
+    # mean still ~1e-7
     from fractions import Fraction
     rng = np.random.default_rng(8)
     base = 0.731 - 0.25j
-    O = base + 1e-7 * (rng.standard_normal((33, 2)) + 1j * rng.standard_normal((33, 2)))
+    O = base + scale * (rng.standard_normal((n, 2)) + 1j * rng.standard_normal((n, 2)))
     ob = estimators.center(O)
     for c in range(2):
         for part in ("real", "imag"):
             col = [Fraction(float(getattr(v, part))) for v in O[:, c]]
             mean = sum(col) / len(col)
-            exact = [float(v - mean) for v in col]
+            exact = np.array([float(v - mean) for v in col])
             got = getattr(ob[:, c], part)
-            bound = 2.0 ** -52 * np.abs(exact) + 2.0 ** -62 * abs(getattr(base, part))
-            assert np.all(np.abs(got - exact) <= bound)
+            assert np.all(np.abs(got - exact) <= 2.0 ** -52 * np.abs(exact))
+    # the mean itself, and the energy path, to double rounding as well
+    m = estimators.mean_O(O)
+    for c in range(2):
+        exact = sum(Fraction(float(v.real)) for v in O[:, c]) / n
+        assert abs(m[c].real - float(exact)) <= 2.0 ** -52 * abs(float(exact))
