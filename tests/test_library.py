@@ -77,3 +77,34 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "missing.so"))
     with pytest.raises(_lib.SRError):
         _lib.load(build_if_missing=False)
+
+
+def test_int8_engine_host_side(lib):
+    """Engine switch and the int8 Gram's workspace query / argument checks (no device work)."""
+    import paper_2510_08430_b200 as sr
+    assert lib.sr_get_gram_engine() == sr.GRAM_INT8           # library default
+    assert lib.sr_set_gram_engine(7) == -1                    # unknown engine: unchanged
+    assert lib.sr_get_gram_engine() == sr.GRAM_INT8
+    assert lib.sr_set_gram_engine(sr.GRAM_FP64) == sr.GRAM_INT8
+    assert lib.sr_set_gram_engine(sr.GRAM_INT8) == sr.GRAM_FP64
+    offs = sr._lib._offsets([0, 3280, 9760, 16240])
+    ws = lib.sr_block_qgt_i8_workspace_bytes(4096, 3, offs)
+    # 7 digit slices x (Re A, Im A, -Re A) x N_s bytes per parameter, plus column exponents
+    assert ws >= 21 * 4096 * 16240
+    assert lib.sr_block_qgt_i8_workspace_bytes(8192, 3, offs) > ws
+    assert lib.sr_block_qgt_i8_workspace_bytes(-1, 3, offs) == 0
+    bad = sr._lib._offsets([0, 10, 5])
+    assert lib.sr_block_qgt_i8_workspace_bytes(16, 2, bad) == 0
+    rc = lib.sr_block_qgt_i8(16, 2, bad, None, 10, None, None, 0, None)
+    assert rc == -1 and b"block_offsets" in lib.sr_last_error()
+    rc = lib.sr_block_qgt_i8(16, 3, offs, None, 16240, None, None, 0, None)
+    assert rc == -1 and b"null" in lib.sr_last_error()
+    rc = lib.sr_block_qgt_i8(16, 3, offs, None, 100, None, None, 0, None)   # lda < n_p
+    assert rc == -1
+
+
+def test_kernel_timer_without_launches(lib):
+    import paper_2510_08430_b200 as sr
+    sr.sr_kernel_timer(True)
+    sr.sr_kernel_timer(False)
+    assert sr.sr_kernel_time_ms("gram_i8") == (0.0, 0)
