@@ -49,6 +49,7 @@ constexpr int kChunkK = 16384;            // K' per exact int32 accumulation
 constexpr bool kATmem = SR_OZ_A_TMEM;     // operand A staged into TMEM by tcgen05.cp
 constexpr uint32_t kACol = kSlices * BN;  // TMEM columns [448, 504): the A digits of one K step
 constexpr int kBand = 8;                  // row panels per rasterisation band
+constexpr int kNonFinite = 1 << 20;       // column exponent marking a column with Inf / NaN
 constexpr int kMaxBlk = 24;
 constexpr int kEpiWarps = 8;              // two per TMEM lane quarter, 32 columns each
 constexpr int kThreads = 64 + 32 * kEpiWarps;   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2.. epilogue
@@ -361,7 +362,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ej = __shfl_sync(0xffffffffu, ej_lane, e);
           const int j = jb + e;
           if (!row_ok || j >= n || j > i) continue;
-          const double val = pow2_scale(vals[e], ei + ej - 60);
+          // a non-finite input column poisons its row and column of the result, as in FP64
+          const double val = (ei == kNonFinite || ej == kNonFinite) ? __longlong_as_double(0x7FF8000000000000LL)
+                                                                     : pow2_scale(vals[e], ei + ej - 60);
           if (MODE == MODE_SUB) {
             // C -= G on the lower triangle by a fire-and-forget reduction in L2
             // (red.global.add.f64): each element receives exactly one addend per launch
@@ -399,18 +402,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// Column maxima of max(|Re|, |Im|) over samples (as ordered bit patterns of non-negative doubles).
+// Column maxima of max(|Re|, |Im|) over samples, as the bit patterns of |x|: for
+// non-negative doubles the order of the patterns is the order of the values, and Inf / NaN
+// patterns exceed every finite one, so a non-finite entry marks its column (kNonFinite).
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+  return (unsigned long long)__double_as_longlong(x) & 0x7FFFFFFFFFFFFFFFULL;
+}
+constexpr unsigned long long kInfBits = 0x7FF0000000000000ULL;
 __global__ void oz_colmax(const double2* __restrict__ A, long long lda, long long c0, int n, long long K,
                           int rows_per, unsigned long long* __restrict__ mx) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const long long k0 = (long long)blockIdx.y * rows_per, k1 = min(K, k0 + rows_per);
-  double m = 0.0;
+  unsigned long long m = 0;
   for (long long k = k0; k < k1; k++) {
     const double2 v = A[k * lda + c0 + j];
-    m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+    m = max(m, max(abs_bits(v.x), abs_bits(v.y)));
   }
-  atomicMax(mx + j, (unsigned long long)__double_as_longlong(m));
+  atomicMax(mx + j, m);
+}
+
+// Column exponent E with max < 2^E (0 for an all-zero column, kNonFinite if Inf / NaN).
+__device__ __forceinline__ int column_exponent(unsigned long long mbits) {
+  if (mbits >= kInfBits) return kNonFinite;
+  int e = 0;
+  const double m = __longlong_as_double((long long)mbits);
+  if (m > 0.0) frexp(m, &e);
+  return e;
 }
 
 // Signed base-256 digits from bytes: with C = 128 sum_{p<7} 256^p (> 2^54 > |X|),
@@ -460,9 +478,9 @@ __global__ void __launch_bounds__(256) oz_split(const double2* __restrict__ A, l
   const long long k0 = (long long)blockIdx.y * 64;
   int e = 0;
   if (j < n) {
-    const double m = __longlong_as_double((long long)mx[j]);
-    if (m > 0.0) frexp(m, &e);
+    e = column_exponent(mx[j]);
     if (blockIdx.y == 0 && kg == 0) expo[j] = e;
+    if (e == kNonFinite) e = 0;   // digits of a marked column are never used
   }
   uint64_t pk[3][kSlices];
   {
@@ -505,13 +523,13 @@ __global__ void __launch_bounds__(256) oz_split_rows(const double2* __restrict__
   const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (i >= m) return;
   const double2* row = L + (long long)i * ldl;
-  double mx = 0.0;
-  for (int k = lane; k < K; k += 32) mx = fmax(mx, fmax(fabs(row[k].x), fabs(row[k].y)));
+  unsigned long long mx = 0;
+  for (int k = lane; k < K; k += 32) mx = max(mx, max(abs_bits(row[k].x), abs_bits(row[k].y)));
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  int e = 0;
-  if (mx > 0.0) frexp(mx, &e);
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int e = column_exponent(mx);
   if (lane == 0) expo[i] = e;
+  if (e == kNonFinite) e = 0;
   for (int k0 = lane * 8; k0 < Kp; k0 += 256) {
     uint64_t pk[3][kSlices];
     {

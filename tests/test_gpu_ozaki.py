@@ -201,3 +201,22 @@ def test_full_and_ntk_int8(sr, int8_engine):
     ref = solvers.full_solve(estimators.qgt_full(O), F, w.lam)
     assert rel(d_full.cpu().numpy(), ref) < 1e-9
     assert rel(d_ntk.cpu().numpy(), ref) < 1e-9
+
+
+def test_block_qgt_i8_non_finite_columns(sr):
+    """Inf / NaN in a column of A poison that row and column of S_b (as an FP64 Gram does)
+    and leave the other entries exact."""
+    rng = np.random.default_rng(4)
+    ns, n = 64, 70
+    A = rng.standard_normal((ns, n)) + 1j * rng.standard_normal((ns, n))
+    A[5, 3] = np.nan
+    A[9, 40] = complex(np.inf, 0.0)
+    S = torch.empty(n * n, dtype=C128, device=dev())
+    sr.sr_block_qgt_i8(T(A), [0, n], S)
+    g = S.cpu().numpy().reshape(n, n)
+    bad = [3, 40]
+    good = [i for i in range(n) if i not in bad]
+    for b in bad:
+        assert np.all(np.isnan(g[b])) and np.all(np.isnan(g[:, b]))
+    ref = A[:, good].conj().T @ A[:, good]
+    assert rel(g[np.ix_(good, good)], ref) < 1e-11
