@@ -173,6 +173,8 @@ SR_API sr_status sr_block_qgt(int64_t n_samples, int n_blocks,
  * n_samples * max_k|A_ki| * max_k|A_kj| per entry, the size of an FP64 dot product's.
  * Workspace: sr_block_qgt_i8_workspace_bytes(n_samples, ...) bytes (digit slices,
  * 42 bytes per sample per parameter of the largest group of blocks, plus column scales).
+ * Non-finite input: an Inf or NaN anywhere in column i of A makes row i and column i of
+ * S_b NaN (the other entries are unaffected), as with an FP64 Gram.
  * Errors: SR_ERR_INVALID on bad sizes, SR_ERR_WORKSPACE if the workspace is too small. */
 SR_API size_t sr_block_qgt_i8_workspace_bytes(int64_t n_samples, int n_blocks,
                                               const int64_t* block_offsets /*host*/);

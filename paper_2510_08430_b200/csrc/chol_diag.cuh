@@ -245,10 +245,12 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
       syrkb<BS>(T, o - BS, t - 32, 224, true);
     }
     __syncthreads();
+    SR_DIAG_PROBE(17 + 2 * k);
     if (k < NB / BS - 1) {
       if (t < 4 * (NB - o - BS)) trsm_quad<BS>(T, o, o + BS + (t >> 2), t & 3, dinv);
       __syncthreads();
     }
+    SR_DIAG_PROBE(18 + 2 * k);
   }
   SR_DIAG_PROBE(2);
   if (t == 0 && bad && info) atomicCAS(info, 0, (int)(B.row_base + (long long)p * NB + bad));

@@ -5,7 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
-__device__ long long g_probe[32];
+__device__ long long g_probe[64];
 #define SR_DIAG_PROBE(i) \
   do {                   \
     if (threadIdx.x == 0) g_probe[i] = clock64(); \
@@ -62,7 +62,7 @@ int main() {
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     if (r > 0) tot += ms;
-    long long h[32];
+    long long h[64];
     cudaMemcpyFromSymbol(h, g_probe, sizeof(h));
     if (r > 0) {
       const int ids[6] = {0, 1, 2, 14, 15, 16};
@@ -77,6 +77,15 @@ int main() {
     all += acc[ids[u]] / (reps - 1);
   }
   printf("total %.0f cycles; event time %.2f us per launch\n", all, 1e3 * tot / (reps - 1));
+  {   // per-round split of the factor phase (last repetition): factor+syrk | trsm
+    long long h[64];
+    cudaMemcpyFromSymbol(h, g_probe, sizeof(h));
+    long long prev = h[1];
+    for (int k = 0; k < 8; k++) {
+      printf("round %d: factor/syrk %6lld  trsm %6lld\n", k, h[17 + 2 * k] - prev, h[18 + 2 * k] - h[17 + 2 * k]);
+      prev = h[18 + 2 * k];
+    }
+  }
   // check: L L^H = A and X L = I (lower triangles)
   std::vector<double2> L(n * n), X(n * n);
   cudaMemcpy(L.data(), dF, n * n * 16, cudaMemcpyDeviceToHost);
