@@ -200,7 +200,11 @@ int trail_ctas(int nblocks) {
 }
 
 // Factorisation + substitutions of ONE block on one stream (two-level blocking, see header).
-sr_status solve_block(CholSet& cs, int b, cudaStream_t st) {
+// st2 / ea / eb: a second stream and two events for this block.  Within a strip, the panel
+// chain on `st` updates only the NEXT column with panel p (it is all that diag(p+1) and
+// trsm(p+1) need); the strip's later columns receive panel p's update on st2 meanwhile,
+// joined back before the next-column update that writes the same column.
+sr_status solve_block(CholSet& cs, int b, cudaStream_t st, cudaStream_t st2, cudaEvent_t ea, cudaEvent_t eb) {
   const CholBlock& B = cs.b[b];
   // Two-level blocking: strips of kStrip panels.  Inside a strip each panel p is factored
   // (chol_diag), its column solved (TRSM), the RHS updated, and only the strip's own later
@@ -217,21 +221,30 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st) {
       SR_LAUNCHED();
       const long long m = B.npad - (long long)(p + 1) * NB;
       if (m <= 0) continue;
-      gram::ProbSet trsm{}, inner{};
+      gram::ProbSet trsm{}, inner_next{}, inner_rest{};
       double2* panel = B.Fm + (long long)(p + 1) * NB * B.npad + (long long)p * NB;
       gram::add_prob(trsm, panel, B.npad, B.linv + (long long)p * NB * NB, NB, panel, B.npad, (int)m, NB, NB, false);
       for (int jj = p + 1; jj < pend; jj++) {   // later columns of the strip, rows i >= jj
         const double2* lrows = B.Fm + (long long)jj * NB * B.npad + (long long)p * NB;
         double2* cblk = B.Fm + (long long)jj * NB * B.npad + (long long)jj * NB;
-        gram::add_prob(inner, lrows, B.npad, lrows, B.npad, cblk, B.npad, (int)(B.npad - (long long)jj * NB), NB, NB,
-                       false);
+        gram::add_prob(jj == p + 1 ? inner_next : inner_rest, lrows, B.npad, lrows, B.npad, cblk, B.npad,
+                       (int)(B.npad - (long long)jj * NB), NB, NB, false);
       }
       timer_begin("chol_trsm", st);
       SR_TRY((gram::launch<gram::NH, gram::STORE>(trsm, st)));
       timer_end(st);
+      const bool rest = inner_rest.count > 0;
+      if (rest) SR_CUDA(cudaEventRecord(ea, st));           // L column p ready for st2
+      // inner_next(p) writes column p+1, which panel p-1's rest update (on st2) also writes
+      if (p > p0 && p + 1 < pend) SR_CUDA(cudaStreamWaitEvent(st, eb, 0));
       timer_begin("chol_inner", st);
-      if (inner.count) SR_TRY((gram::launch<gram::NH, gram::SUB>(inner, st)));
+      if (inner_next.count) SR_TRY((gram::launch<gram::NH, gram::SUB>(inner_next, st)));
       timer_end(st);
+      if (rest) {
+        SR_CUDA(cudaStreamWaitEvent(st2, ea, 0));
+        SR_TRY((gram::launch<gram::NH, gram::SUB>(inner_rest, st2)));
+        SR_CUDA(cudaEventRecord(eb, st2));
+      }
     }
     const long long m = B.npad - (long long)pend * NB;
     if (m > 0) {   // the strip's y applied to the right-hand side of all later rows
@@ -275,8 +288,8 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st) {
 // latency-bound panel chain of one block is scheduled ahead of another block's big update).
 constexpr int kSideStreams = 8;
 struct SidePool {
-  cudaStream_t s[kSideStreams];
-  cudaEvent_t fork, join[kSideStreams];
+  cudaStream_t s[kSideStreams], s2[kSideStreams];
+  cudaEvent_t fork, join[kSideStreams], ea[kSideStreams], eb[kSideStreams];
   bool ok = false;
 };
 sr_status side_pool(SidePool*& out) {
@@ -286,7 +299,10 @@ sr_status side_pool(SidePool*& out) {
     SR_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     for (int i = 0; i < kSideStreams; i++) {
       SR_CUDA(cudaStreamCreateWithPriority(&pool.s[i], cudaStreamNonBlocking, hi));
+      SR_CUDA(cudaStreamCreateWithPriority(&pool.s2[i], cudaStreamNonBlocking, hi));
       SR_CUDA(cudaEventCreateWithFlags(&pool.join[i], cudaEventDisableTiming));
+      SR_CUDA(cudaEventCreateWithFlags(&pool.ea[i], cudaEventDisableTiming));
+      SR_CUDA(cudaEventCreateWithFlags(&pool.eb[i], cudaEventDisableTiming));
     }
     SR_CUDA(cudaEventCreateWithFlags(&pool.fork, cudaEventDisableTiming));
     pool.ok = true;
@@ -311,17 +327,20 @@ sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStr
     SR_CUDA(cudaFuncSetAttribute(chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagSmem));
     diag_attr = true;
   }
+  SidePool* pool;
+  SR_TRY(side_pool(pool));
+  SR_CUDA(cudaEventRecord(pool->fork, st));
   if (cs.count == 1) {
-    SR_TRY(solve_block(cs, 0, st));
+    SR_CUDA(cudaStreamWaitEvent(pool->s2[0], pool->fork, 0));
+    SR_TRY(solve_block(cs, 0, st, pool->s2[0], pool->ea[0], pool->eb[0]));
   } else {
     // independent blocks on side streams, forked from and joined back into `st`
-    SidePool* pool;
-    SR_TRY(side_pool(pool));
-    SR_CUDA(cudaEventRecord(pool->fork, st));
     for (int b = 0; b < cs.count; b++) {
-      cudaStream_t sb = pool->s[b % kSideStreams];
+      const int i = b % kSideStreams;
+      cudaStream_t sb = pool->s[i];
       SR_CUDA(cudaStreamWaitEvent(sb, pool->fork, 0));
-      SR_TRY(solve_block(cs, b, sb));
+      SR_CUDA(cudaStreamWaitEvent(pool->s2[i], pool->fork, 0));
+      SR_TRY(solve_block(cs, b, sb, pool->s2[i], pool->ea[i], pool->eb[i]));
     }
     for (int i = 0; i < std::min(cs.count, kSideStreams); i++) {
       SR_CUDA(cudaEventRecord(pool->join[i], pool->s[i]));
