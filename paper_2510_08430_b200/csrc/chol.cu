@@ -200,11 +200,17 @@ int trail_ctas(int nblocks) {
 }
 
 // Factorisation + substitutions of ONE block on one stream (two-level blocking, see header).
-// st2 / ea / eb: a second stream and two events for this block.  Within a strip, the panel
-// chain on `st` updates only the NEXT column with panel p (it is all that diag(p+1) and
-// trsm(p+1) need); the strip's later columns receive panel p's update on st2 meanwhile,
-// joined back before the next-column update that writes the same column.
-sr_status solve_block(CholSet& cs, int b, cudaStream_t st, cudaStream_t st2, cudaEvent_t ea, cudaEvent_t eb) {
+// Side streams of the block: Q.s2 / Q.s3 with events Q.ea / Q.eb / Q.ec.  Within a strip the
+// panel chain on `st` runs diag(p) -> TRSM(p) -> the update of the next DIAGONAL tile
+// (p+1, p+1) by panel p -> diag(p+1): that tile is all diag(p+1) reads.  The rest of column
+// p+1 (rows below the tile) takes panel p's update on s3 meanwhile, joined before TRSM(p+1);
+// the strip's later columns take it on s2, joined before the next update that writes the
+// same column.
+struct BlockStreams {
+  cudaStream_t s2, s3;
+  cudaEvent_t ea, eb, ec;
+};
+sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q) {
   const CholBlock& B = cs.b[b];
   // Two-level blocking: strips of kStrip panels.  Inside a strip each panel p is factored
   // (chol_diag), its column solved (TRSM), the RHS updated, and only the strip's own later
@@ -219,31 +225,47 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, cudaStream_t st2, cud
       chol_diag<<<1, 256, kDiagSmem, st>>>(B, cs.info, p, p0);
       timer_end(st);
       SR_LAUNCHED();
+      // the previous panel's update of this column below the diagonal tile (s3) must be
+      // complete before TRSM(p) (and joined into st in any case)
+      if (p > p0) SR_CUDA(cudaStreamWaitEvent(st, Q.ec, 0));
       const long long m = B.npad - (long long)(p + 1) * NB;
       if (m <= 0) continue;
-      gram::ProbSet trsm{}, inner_next{}, inner_rest{};
+      gram::ProbSet trsm{}, next_tile{}, next_rows{}, inner_rest{};
       double2* panel = B.Fm + (long long)(p + 1) * NB * B.npad + (long long)p * NB;
       gram::add_prob(trsm, panel, B.npad, B.linv + (long long)p * NB * NB, NB, panel, B.npad, (int)m, NB, NB, false);
       for (int jj = p + 1; jj < pend; jj++) {   // later columns of the strip, rows i >= jj
         const double2* lrows = B.Fm + (long long)jj * NB * B.npad + (long long)p * NB;
         double2* cblk = B.Fm + (long long)jj * NB * B.npad + (long long)jj * NB;
-        gram::add_prob(jj == p + 1 ? inner_next : inner_rest, lrows, B.npad, lrows, B.npad, cblk, B.npad,
-                       (int)(B.npad - (long long)jj * NB), NB, NB, false);
+        const int rows = (int)(B.npad - (long long)jj * NB);
+        if (jj == p + 1) {
+          gram::add_prob(next_tile, lrows, B.npad, lrows, B.npad, cblk, B.npad, NB, NB, NB, false);
+          if (rows > NB)
+            gram::add_prob(next_rows, lrows + (long long)NB * B.npad, B.npad, lrows, B.npad,
+                           cblk + (long long)NB * B.npad, B.npad, rows - NB, NB, NB, false);
+        } else {
+          gram::add_prob(inner_rest, lrows, B.npad, lrows, B.npad, cblk, B.npad, rows, NB, NB, false);
+        }
       }
       timer_begin("chol_trsm", st);
-      SR_TRY((gram::launch<gram::NH, gram::STORE>(trsm, st)));
+      SR_TRY((gram::launch_skinny<gram::STORE>(trsm, st)));
       timer_end(st);
-      const bool rest = inner_rest.count > 0;
-      if (rest) SR_CUDA(cudaEventRecord(ea, st));           // L column p ready for st2
-      // inner_next(p) writes column p+1, which panel p-1's rest update (on st2) also writes
-      if (p > p0 && p + 1 < pend) SR_CUDA(cudaStreamWaitEvent(st, eb, 0));
+      const bool side = next_tile.count > 0;
+      if (side) SR_CUDA(cudaEventRecord(Q.ea, st));           // L column p ready for s2 / s3
+      // the next-column updates write column p+1, which panel p-1's rest update (s2) also writes
+      if (p > p0 && p + 1 < pend) SR_CUDA(cudaStreamWaitEvent(st, Q.eb, 0));
       timer_begin("chol_inner", st);
-      if (inner_next.count) SR_TRY((gram::launch<gram::NH, gram::SUB>(inner_next, st)));
+      if (side) SR_TRY((gram::launch_skinny<gram::SUB>(next_tile, st)));
       timer_end(st);
-      if (rest) {
-        SR_CUDA(cudaStreamWaitEvent(st2, ea, 0));
-        SR_TRY((gram::launch<gram::NH, gram::SUB>(inner_rest, st2)));
-        SR_CUDA(cudaEventRecord(eb, st2));
+      if (side) {
+        SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.ea, 0));
+        if (p > p0) SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.eb, 0));
+        SR_TRY((gram::launch_skinny<gram::SUB>(next_rows, Q.s3)));
+        SR_CUDA(cudaEventRecord(Q.ec, Q.s3));
+      }
+      if (inner_rest.count) {
+        SR_CUDA(cudaStreamWaitEvent(Q.s2, Q.ea, 0));
+        SR_TRY((gram::launch_skinny<gram::SUB>(inner_rest, Q.s2)));
+        SR_CUDA(cudaEventRecord(Q.eb, Q.s2));
       }
     }
     const long long m = B.npad - (long long)pend * NB;
@@ -288,8 +310,9 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, cudaStream_t st2, cud
 // latency-bound panel chain of one block is scheduled ahead of another block's big update).
 constexpr int kSideStreams = 8;
 struct SidePool {
-  cudaStream_t s[kSideStreams], s2[kSideStreams];
-  cudaEvent_t fork, join[kSideStreams], ea[kSideStreams], eb[kSideStreams];
+  cudaStream_t s[kSideStreams];
+  BlockStreams q[kSideStreams];
+  cudaEvent_t fork, join[kSideStreams];
   bool ok = false;
 };
 sr_status side_pool(SidePool*& out) {
@@ -298,11 +321,14 @@ sr_status side_pool(SidePool*& out) {
     int lo = 0, hi = 0;
     SR_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     for (int i = 0; i < kSideStreams; i++) {
+      BlockStreams& q = pool.q[i];
       SR_CUDA(cudaStreamCreateWithPriority(&pool.s[i], cudaStreamNonBlocking, hi));
-      SR_CUDA(cudaStreamCreateWithPriority(&pool.s2[i], cudaStreamNonBlocking, hi));
+      SR_CUDA(cudaStreamCreateWithPriority(&q.s2, cudaStreamNonBlocking, hi));
+      SR_CUDA(cudaStreamCreateWithPriority(&q.s3, cudaStreamNonBlocking, hi));
       SR_CUDA(cudaEventCreateWithFlags(&pool.join[i], cudaEventDisableTiming));
-      SR_CUDA(cudaEventCreateWithFlags(&pool.ea[i], cudaEventDisableTiming));
-      SR_CUDA(cudaEventCreateWithFlags(&pool.eb[i], cudaEventDisableTiming));
+      SR_CUDA(cudaEventCreateWithFlags(&q.ea, cudaEventDisableTiming));
+      SR_CUDA(cudaEventCreateWithFlags(&q.eb, cudaEventDisableTiming));
+      SR_CUDA(cudaEventCreateWithFlags(&q.ec, cudaEventDisableTiming));
     }
     SR_CUDA(cudaEventCreateWithFlags(&pool.fork, cudaEventDisableTiming));
     pool.ok = true;
@@ -331,16 +357,18 @@ sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStr
   SR_TRY(side_pool(pool));
   SR_CUDA(cudaEventRecord(pool->fork, st));
   if (cs.count == 1) {
-    SR_CUDA(cudaStreamWaitEvent(pool->s2[0], pool->fork, 0));
-    SR_TRY(solve_block(cs, 0, st, pool->s2[0], pool->ea[0], pool->eb[0]));
+    SR_CUDA(cudaStreamWaitEvent(pool->q[0].s2, pool->fork, 0));
+    SR_CUDA(cudaStreamWaitEvent(pool->q[0].s3, pool->fork, 0));
+    SR_TRY(solve_block(cs, 0, st, pool->q[0]));
   } else {
     // independent blocks on side streams, forked from and joined back into `st`
     for (int b = 0; b < cs.count; b++) {
       const int i = b % kSideStreams;
       cudaStream_t sb = pool->s[i];
       SR_CUDA(cudaStreamWaitEvent(sb, pool->fork, 0));
-      SR_CUDA(cudaStreamWaitEvent(pool->s2[i], pool->fork, 0));
-      SR_TRY(solve_block(cs, b, sb, pool->s2[i], pool->ea[i], pool->eb[i]));
+      SR_CUDA(cudaStreamWaitEvent(pool->q[i].s2, pool->fork, 0));
+      SR_CUDA(cudaStreamWaitEvent(pool->q[i].s3, pool->fork, 0));
+      SR_TRY(solve_block(cs, b, sb, pool->q[i]));
     }
     for (int i = 0; i < std::min(cs.count, kSideStreams); i++) {
       SR_CUDA(cudaEventRecord(pool->join[i], pool->s[i]));

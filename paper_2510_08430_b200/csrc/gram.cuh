@@ -292,5 +292,123 @@ inline sr_status launch(const ProbSet& ps, cudaStream_t st) {
   return SR_OK;
 }
 
+// Skinny products of the Cholesky panel chain (flavor NH, K <= 64, N <= 64): the panel
+// TRSM L_ip = A_ip Linv_p^H and the in-strip updates C -= L_i L_j^H are M x 64 x 64 with M
+// up to the block size.  One 64x64 tile per CTA leaves most SMs idle and its 4-step
+// pipeline latency (~20 us) sits on the critical path; here a CTA owns 16 full rows
+// (all 64 columns, so the in-place TRSM reads its rows before anyone writes them), the whole
+// K = 64 is staged in two cp.async halves, and 4 warps each take 16 columns.
+constexpr int SK_TM = 16;
+constexpr int SK_LD = 68;   // 1088 B per row (mod 128 = 64: conflict-free LDS.128 fragments)
+constexpr int SK_THREADS = 128;
+constexpr size_t kSkinnySmem = (size_t)(SK_TM + 64) * SK_LD * sizeof(double2);   // 87 KB
+
+template <int EP>
+__global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_constant__ ProbSet ps) {
+  extern __shared__ __align__(16) double2 smem[];
+  double2* sa = smem;
+  double2* sb = smem + SK_TM * SK_LD;
+  int pi = 0;
+#pragma unroll 1
+  while (pi + 1 < ps.count && (long long)blockIdx.x >= ps.p[pi + 1].tile_begin) pi++;
+  const Prob& P = ps.p[pi];
+  const int m0 = (int)((long long)blockIdx.x - P.tile_begin) * SK_TM;
+  const long long K = P.K;
+#pragma unroll
+  for (int h = 0; h < 2; h++) {   // two commit groups: k in [32h, 32h + 32)
+#pragma unroll
+    for (int it = 0; it < (SK_TM * 32) / SK_THREADS; it++) {
+      const int e = threadIdx.x + it * SK_THREADS;
+      const int r = e >> 5, k = 32 * h + (e & 31);
+      const bool v = (m0 + r < P.M) && (k < K);
+      cp_async16(sa + r * SK_LD + k, v ? P.A + (long long)(m0 + r) * P.lda + k : P.A, v);
+    }
+#pragma unroll
+    for (int it = 0; it < (64 * 32) / SK_THREADS; it++) {
+      const int e = threadIdx.x + it * SK_THREADS;
+      const int r = e >> 5, k = 32 * h + (e & 31);
+      const bool v = (r < P.N) && (k < K);
+      cp_async16(sb + r * SK_LD + k, v ? P.B + (long long)r * P.ldb + k : P.B, v);
+    }
+    cp_commit();
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lr = lane >> 2, lk = lane & 3;
+  double acc_r[2][2][2], acc_i[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 2; b++) {
+      acc_r[a][b][0] = acc_r[a][b][1] = 0.0;
+      acc_i[a][b][0] = acc_i[a][b][1] = 0.0;
+    }
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    if (h == 0) cp_wait<1>(); else cp_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int k4 = 32 * h; k4 < 32 * h + 32; k4 += 4) {
+      double ar[2], ai[2], nai[2], br[2], bi[2];
+#pragma unroll
+      for (int mi = 0; mi < 2; mi++) {
+        const double2 v = sa[(mi * 8 + lr) * SK_LD + k4 + lk];
+        ar[mi] = v.x;
+        ai[mi] = v.y;
+        nai[mi] = -v.y;
+      }
+#pragma unroll
+      for (int ni = 0; ni < 2; ni++) {
+        const double2 v = sb[(w * 16 + ni * 8 + lr) * SK_LD + k4 + lk];
+        br[ni] = v.x;
+        bi[ni] = -v.y;   // b(k,n) = conj(B[n][k])
+      }
+#pragma unroll
+      for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+        for (int ni = 0; ni < 2; ni++) {
+          dmma(acc_r[mi][ni][0], acc_r[mi][ni][1], ar[mi], br[ni]);
+          dmma(acc_i[mi][ni][0], acc_i[mi][ni][1], ar[mi], bi[ni]);
+          dmma(acc_r[mi][ni][0], acc_r[mi][ni][1], nai[mi], bi[ni]);
+          dmma(acc_i[mi][ni][0], acc_i[mi][ni][1], ai[mi], br[ni]);
+        }
+    }
+  }
+#pragma unroll
+  for (int mi = 0; mi < 2; mi++)
+#pragma unroll
+    for (int ni = 0; ni < 2; ni++) {
+      const int m = m0 + mi * 8 + lr;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int n = w * 16 + ni * 8 + 2 * lk + h;
+        if (m >= P.M || n >= P.N) continue;
+        const double2 v = make_double2(acc_r[mi][ni][h], acc_i[mi][ni][h]);
+        double2* c = P.C + (long long)m * P.ldc + n;
+        *c = EP == SUB ? csub(*c, v) : v;
+      }
+    }
+}
+
+// Launch a set of NH problems with N <= 64 and K <= 64 (not lower) on the skinny kernel.
+template <int EP>
+inline sr_status launch_skinny(ProbSet ps, cudaStream_t st) {
+  static_assert(EP == SUB || EP == STORE, "skinny epilogues: SUB or STORE");
+  long long total = 0;
+  for (int i = 0; i < ps.count; i++) {
+    if (ps.p[i].N > 64 || ps.p[i].K > 64 || ps.p[i].lower) return SR_ERR_INVALID;
+    ps.p[i].tile_begin = total;
+    total += (ps.p[i].M + SK_TM - 1) / SK_TM;
+  }
+  if (total == 0) return SR_OK;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SR_CUDA(cudaFuncSetAttribute(skinny_kernel<EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSkinnySmem));
+    attr_set = true;
+  }
+  skinny_kernel<EP><<<(unsigned)total, SK_THREADS, kSkinnySmem, st>>>(ps);
+  SR_LAUNCHED();
+  return SR_OK;
+}
+
 }  // namespace gram
 }  // namespace sr

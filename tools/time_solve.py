@@ -30,6 +30,24 @@ def run(sizes, reps=3):
         sr.sr_block_solve(offs, S, F, 1e-3, d, workspace=ws)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            sr.sr_block_solve(offs, S, F, 1e-3, d, workspace=ws)
+        graph.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(10):
+            graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        gms = e0.elapsed_time(e1) / 10
+        plain = []
+        for _ in range(5):   # without the kernel timer's events
+            e0.record()
+            sr.sr_block_solve(offs, S, F, 1e-3, d, workspace=ws)
+            e1.record()
+            torch.cuda.synchronize()
+            plain.append(e0.elapsed_time(e1))
         names = ("trail_i8", "trail_dmma", "chol_diag", "chol_trsm", "chol_rhs", "chol_inner", "chol_back")
         for k in names:
             sr.sr_kernel_time_ms(k)
@@ -48,7 +66,8 @@ def run(sizes, reps=3):
                 parts.append(f"{k} {tk / reps:.2f} ms/{nk // reps} ({1e3 * tk / nk:.1f} us each)")
         out[eng] = d.clone()
         fl = sum(4.0 * n ** 3 / 3 for n in sizes)
-        print(f"sizes={sizes} {eng}: {ms:.2f} ms/solve ({fl / ms / 1e9:.1f} TFLOP/s ZPOTRF-equivalent)"
+        print(f"sizes={sizes} {eng}: {ms:.2f} ms/solve with timer, untimed min/median "
+              f"{min(plain):.2f}/{sorted(plain)[2]:.2f} ms, graph {gms:.2f} ms ({fl / ms / 1e9:.1f} TFLOP/s ZPOTRF-equivalent)"
               + "\n    " + "; ".join(parts), flush=True)
     r = torch.linalg.vector_norm(out["int8"] - out["fp64"]) / torch.linalg.vector_norm(out["fp64"])
     res = []
