@@ -16,6 +16,7 @@
 //   trail (engine)   A_ij -= L_i,strip L_j,strip^H for i >= j beyond the strip (NH/SUB)
 // then back substitution L^H x = y strip by strip (x_p = Linv_p^H y_p inside the strip,
 // then y_{<strip} -= L_strip,<^H x_strip) and dtheta = -x.
+#include <cooperative_groups.h>
 #include <cstdlib>
 
 #include "chol.cuh"
@@ -83,73 +84,110 @@ __global__ void chol_rhs_update(const CholBlock B, long long c0, long long c1) {
 }
 
 // Back substitution L^H x = y by strips of panels [p0, pend), two launches per strip:
-// chol_back_strip (one CTA): for p = pend-1 .. p0: x_p = Linv_p^H y_p, then
-//   y_q -= L_pq^H x_p for the strip's earlier panels q in [p0, p);
-// chol_back_rest (one CTA per 64 columns c < 64 p0): y_c -= sum_{r in strip} conj(L[r][c]) x_r.
+// chol_back_strip, a cluster of kStrip CTAs, CTA j owning panel q = p0 + j and its y_q in
+// shared memory: step p = pend-1 .. p0 the owner of p forms x_p = Linv_p^H y_p and writes
+// it into the shared memory of the CTAs j < p - p0 (distributed shared memory), one
+// cluster barrier, then each of those applies y_q -= L_pq^H x_p.  Every CTA streams the
+// 64x64 blocks it needs (L_pq for p = pend-1 .. q+1, then Linv_q) through a double buffer
+// with cp.async, a step ahead of use, so a step is two shared-memory GEMVs and a barrier
+// instead of a round trip to HBM per block on one SM.
+// chol_back_rest (one CTA per 32 columns c < 64 p0): y_c -= sum_{r in strip} conj(L[r][c]) x_r.
 // Reductions run in a fixed order (deterministic).
-__global__ void __launch_bounds__(256) chol_back_strip(const CholBlock B, int p0, int pend) {
-  __shared__ double2 ys[kStrip][NB];
-  __shared__ double2 xs[NB];
+static_assert(kStrip <= 8, "the back-substitution cluster holds one CTA per strip panel (portable size 8)");
+constexpr size_t kBackSmem = (size_t)2 * NB * NB * sizeof(double2);   // 128 KB
+
+__global__ void __cluster_dims__(kStrip, 1, 1) __launch_bounds__(256) chol_back_strip(const CholBlock B, int p0, int pend) {
+  extern __shared__ __align__(16) double2 bsm[];   // [2][64][64] streamed blocks
+  __shared__ double2 xb[2][NB];
+  __shared__ double2 ys[NB];
+  __shared__ double2 red[4][NB];
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int j = (int)cl.block_rank();
+  const int nps = pend - p0, q = p0 + j;
+  const bool act = j < nps;
+  const int nblk = act ? nps - j : 0;   // L_pq for p = pend-1 .. q+1, then Linv_q
   const long long np = B.npad;
-  const int t = threadIdx.x, c = t >> 2, q4 = t & 3;
-  for (int e = t; e < (pend - p0) * NB; e += 256) ys[e >> 6][e & 63] = B.rhs[(long long)p0 * NB + e];
-  __syncthreads();
-  for (int p = pend - 1; p >= p0; p--) {
-    const double2* linv = B.linv + (long long)p * NB * NB;
-    // Linv_p is lower triangular: entries r < c are zero, so the full 16-term sums are exact;
-    // 4 independent partial sums keep 4 loads in flight.
+  const int t = threadIdx.x, c = t & 63, rq = t >> 6;
+  auto issue = [&](int i) {
+    double2* dst = bsm + (size_t)(i & 1) * NB * NB;
+    const bool lin = i == nblk - 1;
+    const double2* src = lin ? B.linv + (long long)q * NB * NB : B.Fm + (long long)(pend - 1 - i) * NB * np + (long long)q * NB;
+    const long long ld = lin ? NB : np;
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const int e = t + 256 * u, r = e >> 6, cc = e & 63;
+      gram::cp_async16(dst + r * NB + cc, src + (long long)r * ld + cc, true);
+    }
+    gram::cp_commit();
+  };
+  // y_blk = sum_r conj(Blk[r][c]) v[r] over the 64 rows, 4 row groups then a fixed-order sum
+  auto gemv = [&](const double2* blk, const double2* v) {
     double2 sa[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
 #pragma unroll
-    for (int i = 0; i < 16; i++) cfma_conj(sa[i & 3], linv[(4 * i + q4) * NB + c], ys[p - p0][4 * i + q4]);
-    double2 sx = cadd(cadd(sa[0], sa[1]), cadd(sa[2], sa[3]));
-    sx.x += __shfl_xor_sync(0xffffffffu, sx.x, 1);
-    sx.y += __shfl_xor_sync(0xffffffffu, sx.y, 1);
-    sx.x += __shfl_xor_sync(0xffffffffu, sx.x, 2);
-    sx.y += __shfl_xor_sync(0xffffffffu, sx.y, 2);
-    if (q4 == 0) {
-      xs[c] = sx;
-      B.xout[(long long)p * NB + c] = sx;
-    }
+    for (int i = 0; i < 16; i++) cfma_conj(sa[i & 3], blk[(rq + 4 * i) * NB + c], v[rq + 4 * i]);
+    red[rq][c] = cadd(cadd(sa[0], sa[1]), cadd(sa[2], sa[3]));
     __syncthreads();
-    for (int q = p0; q < p; q++) {   // y_q[c] -= sum_r conj(L[p*64+r][q*64+c]) x_p[r]
-      const double2* lp = B.Fm + (long long)p * NB * np + (long long)q * NB + c;
-      double2 sb[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
-                       make_double2(0.0, 0.0)};
-#pragma unroll
-      for (int i = 0; i < 16; i++) cfma_conj(sb[i & 3], lp[(long long)(4 * i + q4) * np], xs[4 * i + q4]);
-      double2 sy = cadd(cadd(sb[0], sb[1]), cadd(sb[2], sb[3]));
-      sy.x += __shfl_xor_sync(0xffffffffu, sy.x, 1);
-      sy.y += __shfl_xor_sync(0xffffffffu, sy.y, 1);
-      sy.x += __shfl_xor_sync(0xffffffffu, sy.x, 2);
-      sy.y += __shfl_xor_sync(0xffffffffu, sy.y, 2);
-      if (q4 == 0) ys[q - p0][c] = csub(ys[q - p0][c], sy);
+    return cadd(cadd(red[0][c], red[1][c]), cadd(red[2][c], red[3][c]));
+  };
+  if (act) {
+    if (t < NB) ys[t] = B.rhs[(long long)q * NB + t];
+    issue(0);
+    if (nblk > 1) issue(1);
+  }
+  int cur = 0;
+  for (int st = 0; st < nps; st++) {
+    const int jp = nps - 1 - st;   // owner of panel p = pend - 1 - st
+    if (j == jp) {                 // x_p = Linv_p^H y_p (Linv is this CTA's last block)
+      gram::cp_wait<0>();
+      __syncthreads();
+      const double2 x = gemv(bsm + (size_t)(cur & 1) * NB * NB, ys);
+      if (t < NB) {
+        B.xout[(long long)(p0 + jp) * NB + t] = x;
+        for (int jj = 0; jj < jp; jj++) cl.map_shared_rank(&xb[st & 1][0], jj)[t] = x;
+      }
     }
-    __syncthreads();
+    cl.sync();
+    if (j < jp) {   // y_q -= L_pq^H x_p
+      if (cur + 1 < nblk) gram::cp_wait<1>();
+      else gram::cp_wait<0>();
+      __syncthreads();
+      const double2 v = gemv(bsm + (size_t)(cur & 1) * NB * NB, &xb[st & 1][0]);
+      if (t < NB) ys[t] = csub(ys[t], v);
+      __syncthreads();   // the buffer of block cur is free, ys updated
+      cur++;
+      if (cur + 1 < nblk) issue(cur + 1);
+    }
   }
 }
 
+// One CTA per 32 columns: warp w sums rows w, w + 8, ... of the strip (8 loads in flight
+// per thread: the column GEMV is latency-bound with fewer), then a fixed-order reduction.
 __global__ void __launch_bounds__(256) chol_back_rest(const CholBlock B, int p0, int pend) {
   __shared__ double2 xs[kStrip * NB];
-  __shared__ double2 red[4][NB];
+  __shared__ double2 red[8][33];
   const long long np = B.npad;
-  const int t = threadIdx.x, cl = t & 63, rq = t >> 6;
+  const int t = threadIdx.x, cl = t & 31, rq = t >> 5;
   const int nr = (pend - p0) * NB;
   for (int e = t; e < nr; e += 256) xs[e] = B.xout[(long long)p0 * NB + e];
   __syncthreads();
   const long long ncol = (long long)p0 * NB;
-  for (long long cb = (long long)blockIdx.x * NB; cb < ncol; cb += (long long)gridDim.x * NB) {
+  for (long long cb = (long long)blockIdx.x * 32; cb < ncol; cb += (long long)gridDim.x * 32) {
     const long long c = cb + cl;
-    double2 sa[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-    const double2* col = B.Fm + ((long long)p0 * NB) * np + c;
-    for (int r0 = rq; r0 < nr; r0 += 16) {   // nr is a multiple of 64
+    double2 sa[8];
 #pragma unroll
-      for (int u = 0; u < 4; u++) cfma_conj(sa[u], col[(long long)(r0 + 4 * u) * np], xs[r0 + 4 * u]);
+    for (int u = 0; u < 8; u++) sa[u] = make_double2(0.0, 0.0);
+    const double2* col = B.Fm + ((long long)p0 * NB) * np + c;
+    for (int r0 = rq; r0 < nr; r0 += 64) {   // nr is a multiple of 64
+#pragma unroll
+      for (int u = 0; u < 8; u++) cfma_conj(sa[u], col[(long long)(r0 + 8 * u) * np], xs[r0 + 8 * u]);
     }
-    const double2 s = cadd(cadd(sa[0], sa[1]), cadd(sa[2], sa[3]));
-    red[rq][cl] = s;
+    red[rq][cl] = cadd(cadd(cadd(sa[0], sa[1]), cadd(sa[2], sa[3])), cadd(cadd(sa[4], sa[5]), cadd(sa[6], sa[7])));
     __syncthreads();
     if (rq == 0) {
-      const double2 v = cadd(cadd(red[0][cl], red[1][cl]), cadd(red[2][cl], red[3][cl]));
+      double2 v = red[0][cl];
+#pragma unroll
+      for (int w = 1; w < 8; w++) v = cadd(v, red[w][cl]);
       B.rhs[c] = csub(B.rhs[c], v);
     }
     __syncthreads();
@@ -295,13 +333,15 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
   for (int p0 = (B.P - 1) / kStrip * kStrip; p0 >= 0; p0 -= kStrip) {
     const int pend = std::min(p0 + kStrip, B.P);
     timer_begin("chol_back", st);
-    chol_back_strip<<<1, 256, 0, st>>>(B, p0, pend);
+    chol_back_strip<<<kStrip, 256, kBackSmem, st>>>(B, p0, pend);
     SR_LAUNCHED();
-    if (p0 > 0) {
-      chol_back_rest<<<(unsigned)std::min(p0, 4 * kNumSMs), 256, 0, st>>>(B, p0, pend);
-      SR_LAUNCHED();
-    }
     timer_end(st);
+    if (p0 > 0) {
+      timer_begin("chol_back_rest", st);
+      chol_back_rest<<<(unsigned)std::min(2 * p0, 4 * kNumSMs), 256, 0, st>>>(B, p0, pend);
+      SR_LAUNCHED();
+      timer_end(st);
+    }
   }
   return SR_OK;
 }
@@ -351,6 +391,7 @@ sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStr
   static bool diag_attr = false;
   if (!diag_attr) {
     SR_CUDA(cudaFuncSetAttribute(chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagSmem));
+    SR_CUDA(cudaFuncSetAttribute(chol_back_strip, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBackSmem));
     diag_attr = true;
   }
   SidePool* pool;

@@ -6,6 +6,9 @@
 #ifndef SR_DIAG_PROBE
 #define SR_DIAG_PROBE(i)
 #endif
+#ifndef SR_DIAG_ISOLATE
+#define SR_DIAG_ISOLATE 1
+#endif
 #ifndef SR_DIAG_BS
 #define SR_DIAG_BS 8   // diagonal sub-block of the single-warp factor (8 or 16)
 #endif
@@ -78,6 +81,48 @@ __device__ __forceinline__ void factorb(double2* T, int o, int lane, double* din
         d[s] = v;
       }
     }
+  }
+}
+
+// (a') BS = 8, the form used: lane r < 8 holds row r of the block in registers; step c
+// takes the pivot from lane c and column c from lanes s > c by shuffles (no shared-memory
+// round trip, no redundant per-lane diagonal), so a step is shfl -> rsqrt -> scale ->
+// shfl -> next-pivot update (~200 cycles) with ~4 (7 - c) FP64 instructions issued.
+__device__ __forceinline__ void factor8(double2* T, int o, int lane, double* dinv, int* bad) {
+  const int r = lane & 7;
+  double2 d[8];
+#pragma unroll
+  for (int s = 0; s < 8; s++) d[s] = s <= r ? T[(o + r) * LDT + o + s] : make_double2(0.0, 0.0);
+  double piv = __shfl_sync(0xffffffffu, d[0].x, 0);
+#pragma unroll
+  for (int c = 0; c < 8; c++) {
+    if (!(piv > 0.0)) {
+      if (lane == 0 && *bad == 0) *bad = o + c + 1;
+      piv = 1.0;
+    }
+    // the next pivot first (the critical path): lane c+1 holds A[c+1][c+1] and the
+    // unscaled A[c+1][c], so A[c+1][c+1] - |A[c+1][c]|^2 / piv needs only isd^2
+    const double n2 = d[c].x * d[c].x + d[c].y * d[c].y;
+    const double isd = rsqrt(piv);
+    double pn = 0.0;
+    if (c < 7) pn = __shfl_sync(0xffffffffu, d[c < 7 ? c + 1 : 7].x - n2 * (isd * isd), c < 7 ? c + 1 : 7);
+    if (r == c) d[c] = make_double2(piv * isd, 0.0);
+    else if (r > c) d[c] = cscale(d[c], isd);
+    if (lane == 0) dinv[o + c] = isd;
+#pragma unroll
+    for (int s = c + 1; s < 8; s++) {
+      const double lx = __shfl_sync(0xffffffffu, d[c].x, s), ly = __shfl_sync(0xffffffffu, d[c].y, s);
+      if (r >= s) {   // d[s] -= L[r][c] conj(L[s][c])
+        d[s].x -= d[c].x * lx + d[c].y * ly;
+        d[s].y -= d[c].y * lx - d[c].x * ly;
+      }
+    }
+    piv = pn;
+  }
+  if (lane < 8) {
+#pragma unroll
+    for (int s = 0; s < 8; s++)
+      if (s <= r) T[(o + r) * LDT + o + s] = d[s];
   }
 }
 
@@ -240,9 +285,16 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
     if (warp == 0) {
       if (k > 0) syrkb_diag<BS>(T, o - BS, lane);
       __syncwarp();
-      factorb<BS>(T, o, lane, dinv, &bad);
+      if (BS == 8) factor8(T, o, lane, dinv, &bad);
+      else factorb<BS>(T, o, lane, dinv, &bad);
     } else if (k > 0) {
+#if SR_DIAG_ISOLATE
+      // warp 4 shares warp 0's scheduler (and FP64 pipe): it stays idle so the factor
+      // steps, the critical path, are not slowed by SYRK instructions on that pipe
+      if (warp != 4) syrkb<BS>(T, o - BS, warp < 4 ? t - 32 : t - 64, 192, true);
+#else
       syrkb<BS>(T, o - BS, t - 32, 224, true);
+#endif
     }
     __syncthreads();
     SR_DIAG_PROBE(17 + 2 * k);

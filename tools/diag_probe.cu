@@ -86,6 +86,12 @@ int main() {
       prev = h[18 + 2 * k];
     }
   }
+  {   // optional fine probes 40..50 (inside factor8 for o == 0, when compiled in)
+    long long h[64];
+    cudaMemcpyFromSymbol(h, g_probe, sizeof(h));
+    for (int i = 41; i <= 50; i++)
+      if (h[i] && h[i - 1]) printf("probe %d-%d: %lld\n", i - 1, i, h[i] - h[i - 1]);
+  }
   // check: L L^H = A and X L = I (lower triangles)
   std::vector<double2> L(n * n), X(n * n);
   cudaMemcpy(L.data(), dF, n * n * 16, cudaMemcpyDeviceToHost);

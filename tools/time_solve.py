@@ -48,7 +48,7 @@ def run(sizes, reps=3):
             e1.record()
             torch.cuda.synchronize()
             plain.append(e0.elapsed_time(e1))
-        names = ("trail_i8", "trail_dmma", "chol_diag", "chol_trsm", "chol_rhs", "chol_inner", "chol_back")
+        names = ("trail_i8", "trail_dmma", "chol_diag", "chol_trsm", "chol_rhs", "chol_inner", "chol_back", "chol_back_rest")
         for k in names:
             sr.sr_kernel_time_ms(k)
         sr.sr_kernel_timer(True)
