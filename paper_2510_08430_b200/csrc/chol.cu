@@ -237,6 +237,17 @@ int trail_ctas(int nblocks) {
   return 0;   // measured: capping the grid slows the 3-block solve (trailing throughput bound)
 }
 
+// Programmatic dependent launch along the panel chain (diag -> TRSM -> next tile -> diag);
+// SR_PDL=0 turns it off (A/B measurements).
+bool pdl_chain() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SR_PDL");
+    v = e ? atoi(e) != 0 : 1;
+  }
+  return v != 0;
+}
+
 // Factorisation + substitutions of ONE block on one stream (two-level blocking, see header).
 // Side streams of the block: Q.s2 / Q.s3 with events Q.ea / Q.eb / Q.ec.  Within a strip the
 // panel chain on `st` runs diag(p) -> TRSM(p) -> the update of the next DIAGONAL tile
@@ -260,7 +271,8 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
     const int pend = std::min(p0 + kStrip, B.P);
     for (int p = p0; p < pend; p++) {
       timer_begin("chol_diag", st);
-      chol_diag<<<1, 256, kDiagSmem, st>>>(B, cs.info, p, p0);
+      if (pdl_chain()) SR_CUDA(launch_pdl(chol_diag, dim3(1), dim3(256), kDiagSmem, st, B, cs.info, p, p0));
+      else chol_diag<<<1, 256, kDiagSmem, st>>>(B, cs.info, p, p0);
       timer_end(st);
       SR_LAUNCHED();
       // the previous panel's update of this column below the diagonal tile (s3) must be
@@ -285,14 +297,14 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
         }
       }
       timer_begin("chol_trsm", st);
-      SR_TRY((gram::launch_skinny<gram::STORE>(trsm, st)));
+      SR_TRY((gram::launch_skinny<gram::STORE>(trsm, st, pdl_chain())));
       timer_end(st);
       const bool side = next_tile.count > 0;
       if (side) SR_CUDA(cudaEventRecord(Q.ea, st));           // L column p ready for s2 / s3
       // the next-column updates write column p+1, which panel p-1's rest update (s2) also writes
       if (p > p0 && p + 1 < pend) SR_CUDA(cudaStreamWaitEvent(st, Q.eb, 0));
       timer_begin("chol_inner", st);
-      if (side) SR_TRY((gram::launch_skinny<gram::SUB>(next_tile, st)));
+      if (side) SR_TRY((gram::launch_skinny<gram::SUB>(next_tile, st, pdl_chain())));
       timer_end(st);
       if (side) {
         SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.ea, 0));

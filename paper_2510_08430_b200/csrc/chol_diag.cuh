@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
   const long long np = B.npad;
   double2* tile = B.Fm + (long long)p * NB * np + (long long)p * NB;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  pdl_wait();
   SR_DIAG_PROBE(0);
   {   // 16 independent loads per thread in flight, then the shared-memory stores
     double2 v[16];
@@ -372,6 +373,7 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
     y.y += __shfl_xor_sync(0xffffffffu, y.y, 2);
     if (q == 0) B.rhs[(long long)p * NB + r] = y;
   }
+  pdl_trigger();
   __syncthreads();
   SR_DIAG_PROBE(16);
 }

@@ -1,5 +1,6 @@
 // common.cuh — shared device helpers for the block-SR library (sm_100a only).
 #pragma once
+#include <utility>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -55,6 +56,30 @@ int gram_engine();
       return SR_ERR_CUDA;                                                              \
     }                                                                                  \
   } while (0)
+
+// Programmatic dependent launch (panel chain of the Cholesky): a kernel launched with
+// launch_pdl may begin while its stream predecessor finishes; it calls pdl_wait() before
+// touching anything the predecessor writes (a no-op for an ordinary launch), and a
+// predecessor calls pdl_trigger() after its last store so the dependent is launched
+// without waiting for the grid's retirement.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 #define SR_TRY(call)                 \
   do {                               \

@@ -314,6 +314,7 @@ __global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_cons
   const Prob& P = ps.p[pi];
   const int m0 = (int)((long long)blockIdx.x - P.tile_begin) * SK_TM;
   const long long K = P.K;
+  pdl_wait();
 #pragma unroll
   for (int h = 0; h < 2; h++) {   // two commit groups: k in [32h, 32h + 32)
 #pragma unroll
@@ -387,11 +388,12 @@ __global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_cons
         *c = EP == SUB ? csub(*c, v) : v;
       }
     }
+  pdl_trigger();
 }
 
 // Launch a set of NH problems with N <= 64 and K <= 64 (not lower) on the skinny kernel.
 template <int EP>
-inline sr_status launch_skinny(ProbSet ps, cudaStream_t st) {
+inline sr_status launch_skinny(ProbSet ps, cudaStream_t st, bool pdl = false) {
   static_assert(EP == SUB || EP == STORE, "skinny epilogues: SUB or STORE");
   long long total = 0;
   for (int i = 0; i < ps.count; i++) {
@@ -405,7 +407,8 @@ inline sr_status launch_skinny(ProbSet ps, cudaStream_t st) {
     SR_CUDA(cudaFuncSetAttribute(skinny_kernel<EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSkinnySmem));
     attr_set = true;
   }
-  skinny_kernel<EP><<<(unsigned)total, SK_THREADS, kSkinnySmem, st>>>(ps);
+  if (pdl) SR_CUDA(launch_pdl(skinny_kernel<EP>, dim3((unsigned)total), dim3(SK_THREADS), kSkinnySmem, st, ps));
+  else skinny_kernel<EP><<<(unsigned)total, SK_THREADS, kSkinnySmem, st>>>(ps);
   SR_LAUNCHED();
   return SR_OK;
 }
