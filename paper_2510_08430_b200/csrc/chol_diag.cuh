@@ -31,7 +31,7 @@ constexpr int NB = 64;
 //   inverse: X_kk = D_k^{-1} (warp k, lane j = column j), then by block distance d = 1..3:
 //     W_ik = sum_{j=k}^{i-1} L_ij X_jk and X_ik = -X_ii W_ik (i = k + d), 2x2 patches.
 constexpr int LDT = NB + 1;   // 1040-byte rows
-constexpr size_t kDiagSmem = (size_t)2 * NB * LDT * sizeof(double2);
+constexpr size_t kDiagSmem = ((size_t)2 * NB * LDT + 32 * 33) * sizeof(double2);   // T, X, W
 
 __device__ __forceinline__ void cfma_conjb(double2& acc, double2 a, double2 b) {   // acc += a conj(b)
   acc.x = fma(a.x, b.x, acc.x);
@@ -85,9 +85,10 @@ __device__ __forceinline__ void factorb(double2* T, int o, int lane, double* din
 }
 
 // (a') BS = 8, the form used: lane r < 8 holds row r of the block in registers; step c
-// takes the pivot from lane c and column c from lanes s > c by shuffles (no shared-memory
-// round trip, no redundant per-lane diagonal), so a step is shfl -> rsqrt -> scale ->
-// shfl -> next-pivot update (~200 cycles) with ~4 (7 - c) FP64 instructions issued.
+// takes column c from lanes s > c by shuffles (no shared-memory round trip, no redundant
+// per-lane diagonal), and lane c+1 forms the next pivot A[c+1][c+1] - |A[c+1][c]|^2 isd^2
+// before the rank-1 update.  (Spreading the block over all 32 lanes, two entries per
+// lane, measured slower: 3.5k vs 2.9k cycles per 8x8 factor, tools/diag_probe.cu.)
 __device__ __forceinline__ void factor8(double2* T, int o, int lane, double* dinv, int* bad) {
   const int r = lane & 7;
   double2 d[8];
@@ -100,8 +101,6 @@ __device__ __forceinline__ void factor8(double2* T, int o, int lane, double* din
       if (lane == 0 && *bad == 0) *bad = o + c + 1;
       piv = 1.0;
     }
-    // the next pivot first (the critical path): lane c+1 holds A[c+1][c+1] and the
-    // unscaled A[c+1][c], so A[c+1][c+1] - |A[c+1][c]|^2 / piv needs only isd^2
     const double n2 = d[c].x * d[c].x + d[c].y * d[c].y;
     const double isd = rsqrt(piv);
     double pn = 0.0;
@@ -232,6 +231,70 @@ __device__ __forceinline__ void inv16(const double2* T, double2* X, int o, int l
   }
 }
 
+// 8x8 complex tile on DMMA: C += sum_{k in [k0, k1)} A[r][k] B[k][c] for r, c < 8, with A and
+// B row-major in shared memory (k0, k1 multiples of 4).  Lane l holds C[l/4][2(l%4) + {0,1}].
+constexpr int LDW = 33;
+__device__ __forceinline__ void dmma_t(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void tile_mma(const double2* A, int lda, const double2* B, int ldb, int k0, int k1, int lane,
+                                         double* cr, double* ci) {
+  const int lr = lane >> 2, lk = lane & 3;
+#pragma unroll 4
+  for (int k = k0; k < k1; k += 4) {
+    const double2 a = A[lr * lda + k + lk], b = B[(k + lk) * ldb + lr];
+    dmma_t(cr[0], cr[1], a.x, b.x);
+    dmma_t(cr[0], cr[1], -a.y, b.y);
+    dmma_t(ci[0], ci[1], a.x, b.y);
+    dmma_t(ci[0], ci[1], a.y, b.x);
+  }
+}
+__device__ __forceinline__ void tile_put(double2* C, int ldc, int lane, const double* cr, const double* ci, double sg) {
+  const int lr = lane >> 2, lk = lane & 3;
+  C[lr * ldc + 2 * lk] = make_double2(sg * cr[0], sg * ci[0]);
+  C[lr * ldc + 2 * lk + 1] = make_double2(sg * cr[1], sg * ci[1]);
+}
+
+// C[r][c] -= sum_{m < 8} L[r][o+m] conj(L[c][o+m]) for the 8x8 tile at (r0, c0), r >= c only.
+__device__ __forceinline__ void syrk_tile(double2* T, int o, int r0, int c0, int lane) {
+  const int lr = lane >> 2, lk = lane & 3;
+  double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < 8; k += 4) {
+    const double2 a = T[(r0 + lr) * LDT + o + k + lk], b = T[(c0 + lr) * LDT + o + k + lk];
+    dmma_t(cr[0], cr[1], a.x, b.x);
+    dmma_t(cr[0], cr[1], a.y, b.y);
+    dmma_t(ci[0], ci[1], a.y, b.x);
+    dmma_t(ci[0], ci[1], -a.x, b.y);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const int r = r0 + lr, c = c0 + 2 * lk + h;
+    if (r >= c) {
+      double2& x = T[r * LDT + c];
+      x = make_double2(x.x - cr[h], x.y - ci[h]);
+    }
+  }
+}
+
+// (c') BS = 8 trailing update on DMMA: A[r][s] -= sum_m L[r][o+m] conj(L[s][o+m]) over
+// 8x8 tiles (I >= J) of the trailing triangle, one tile per warp at a time; the tile of
+// the next diagonal block is left to warp 0 (syrk_diag_mma).
+__device__ __forceinline__ void syrk_mma(double2* T, int o, int wi, int nw, int lane) {
+  const int b0 = o + 8, nb = (NB - b0) / 8, cnt = nb * (nb + 1) / 2;
+  for (int e = wi; e < cnt; e += nw) {
+    int I, J;
+    tri_patch(e, I, J);
+    if (I == 0) continue;
+    syrk_tile(T, o, b0 + 8 * I, b0 + 8 * J, lane);
+  }
+}
+
+// Warp 0: the next diagonal block (o+8, o+8) receives block o's update (one DMMA tile).
+__device__ __forceinline__ void syrk_diag_mma(double2* T, int o, int lane) { syrk_tile(T, o, o + 8, o + 8, lane); }
+
 __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, int p, int p0) {
   extern __shared__ double2 dsm[];
   double2* T = dsm;              // [64][LDT]: A (lower) -> L
@@ -284,7 +347,10 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
   for (int k = 0; k < NB / BS; k++) {
     const int o = BS * k;
     if (warp == 0) {
-      if (k > 0) syrkb_diag<BS>(T, o - BS, lane);
+      if (k > 0) {
+        if (BS == 8) syrk_diag_mma(T, o - BS, lane);
+        else syrkb_diag<BS>(T, o - BS, lane);
+      }
       __syncwarp();
       if (BS == 8) factor8(T, o, lane, dinv, &bad);
       else factorb<BS>(T, o, lane, dinv, &bad);
@@ -292,7 +358,10 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
 #if SR_DIAG_ISOLATE
       // warp 4 shares warp 0's scheduler (and FP64 pipe): it stays idle so the factor
       // steps, the critical path, are not slowed by SYRK instructions on that pipe
-      if (warp != 4) syrkb<BS>(T, o - BS, warp < 4 ? t - 32 : t - 64, 192, true);
+      if (warp != 4) {
+        if (BS == 8) syrk_mma(T, o - BS, warp < 4 ? warp - 1 : warp - 2, 6, lane);
+        else syrkb<BS>(T, o - BS, warp < 4 ? t - 32 : t - 64, 192, true);
+      }
 #else
       syrkb<BS>(T, o - BS, t - 32, 224, true);
 #endif
@@ -310,51 +379,43 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
   if (warp < 4) inv16(T, X, 16 * warp, lane, dinv);
   __syncthreads();
   SR_DIAG_PROBE(14);
-  for (int d = 1; d < 4; d++) {
-    const int nbk = 4 - d;
-    const bool act = t < nbk * 64;
-    const int kb = t >> 6, ib = kb + d, pr = (t & 63) >> 3, pc = t & 7;
-    const int r0 = 16 * ib + 2 * pr, c0 = 16 * kb + 2 * pc;
-    double2 acc[2][2] = {{make_double2(0.0, 0.0), make_double2(0.0, 0.0)},
-                         {make_double2(0.0, 0.0), make_double2(0.0, 0.0)}};
-    if (act) {   // W_ik = sum_{m in blocks k..i-1} L[r][m] X[m][c]
-      for (int m = 16 * kb; m < 16 * ib; m++) {
-        const double2 l0 = T[r0 * LDT + m], l1 = T[(r0 + 1) * LDT + m];
-        const double2 x0 = X[m * LDT + c0], x1 = X[m * LDT + c0 + 1];
-        cfma(acc[0][0], l0, x0);
-        cfma(acc[0][1], l0, x1);
-        cfma(acc[1][0], l1, x0);
-        cfma(acc[1][1], l1, x1);
+  // Inverse by recursive doubling on the FP64 tensor cores: X21 = -X22 L21 X11 for the
+  // 16-blocks inside each 32-block (both at once), then for the two 32-blocks.  Each warp
+  // owns 8x8 output tiles (DMMA 8x8x4, a complex product as 4 real MMAs); X is lower
+  // triangular with explicit zeros above the diagonal inside the 16-blocks (inv16), so a
+  // tile's K range starts at its column (L X) or ends at its row (X W).
+  {
+    double2* W = dsm + 2 * NB * LDT;   // [32][LDW] scratch product
+    {   // 16 -> 32: W' = L21' X11' (rows 32b+16.., cols 32b..), X21' = -X22' W'
+      const int bb = warp >> 2, ti = (warp >> 1) & 1, tj = warp & 1, o = 32 * bb;
+      double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+      tile_mma(T + (o + 16 + 8 * ti) * LDT + o, LDT, X + o * LDT + o + 8 * tj, LDT, 8 * tj, 16, lane, cr, ci);
+      tile_put(W + (16 * bb + 8 * ti) * LDW + 8 * tj, LDW, lane, cr, ci, 1.0);
+      __syncthreads();
+      cr[0] = cr[1] = ci[0] = ci[1] = 0.0;
+      tile_mma(X + (o + 16 + 8 * ti) * LDT + o + 16, LDT, W + 16 * bb * LDW + 8 * tj, LDW, 0, 8 * ti + 8, lane, cr, ci);
+      tile_put(X + (o + 16 + 8 * ti) * LDT + o + 8 * tj, LDT, lane, cr, ci, -1.0);
+      __syncthreads();
+    }
+    {   // 32 -> 64: W = L21 X11 (rows 32.., cols 0..31), X21 = -X22 W; two tiles per warp
+      const int ti = warp >> 1;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int tj = 2 * (warp & 1) + h;
+        double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+        tile_mma(T + (32 + 8 * ti) * LDT, LDT, X + 8 * tj, LDT, 8 * tj, 32, lane, cr, ci);
+        tile_put(W + 8 * ti * LDW + 8 * tj, LDW, lane, cr, ci, 1.0);
       }
+      __syncthreads();
 #pragma unroll
-      for (int u = 0; u < 2; u++)
-#pragma unroll
-        for (int v = 0; v < 2; v++) X[(r0 + u) * LDT + c0 + v] = acc[u][v];
-    }
-    __syncthreads();
-    if (act) {   // X_ik = -X_ii W_ik (X_ii lower triangular)
-#pragma unroll
-      for (int u = 0; u < 2; u++)
-#pragma unroll
-        for (int v = 0; v < 2; v++) acc[u][v] = make_double2(0.0, 0.0);
-      for (int m = 16 * ib; m <= r0 + 1; m++) {
-        const double2 w0 = X[m * LDT + c0], w1 = X[m * LDT + c0 + 1];
-        const double2 x0 = m <= r0 ? X[r0 * LDT + m] : make_double2(0.0, 0.0);
-        const double2 x1 = X[(r0 + 1) * LDT + m];
-        cfma(acc[0][0], x0, w0);
-        cfma(acc[0][1], x0, w1);
-        cfma(acc[1][0], x1, w0);
-        cfma(acc[1][1], x1, w1);
+      for (int h = 0; h < 2; h++) {
+        const int tj = 2 * (warp & 1) + h;
+        double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+        tile_mma(X + (32 + 8 * ti) * LDT + 32, LDT, W + 8 * tj, LDW, 0, 8 * ti + 8, lane, cr, ci);
+        tile_put(X + (32 + 8 * ti) * LDT + 8 * tj, LDT, lane, cr, ci, -1.0);
       }
+      __syncthreads();
     }
-    __syncthreads();
-    if (act) {
-#pragma unroll
-      for (int u = 0; u < 2; u++)
-#pragma unroll
-        for (int v = 0; v < 2; v++) X[(r0 + u) * LDT + c0 + v] = make_double2(-acc[u][v].x, -acc[u][v].y);
-    }
-    __syncthreads();
   }
   SR_DIAG_PROBE(15);
   double2* linv = B.linv + (long long)p * NB * NB;
