@@ -6,230 +6,26 @@
 #ifndef SR_DIAG_PROBE
 #define SR_DIAG_PROBE(i)
 #endif
-#ifndef SR_DIAG_ISOLATE
-#define SR_DIAG_ISOLATE 1
-#endif
-#ifndef SR_DIAG_BS
-#define SR_DIAG_BS 8   // diagonal sub-block of the single-warp factor (8 or 16)
-#endif
-
 namespace sr {
 namespace cholk {
 
 constexpr int NB = 64;
 
 // One CTA per block: factor the 64x64 diagonal tile of panel p, form its inverse
-// X = Linv_p and y_p = Linv_p b_p.  Blocked by BS = 8 (the latency of a 64-step column
-// recursion with a block barrier per step is what limited the unblocked forms; 8 beat 16,
-// tools/diag_probe.cu: 66.6k vs 75.3k cycles):
-//   for each BS-column block k (offset o = BS k):
-//     (a) warp 0 factors D_k = A[o:o+BS, o:o+BS] in registers, lane r = row r, columns
-//         broadcast through shared memory, 1/sqrt of each pivot kept in dinv;
-//     (b) rows r >= o+BS solve x D_k^H = A[r, o:o+BS] (a quad per row, right-looking);
-//     (c) A[r][s] -= sum_m L[r][o+m] conj(L[s][o+m]) on the trailing lower triangle
-//         (2x2 register patches), overlapped with (a) of the next block.
-//   inverse: X_kk = D_k^{-1} (warp k, lane j = column j), then by block distance d = 1..3:
-//     W_ik = sum_{j=k}^{i-1} L_ij X_jk and X_ik = -X_ii W_ik (i = k + d), 2x2 patches.
+// X = Linv_p and y_p = Linv_p b_p.  Blocked by 8 (a 64-step column recursion with a block
+// barrier per step is what limited the unblocked forms):
+//   for each 8-column block k (offset o = 8k):
+//     (a) warp 0 factors D_k = A[o:o+8, o:o+8] in registers (lane r = row r, columns by
+//         shuffles) and, in lanes 8..15 of the same instruction stream, D_k^{-1};
+//     (b) rows r >= o+8: L[r, o:o+8] = A[r, o:o+8] D_k^{-H}, 8x8 DMMA tiles;
+//     (c) A[r][s] -= sum_m L[r][o+m] conj(L[s][o+m]) on the trailing lower triangle as
+//         8x8 DMMA tiles (warps 1-3, 5-7), overlapped with (a) of the next block, whose
+//         own diagonal tile warp 0 updates first.
+//   inverse: X21 = -X22 L21 X11 by recursive doubling 8 -> 16 -> 32 -> 64 on DMMA.
+// Phase timings: tools/diag_probe.cu (66.9k cycles for the first scalar-FP64 version,
+// 50.1k with the DMMA SYRK and inverse levels).
 constexpr int LDT = NB + 1;   // 1040-byte rows
 constexpr size_t kDiagSmem = ((size_t)2 * NB * LDT + 32 * 33) * sizeof(double2);   // T, X, W
-
-__device__ __forceinline__ void cfma_conjb(double2& acc, double2 a, double2 b) {   // acc += a conj(b)
-  acc.x = fma(a.x, b.x, acc.x);
-  acc.x = fma(a.y, b.y, acc.x);
-  acc.y = fma(a.y, b.x, acc.y);
-  acc.y = fma(-a.x, b.y, acc.y);
-}
-
-// (a) warp 0: D = L L^H for the 16x16 block at (o, o) of T, in place.  Lane r < 16 holds
-// row r; step c scales column c, publishes it to T (one __syncwarp) and applies the
-// rank-1 update to the later columns of its row, reading L[s][c] back as shared-memory
-// broadcasts.  Every lane also keeps the running diagonal dg[s] = A_ss - sum_k |L_sk|^2
-// (the same arithmetic as the owner's update of its own diagonal entry), so each step's
-// pivot is available locally without a broadcast.
-template <int BS>
-__device__ __forceinline__ void factorb(double2* T, int o, int lane, double* dinv, int* bad) {
-  double2 d[BS];
-  double dg[BS];
-  const int r = lane;
-#pragma unroll
-  for (int s = 0; s < BS; s++) {
-    d[s] = (r < BS && s <= r) ? T[(o + r) * LDT + o + s] : make_double2(0.0, 0.0);
-    dg[s] = T[(o + s) * LDT + o + s].x;
-  }
-#pragma unroll
-  for (int c = 0; c < BS; c++) {
-    double piv = dg[c];
-    if (!(piv > 0.0)) {
-      if (lane == 0 && *bad == 0) *bad = o + c + 1;
-      piv = 1.0;
-    }
-    const double isd = rsqrt(piv);
-    if (r == c) d[c] = make_double2(piv * isd, 0.0);
-    else if (r > c) d[c] = cscale(d[c], isd);
-    if (r < BS && r >= c) T[(o + r) * LDT + o + c] = d[c];
-    if (lane == 0) dinv[o + c] = isd;
-    __syncwarp();
-#pragma unroll
-    for (int s = 1; s < BS; s++) {
-      if (s <= c) continue;
-      const double2 ls = T[(o + s) * LDT + o + c];   // L[s][c]
-      dg[s] -= ls.x * ls.x + ls.y * ls.y;
-      if (r >= s && r < BS) {
-        double2 v = d[s];
-        v.x -= d[c].x * ls.x + d[c].y * ls.y;
-        v.y -= d[c].y * ls.x - d[c].x * ls.y;
-        d[s] = v;
-      }
-    }
-  }
-}
-
-// (a') BS = 8, the form used: lane r < 8 holds row r of the block in registers; step c
-// takes column c from lanes s > c by shuffles (no shared-memory round trip, no redundant
-// per-lane diagonal), and lane c+1 forms the next pivot A[c+1][c+1] - |A[c+1][c]|^2 isd^2
-// before the rank-1 update.  (Spreading the block over all 32 lanes, two entries per
-// lane, measured slower: 3.5k vs 2.9k cycles per 8x8 factor, tools/diag_probe.cu.)
-__device__ __forceinline__ void factor8(double2* T, int o, int lane, double* dinv, int* bad) {
-  const int r = lane & 7;
-  double2 d[8];
-#pragma unroll
-  for (int s = 0; s < 8; s++) d[s] = s <= r ? T[(o + r) * LDT + o + s] : make_double2(0.0, 0.0);
-  double piv = __shfl_sync(0xffffffffu, d[0].x, 0);
-#pragma unroll
-  for (int c = 0; c < 8; c++) {
-    if (!(piv > 0.0)) {
-      if (lane == 0 && *bad == 0) *bad = o + c + 1;
-      piv = 1.0;
-    }
-    const double n2 = d[c].x * d[c].x + d[c].y * d[c].y;
-    const double isd = rsqrt(piv);
-    double pn = 0.0;
-    if (c < 7) pn = __shfl_sync(0xffffffffu, d[c < 7 ? c + 1 : 7].x - n2 * (isd * isd), c < 7 ? c + 1 : 7);
-    if (r == c) d[c] = make_double2(piv * isd, 0.0);
-    else if (r > c) d[c] = cscale(d[c], isd);
-    if (lane == 0) dinv[o + c] = isd;
-#pragma unroll
-    for (int s = c + 1; s < 8; s++) {
-      const double lx = __shfl_sync(0xffffffffu, d[c].x, s), ly = __shfl_sync(0xffffffffu, d[c].y, s);
-      if (r >= s) {   // d[s] -= L[r][c] conj(L[s][c])
-        d[s].x -= d[c].x * lx + d[c].y * ly;
-        d[s].y -= d[c].y * lx - d[c].x * ly;
-      }
-    }
-    piv = pn;
-  }
-  if (lane < 8) {
-#pragma unroll
-    for (int s = 0; s < 8; s++)
-      if (s <= r) T[(o + r) * LDT + o + s] = d[s];
-  }
-}
-
-// (b) rows below the block solve x D^H = A[r, o:o+16] with D = L[o:o+16, o:o+16]
-// (diagonal real, 1/D_cc in dinv): a quad per row, lane q holding entries m = q mod 4;
-// step c: x_c = a_c / D_cc from the owner lane, shuffled inside the quad, then
-// a_m -= x_c conj(D[m][c]) for m > c.
-template <int BS>
-__device__ __forceinline__ void trsm_quad(double2* T, int o, int r, int q, const double* dinv) {
-  double2 a[BS / 4];
-#pragma unroll
-  for (int k = 0; k < BS / 4; k++) a[k] = T[r * LDT + o + 4 * k + q];
-#pragma unroll
-  for (int c = 0; c < BS; c++) {
-    if (q == (c & 3)) {   // owner: x_c final, published in place
-      a[c >> 2] = cscale(a[c >> 2], dinv[o + c]);
-      T[r * LDT + o + c] = a[c >> 2];
-    }
-    __syncwarp();
-    const double2 x = T[r * LDT + o + c];
-#pragma unroll
-    for (int k = 0; k < BS / 4; k++) {
-      const int m = 4 * k + q;
-      if (m > c) {
-        const double2 dm = T[(o + m) * LDT + o + c];
-        a[k].x -= x.x * dm.x + x.y * dm.y;
-        a[k].y -= x.y * dm.x - x.x * dm.y;
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < BS / 4; k++) T[r * LDT + o + 4 * k + q] = a[k];
-}
-
-// Lower-triangle patch index e -> (pi, pj), pi >= pj.
-__device__ __forceinline__ void tri_patch(int e, int& pi, int& pj) {
-  pi = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
-  while ((pi + 1) * (pi + 2) / 2 <= e) pi++;
-  while (pi * (pi + 1) / 2 > e) pi--;
-  pj = e - pi * (pi + 1) / 2;
-}
-
-// (c) trailing update of rows/cols [o+BS, 64) by the BS columns L[:, o:o+BS], by threads
-// t in [0, nt); with skip_next the BS x BS diagonal block at o+BS is left to syrkb_diag.
-template <int BS>
-__device__ __forceinline__ void syrkb(double2* T, int o, int t, int nt, bool skip_next) {
-  const int b0 = o + BS, P = (NB - b0) / 2, cnt = P * (P + 1) / 2;
-  for (int e = t; e < cnt; e += nt) {
-    int pi, pj;
-    tri_patch(e, pi, pj);
-    if (skip_next && pi < BS / 2) continue;   // patch rows (and so columns) inside block o+BS
-    const int r0 = b0 + 2 * pi, s0 = b0 + 2 * pj;
-    double2 acc[2][2] = {{make_double2(0.0, 0.0), make_double2(0.0, 0.0)},
-                         {make_double2(0.0, 0.0), make_double2(0.0, 0.0)}};
-#pragma unroll 4
-    for (int m = 0; m < BS; m++) {
-      const double2 lr0 = T[r0 * LDT + o + m], lr1 = T[(r0 + 1) * LDT + o + m];
-      const double2 ls0 = T[s0 * LDT + o + m], ls1 = T[(s0 + 1) * LDT + o + m];
-      cfma_conjb(acc[0][0], lr0, ls0);
-      cfma_conjb(acc[0][1], lr0, ls1);
-      cfma_conjb(acc[1][0], lr1, ls0);
-      cfma_conjb(acc[1][1], lr1, ls1);
-    }
-#pragma unroll
-    for (int u = 0; u < 2; u++)
-#pragma unroll
-      for (int v = 0; v < 2; v++)
-        if (r0 + u >= s0 + v) {
-          double2& x = T[(r0 + u) * LDT + s0 + v];
-          x = csub(x, acc[u][v]);
-        }
-  }
-}
-
-// Warp 0: the diagonal block at o+BS receives block o's update (BS(BS+1)/2 lower entries).
-template <int BS>
-__device__ __forceinline__ void syrkb_diag(double2* T, int o, int lane) {
-  const int b0 = o + BS;
-  for (int e = lane; e < BS * (BS + 1) / 2; e += 32) {
-    int r, c;
-    tri_patch(e, r, c);
-    double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int m = 0; m < BS; m++) cfma_conjb(acc, T[(b0 + r) * LDT + o + m], T[(b0 + c) * LDT + o + m]);
-    double2& x = T[(b0 + r) * LDT + b0 + c];
-    x = csub(x, acc);
-  }
-}
-
-// X[o:o+16, o:o+16] = L[o:o+16, o:o+16]^{-1} (lane j < 16 = column j; zeros above the diagonal).
-__device__ __forceinline__ void inv16(const double2* T, double2* X, int o, int lane, const double* dinv) {
-  if (lane >= 16) return;
-  const int j = lane;
-  double2 b[16];
-#pragma unroll
-  for (int i = 0; i < 16; i++) b[i] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-#pragma unroll
-  for (int i = 0; i < 16; i++) {
-    const double2 x = cscale(b[i], dinv[o + i]);
-    X[(o + i) * LDT + o + j] = x;
-#pragma unroll
-    for (int m = i + 1; m < 16; m++) {
-      const double2 l = T[(o + m) * LDT + o + i];
-      b[m].x -= l.x * x.x - l.y * x.y;
-      b[m].y -= l.x * x.y + l.y * x.x;
-    }
-  }
-}
 
 // 8x8 complex tile on DMMA: C += sum_{k in [k0, k1)} A[r][k] B[k][c] for r, c < 8, with A and
 // B row-major in shared memory (k0, k1 multiples of 4).  Lane l holds C[l/4][2(l%4) + {0,1}].
@@ -255,6 +51,86 @@ __device__ __forceinline__ void tile_put(double2* C, int ldc, int lane, const do
   const int lr = lane >> 2, lk = lane & 3;
   C[lr * ldc + 2 * lk] = make_double2(sg * cr[0], sg * ci[0]);
   C[lr * ldc + 2 * lk + 1] = make_double2(sg * cr[1], sg * ci[1]);
+}
+
+// (a') warp 0, lanes r < 8: row r of the 8x8 block D in registers; step c takes column c
+// from lanes s > c by shuffles (no shared-memory round trip), and lane c+1 forms the next
+// pivot A[c+1][c+1] - |A[c+1][c]|^2 isd^2 before the rank-1 update.  Lanes 8 + j run the
+// forward substitution D x = e_j on the same broadcasts (x_c = b_c isd_c, then
+// b_s -= L[s][c] x_c), so D^{-1} comes out of the same instruction stream and lands in X.
+// (Spreading D over all 32 lanes, two entries per lane, measured slower: 3.5k vs 2.9k
+// cycles per 8x8 factor, tools/diag_probe.cu.)
+__device__ __forceinline__ void factor8(double2* T, double2* X, int o, int lane, double* dinv, int* bad) {
+  const int r = lane & 7;
+  const bool fl = lane < 8, il = lane >= 8 && lane < 16;   // factor lanes, inverse lanes
+  double2 d[8];
+#pragma unroll
+  for (int s = 0; s < 8; s++)
+    d[s] = fl ? (s <= r ? T[(o + r) * LDT + o + s] : make_double2(0.0, 0.0)) : make_double2(s == r ? 1.0 : 0.0, 0.0);
+  double piv = __shfl_sync(0xffffffffu, d[0].x, 0);
+  const int sgn = fl ? (int)0x80000000 : 0;   // factor lanes multiply by conj(L[s][c])
+  const bool upd = !fl;
+#pragma unroll
+  for (int c = 0; c < 8; c++) {
+    if (!(piv > 0.0)) {
+      if (lane == 0 && *bad == 0) *bad = o + c + 1;
+      piv = 1.0;
+    }
+    const double n2 = d[c].x * d[c].x + d[c].y * d[c].y;
+    const double isd = rsqrt(piv);
+    double pn = 0.0;
+    if (c < 7) pn = __shfl_sync(0xffffffffu, d[c < 7 ? c + 1 : 7].x - n2 * (isd * isd), c < 7 ? c + 1 : 7);
+    // No lane-dependent branches around whole steps: the compiler would otherwise unswitch
+    // the loop into a factor copy and an inverse copy that the warp runs one after the other.
+    d[c] = cscale(d[c], isd);
+    if (fl && r == c) d[c] = make_double2(piv * isd, 0.0);
+    if (lane == 0) dinv[o + c] = isd;
+#pragma unroll
+    for (int s = c + 1; s < 8; s++) {
+      // factor lanes: d[s] -= L[r][c] conj(L[s][c]); inverse lanes: b_s -= x_c L[s][c]
+      const double lx = __shfl_sync(0xffffffffu, d[c].x, s);
+      const double ly0 = __shfl_sync(0xffffffffu, d[c].y, s);
+      const double ly = __hiloint2double(__double2hiint(ly0) ^ sgn, __double2loint(ly0));
+      if (upd || r >= s) {
+        d[s].x -= d[c].x * lx - d[c].y * ly;
+        d[s].y -= d[c].x * ly + d[c].y * lx;
+      }
+    }
+    piv = pn;
+  }
+  if (fl) {
+#pragma unroll
+    for (int s = 0; s < 8; s++)
+      if (s <= r) T[(o + r) * LDT + o + s] = d[s];
+  } else if (il) {   // X[o+s][o+j] = x_s (zeros above the diagonal)
+#pragma unroll
+    for (int s = 0; s < 8; s++) X[(o + s) * LDT + o + r] = d[s];
+  }
+}
+
+// (b') rows below block o: L[r][o:o+8] = A[r][o:o+8] D^{-H}, one 8x8 DMMA tile per warp.
+__device__ __forceinline__ void trsm_tile(double2* T, const double2* X, int o, int r0, int lane) {
+  const int lr = lane >> 2, lk = lane & 3;
+  double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < 8; k += 4) {   // sum_m A[r][m] conj(Dinv[c][m])
+    const double2 a = T[(r0 + lr) * LDT + o + k + lk], b = X[(o + lr) * LDT + o + k + lk];
+    dmma_t(cr[0], cr[1], a.x, b.x);
+    dmma_t(cr[0], cr[1], a.y, b.y);
+    dmma_t(ci[0], ci[1], a.y, b.x);
+    dmma_t(ci[0], ci[1], -a.x, b.y);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; h++) T[(r0 + lr) * LDT + o + 2 * lk + h] = make_double2(cr[h], ci[h]);
+}
+
+// Lower-triangle patch index e -> (pi, pj), pi >= pj.
+__device__ __forceinline__ void tri_patch(int e, int& pi, int& pj) {
+  pi = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+  while ((pi + 1) * (pi + 2) / 2 <= e) pi++;
+  while (pi * (pi + 1) / 2 > e) pi--;
+  pj = e - pi * (pi + 1) / 2;
 }
 
 // C[r][c] -= sum_{m < 8} L[r][o+m] conj(L[c][o+m]) for the 8x8 tile at (r0, c0), r >= c only.
@@ -339,51 +215,50 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
   if (t == 0) bad = 0;
   __syncthreads();
   SR_DIAG_PROBE(1);
-  // Block k (BS columns): warp 0 applies block k-1's update to the diagonal block k and
-  // factors it while warps 1-7 apply block k-1's update to the rest of the trailing
-  // triangle (the SYRK is off the critical path); then every warp solves the rows below.
-  constexpr int BS = SR_DIAG_BS;
-  static_assert(BS == 8 || BS == 16, "diagonal sub-block must be 8 or 16");
-  for (int k = 0; k < NB / BS; k++) {
-    const int o = BS * k;
+  // Block k: warp 0 applies block k-1's update to the diagonal block k and factors it
+  // (with D_k^{-1}) while warps 1-3, 5-7 apply block k-1's update to the rest of the
+  // trailing triangle; warp 4 shares warp 0's scheduler and stays idle so the factor, the
+  // critical path, does not compete for its FP64 pipe.  Then the rows below are solved.
+  for (int k = 0; k < NB / 8; k++) {
+    const int o = 8 * k;
     if (warp == 0) {
-      if (k > 0) {
-        if (BS == 8) syrk_diag_mma(T, o - BS, lane);
-        else syrkb_diag<BS>(T, o - BS, lane);
-      }
+      if (k > 0) syrk_diag_mma(T, o - 8, lane);
       __syncwarp();
-      if (BS == 8) factor8(T, o, lane, dinv, &bad);
-      else factorb<BS>(T, o, lane, dinv, &bad);
-    } else if (k > 0) {
-#if SR_DIAG_ISOLATE
-      // warp 4 shares warp 0's scheduler (and FP64 pipe): it stays idle so the factor
-      // steps, the critical path, are not slowed by SYRK instructions on that pipe
-      if (warp != 4) {
-        if (BS == 8) syrk_mma(T, o - BS, warp < 4 ? warp - 1 : warp - 2, 6, lane);
-        else syrkb<BS>(T, o - BS, warp < 4 ? t - 32 : t - 64, 192, true);
-      }
-#else
-      syrkb<BS>(T, o - BS, t - 32, 224, true);
-#endif
+      factor8(T, X, o, lane, dinv, &bad);
+    } else if (k > 0 && warp != 4) {
+      syrk_mma(T, o - 8, warp < 4 ? warp - 1 : warp - 2, 6, lane);
     }
     __syncthreads();
     SR_DIAG_PROBE(17 + 2 * k);
-    if (k < NB / BS - 1) {
-      if (t < 4 * (NB - o - BS)) trsm_quad<BS>(T, o, o + BS + (t >> 2), t & 3, dinv);
+    if (k < NB / 8 - 1) {
+      if (warp < 7 - k) trsm_tile(T, X, o, o + 8 + 8 * warp, lane);
       __syncthreads();
     }
     SR_DIAG_PROBE(18 + 2 * k);
   }
   SR_DIAG_PROBE(2);
   if (t == 0 && bad && info) atomicCAS(info, 0, (int)(B.row_base + (long long)p * NB + bad));
-  if (warp < 4) inv16(T, X, 16 * warp, lane, dinv);
-  __syncthreads();
+  {   // 8 -> 16: X21 = -X22 (L21 X11) inside each 16-block (warps 0-3, one block each)
+    double2* W = dsm + 2 * NB * LDT;
+    if (warp < 4) {
+      const int o = 16 * warp;
+      double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+      tile_mma(T + (o + 8) * LDT + o, LDT, X + o * LDT + o, LDT, 0, 8, lane, cr, ci);
+      tile_put(W + 8 * warp * LDW, LDW, lane, cr, ci, 1.0);
+      __syncwarp();
+      cr[0] = cr[1] = ci[0] = ci[1] = 0.0;
+      tile_mma(X + (o + 8) * LDT + o + 8, LDT, W + 8 * warp * LDW, LDW, 0, 8, lane, cr, ci);
+      tile_put(X + (o + 8) * LDT + o, LDT, lane, cr, ci, -1.0);
+    }
+    __syncthreads();
+  }
   SR_DIAG_PROBE(14);
   // Inverse by recursive doubling on the FP64 tensor cores: X21 = -X22 L21 X11 for the
   // 16-blocks inside each 32-block (both at once), then for the two 32-blocks.  Each warp
   // owns 8x8 output tiles (DMMA 8x8x4, a complex product as 4 real MMAs); X is lower
-  // triangular with explicit zeros above the diagonal inside the 16-blocks (inv16), so a
-  // tile's K range starts at its column (L X) or ends at its row (X W).
+  // triangular with explicit zeros above the diagonal inside the 8-blocks (factor8) and
+  // the 16-blocks (the level above), so a tile's K range starts at its column (L X) or ends
+  // at its row (X W).
   {
     double2* W = dsm + 2 * NB * LDT;   // [32][LDW] scratch product
     {   // 16 -> 32: W' = L21' X11' (rows 32b+16.., cols 32b..), X21' = -X22' W'
