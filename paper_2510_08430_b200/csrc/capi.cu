@@ -149,9 +149,68 @@ sr_status block_solve_impl(int nblk, const int64_t* offs, const double2* S, cons
 struct StepLayout {
   NetDesc net;
   std::vector<int64_t> offs;
-  size_t log_psi, O, e_loc, energy, e_tilde, F, S, scratch, scratch_bytes, total;
+  size_t log_psi, O, e_loc, energy, e_tilde, F, S, scratch, scratch_bytes, total, chol_off;
   size_t h_theta, h_spins, h_bij, h_bj, h_dtheta, h_energy, host_total;
 };
+
+std::vector<int64_t> largest_block(const std::vector<int64_t>& offs) {
+  int64_t mx = 0;
+  for (size_t b = 0; b + 1 < offs.size(); b++) mx = std::max(mx, offs[b + 1] - offs[b]);
+  return {0, mx};
+}
+
+// Pipelined step (int8 engine): the Grams of the blocks run one after another on the step
+// stream, largest first, and block b's Cholesky starts on its side stream as soon as S_b
+// is complete, so the latency-bound panel chains overlap the remaining Grams.
+// SR_PIPE=0 restores Gram-all-then-solve-all.
+bool pipe_step() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SR_PIPE");
+    v = e ? atoi(e) != 0 : 1;
+  }
+  return v != 0;
+}
+
+sr_status pipelined_qgt_solve(int nblk, const int64_t* offs, long long ns, const double2* A, long long lda,
+                              double2* S, const double2* F, double lam, double2* dtheta, char* scr,
+                              size_t scr_bytes, size_t chol_off, cudaStream_t st) {
+  static cudaEvent_t ready[kMaxBlocks];
+  static bool made = false;
+  if (!made) {
+    for (int b = 0; b < kMaxBlocks; b++) SR_CUDA(cudaEventCreateWithFlags(&ready[b], cudaEventDisableTiming));
+    made = true;
+  }
+  std::vector<long long> sizes(nblk), soff(nblk);
+  std::vector<int> order(nblk);
+  long long so = 0;
+  for (int b = 0; b < nblk; b++) {
+    sizes[b] = offs[b + 1] - offs[b];
+    soff[b] = so;
+    so += sizes[b] * sizes[b];
+    order[b] = b;
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return sizes[x] > sizes[y]; });
+  Arena a(scr + chol_off, scr_bytes - chol_off);
+  CholSet cs{};
+  cs.info = nullptr;
+  carve_chol(a, cs, sizes.data(), nblk);
+  if (!a.ok()) {
+    set_error("sr_step: workspace too small");
+    return SR_ERR_WORKSPACE;
+  }
+  for (int b = 0; b < nblk; b++) {
+    cs.b[b].S = S + soff[b];
+    cs.b[b].F = F + offs[b];
+    cs.b[b].out = dtheta + offs[b];
+  }
+  for (int b : order) {
+    const int64_t o1[2] = {0, sizes[b]};
+    SR_TRY(oz::block_qgt_i8(ns, 1, o1, A + offs[b], lda, S + soff[b], scr, chol_off, st));
+    SR_CUDA(cudaEventRecord(ready[b], st));
+  }
+  return chol_solve(cs, lam, false, -1.0, st, ready);
+}
 
 sr_status step_layout(int n_layers, const int32_t* widths, long long ns, long long nb, StepLayout* L) {
   SR_TRY(make_net(n_layers, widths, &L->net));
@@ -179,6 +238,10 @@ sr_status step_layout(int n_layers, const int32_t* widths, long long ns, long lo
   scr = std::max(scr, center_force_ws(ns, net.n_p));
   scr = std::max(scr, block_solve_ws(n_layers, L->offs.data()));
   scr = std::max(scr, oz::workspace_bytes(ns, n_layers, L->offs.data()));
+  // pipelined int8 step: the digit slices of one block and the Cholesky workspace of all
+  // blocks are live at once
+  L->chol_off = round256(oz::workspace_bytes(ns, 1, largest_block(L->offs).data()));
+  scr = std::max(scr, L->chol_off + block_solve_ws(n_layers, L->offs.data()));
   L->scratch_bytes = round256(scr);
   L->scratch = take(L->scratch_bytes);
   L->total = off;
@@ -206,6 +269,10 @@ sr_status step_impl(const StepLayout& L, const double* theta, const int8_t* spin
   SR_TRY(jacobian_impl(net, theta, spins, ns, log_psi, O, net.n_p, scr, L.scratch_bytes, st));
   SR_TRY(local_energy_impl(net, theta, nb, bij, bj, spins, ns, log_psi, e_loc, scr, L.scratch_bytes, st));
   SR_TRY(center_force_impl(ns, net.n_p, O, net.n_p, nullptr, e_loc, energy, e_tilde, F, scr, L.scratch_bytes, st));
+  if (g_gram_engine == SR_GRAM_INT8 && pipe_step())
+    return pipelined_qgt_solve(net.L, L.offs.data(), ns, reinterpret_cast<const double2*>(O), net.n_p, S,
+                               reinterpret_cast<const double2*>(F), lam, reinterpret_cast<double2*>(dtheta),
+                               reinterpret_cast<char*>(scr), L.scratch_bytes, L.chol_off, st);
   if (g_gram_engine == SR_GRAM_INT8)
     SR_TRY(oz::block_qgt_i8(ns, net.L, L.offs.data(), reinterpret_cast<const double2*>(O), net.n_p, S, scr,
                             L.scratch_bytes, st));

@@ -35,8 +35,8 @@ using cholk::chol_diag;
 using cholk::kDiagSmem;
 constexpr int kStrip = SR_KSTRIP;   // panels per strip (deferred trailing update with K = 64 kStrip)
 
-__global__ void chol_init(CholSet cs, double lam, int inplace) {
-  const int b = blockIdx.y;
+__global__ void chol_init(CholSet cs, double lam, int inplace, int b0) {
+  const int b = b0 + blockIdx.y;
   const CholBlock& B = cs.b[b];
   const long long n = B.n, np = B.npad;
   const long long total = np * np;
@@ -391,13 +391,21 @@ sr_status side_pool(SidePool*& out) {
 
 }  // namespace
 
-sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStream_t st) {
+sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStream_t st,
+                     const cudaEvent_t* ready) {
+  if (ready && cs.info) {   // the reset on st would race with blocks already released by ready[b]
+    set_error("chol_solve: info must be null with ready events");
+    return SR_ERR_INVALID;
+  }
   if (cs.info) SR_CUDA(cudaMemsetAsync(cs.info, 0, sizeof(int), st));
-  {
+  auto init_grid = [](const CholBlock& B, int nb) {
+    return dim3((unsigned)std::min<long long>((B.npad * B.npad + 255) / 256, 2 * kNumSMs), (unsigned)nb);
+  };
+  if (!ready) {
     long long mx = 0;
     for (int b = 0; b < cs.count; b++) mx = std::max(mx, cs.b[b].npad * cs.b[b].npad);
     dim3 g((unsigned)std::min<long long>((mx + 255) / 256, 2 * kNumSMs), (unsigned)cs.count);
-    chol_init<<<g, 256, 0, st>>>(cs, lam, inplace ? 1 : 0);
+    chol_init<<<g, 256, 0, st>>>(cs, lam, inplace ? 1 : 0, 0);
     SR_LAUNCHED();
   }
   static bool diag_attr = false;
@@ -409,7 +417,7 @@ sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStr
   SidePool* pool;
   SR_TRY(side_pool(pool));
   SR_CUDA(cudaEventRecord(pool->fork, st));
-  if (cs.count == 1) {
+  if (cs.count == 1 && !ready) {
     SR_CUDA(cudaStreamWaitEvent(pool->q[0].s2, pool->fork, 0));
     SR_CUDA(cudaStreamWaitEvent(pool->q[0].s3, pool->fork, 0));
     SR_TRY(solve_block(cs, 0, st, pool->q[0]));
@@ -418,9 +426,16 @@ sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStr
     for (int b = 0; b < cs.count; b++) {
       const int i = b % kSideStreams;
       cudaStream_t sb = pool->s[i];
-      SR_CUDA(cudaStreamWaitEvent(sb, pool->fork, 0));
-      SR_CUDA(cudaStreamWaitEvent(pool->q[i].s2, pool->fork, 0));
-      SR_CUDA(cudaStreamWaitEvent(pool->q[i].s3, pool->fork, 0));
+      // pipelined: block b's S (and everything queued on st before it) is complete once
+      // ready[b] fires; otherwise everything queued on st before this call
+      const cudaEvent_t go = ready ? ready[b] : pool->fork;
+      SR_CUDA(cudaStreamWaitEvent(sb, go, 0));
+      SR_CUDA(cudaStreamWaitEvent(pool->q[i].s2, go, 0));
+      SR_CUDA(cudaStreamWaitEvent(pool->q[i].s3, go, 0));
+      if (ready) {
+        chol_init<<<init_grid(cs.b[b], 1), 256, 0, sb>>>(cs, lam, inplace ? 1 : 0, b);
+        SR_LAUNCHED();
+      }
       SR_TRY(solve_block(cs, b, sb, pool->q[i]));
     }
     for (int i = 0; i < std::min(cs.count, kSideStreams); i++) {

@@ -31,7 +31,10 @@ struct CholSet {
 void carve_chol(Arena& a, CholSet& cs, const long long* sizes, int nblk);
 // Solves (M_b + lam I) x_b = F_b for all blocks; writes out_b = sign * x_b.  With
 // inplace, M_b is already in Fm (ld npad, rows/cols < n) and only the diagonal shift
-// and the identity padding are applied.
-sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStream_t st);
+// and the identity padding are applied.  With ready (one event per block), block b's
+// copy-in and factorisation wait for ready[b] instead of running after everything queued
+// on st before the call (the step overlaps block b's solve with later blocks' Grams).
+sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStream_t st,
+                     const cudaEvent_t* ready = nullptr);
 
 }  // namespace sr

@@ -1,5 +1,6 @@
 // mlp.cu — stage (1) sr_jacobian and stage (2) sr_local_energy.
 //
+// The dense layers of both stages run on the FP64 tensor cores (dense_rows, net.cuh).
 // Stage 1 (§2 Eq. 2, O_i(x) = d_theta_i log psi(x)):
 //   jac_forward   rows = samples; z_l = W_l h_l + b_l, stores h_{l+1} = lncosh(z_l) and
 //                 tanh(z_l) per layer to [N_s][w] scratch, ln psi = sum_j h_L[j]
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(kThreads) jac_forward(NetDesc net, const doubl
                                                         double2* __restrict__ hs, double2* __restrict__ ts,
                                                         double2* __restrict__ log_psi) {
   extern __shared__ double2 smem[];
-  const int ld = net.wmax + 1;
+  const int ld = act_ld(net.wmax);
   double2* cur = smem;
   double2* nxt = smem + RB * ld;
   const long long row0 = (long long)blockIdx.x * RB;
@@ -120,7 +121,7 @@ template <int RB>
 __global__ void __launch_bounds__(kThreads) jac_backward(NetDesc net, const double2* __restrict__ theta,
                                                          double2* __restrict__ ts, long long ns) {
   extern __shared__ double2 smem[];
-  const int ld = net.wmax + 1;
+  const int ld = act_ld(net.wmax);
   double2* cur = smem;
   double2* nxt = smem + RB * ld;
   const long long row0 = (long long)blockIdx.x * RB;
@@ -284,14 +285,14 @@ __global__ void __launch_bounds__(kThreads) energy_eval(NetDesc net, const doubl
                                                         double2* __restrict__ contrib) {
   extern __shared__ double2 smem[];
   __shared__ longlong2 tile_sb[RB];
-  const int ld = net.wmax + 1;
+  const int ld = act_ld(net.wmax);
   const long long R = off[ns];
   const int n0 = net.w[0], w1 = net.w[1];
   const double2* wt0 = wt + net.toff[0];
   for (long long row0 = (long long)blockIdx.x * RB; row0 < R; row0 += (long long)gridDim.x * RB) {
     double2* cur = smem;
     double2* nxt = smem + RB * ld;
-    if (threadIdx.x < RB) {
+      if (threadIdx.x < RB) {
       const long long r = row0 + threadIdx.x;
       tile_sb[threadIdx.x] = r < R ? row_sb[r] : make_longlong2(-1, 0);
     }
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(kThreads) energy_eval(NetDesc net, const doubl
     __syncthreads();
     for (int l = 1; l < net.L; l++) {
       auto epi = [&](int r, int j, double2 z) { nxt[r * ld + j] = lncosh(z); };
-      dense_rows<RB, decltype(epi), 8>(wt + net.toff[l], theta + net.boff[l], net.w[l], net.w[l + 1], cur, ld, epi);
+      dense_rows<RB>(wt + net.toff[l], theta + net.boff[l], net.w[l], net.w[l + 1], cur, ld, epi);
       __syncthreads();
       double2* tmp = cur;
       cur = nxt;
@@ -353,8 +354,11 @@ __global__ void energy_reduce(const double* __restrict__ diag, const long long* 
   }
 }
 
-int rows_per_tile(const NetDesc& net) { return net.wmax <= 160 ? 32 : 16; }
-size_t tile_smem(const NetDesc& net, int rb) { return (size_t)2 * rb * (net.wmax + 1) * sizeof(double2); }
+size_t tile_smem(const NetDesc& net, int rb);
+int rows_per_tile(const NetDesc& net) { return tile_smem(net, 32) <= 200 * 1024 ? 32 : 16; }
+size_t tile_smem(const NetDesc& net, int rb) {
+  return (size_t)2 * rb * act_ld(net.wmax) * sizeof(double2);
+}
 
 template <typename K>
 sr_status set_smem(K kernel, size_t bytes) {
@@ -395,6 +399,17 @@ EnWs carve_en(Arena& a, const NetDesc& net, long long ns, long long nb) {
 
 }  // namespace
 
+// Row tile of the Jacobian kernels: the largest of 32/16/8 rows (shared memory permitting)
+// that still gives jac_min_ctas() CTAs; SR_JAC_MIN_CTAS overrides for tuning.
+long long jac_min_ctas() {
+  static long long v = -1;
+  if (v < 0) {
+    const char* e = getenv("SR_JAC_MIN_CTAS");
+    v = e ? atoll(e) : kNumSMs;
+  }
+  return v;
+}
+
 template <int RB>
 sr_status launch_jac(const NetDesc& net, const double2* theta, const JacWs& w, const int8_t* spins, long long ns,
                      double* log_psi, unsigned grid, size_t sm, cudaStream_t st) {
@@ -423,10 +438,10 @@ sr_status jacobian_impl(const NetDesc& net, const double* theta_d, const int8_t*
   const double2* theta = reinterpret_cast<const double2*>(theta_d);
   transpose_weights<<<64, kThreads, 0, st>>>(net, theta, w.wt);
   SR_LAUNCHED();
-  // Row tile: the largest of 32/16/8 rows (shared-memory bound by the widths) that still
-  // gives two waves of CTAs over the 148 SMs (configs[1]: 4096 rows -> 8 rows, 512 CTAs).
+  // configs[1]: 4096 rows -> 16-row tiles, 256 CTAs (measured: 0.279 ms vs 0.285 with 8 rows
+  // and 0.336 with 32)
   int rb = rows_per_tile(net);
-  while (rb > 8 && (ns + rb - 1) / rb < 2 * kNumSMs) rb /= 2;
+  while (rb > 8 && (ns + rb - 1) / rb < jac_min_ctas()) rb /= 2;
   const size_t sm = tile_smem(net, rb);
   const unsigned grid = (unsigned)((ns + rb - 1) / rb);
   if (rb == 32) {
@@ -482,19 +497,27 @@ sr_status local_energy_impl(const NetDesc& net, const double* theta_d, long long
   if (const char* e = getenv("SR_ENERGY_RB")) rb = atoi(e) == 32 ? 32 : atoi(e) == 8 ? 8 : 16;
   const size_t sm = tile_smem(net, rb);
   const long long max_tiles = (ns * nb + rb - 1) / rb;
-  const unsigned grid =
-      (unsigned)std::max<long long>(1, std::min<long long>(max_tiles, (rb == 32 ? 4LL : 8LL) * kNumSMs));
   const double2* lp = reinterpret_cast<const double2*>(log_psi);
+  // persistent: as many CTAs as fit on the SMs at once
+  auto grid_of = [&](auto kernel) -> unsigned {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, sm) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    return (unsigned)std::max<long long>(1, std::min<long long>(max_tiles, (long long)per_sm * kNumSMs));
+  };
   if (rb == 32) {
     SR_TRY(set_smem(energy_eval<32>, sm));
+    const unsigned grid = grid_of(energy_eval<32>);
     energy_eval<32><<<grid, kThreads, sm, st>>>(net, theta, w.wt, spins, bij, bond_j, w.z0, lp, w.off, ns, w.rows,
                                                 w.contrib);
   } else if (rb == 16) {
     SR_TRY(set_smem(energy_eval<16>, sm));
+    const unsigned grid = grid_of(energy_eval<16>);
     energy_eval<16><<<grid, kThreads, sm, st>>>(net, theta, w.wt, spins, bij, bond_j, w.z0, lp, w.off, ns, w.rows,
                                                 w.contrib);
   } else {
     SR_TRY(set_smem(energy_eval<8>, sm));
+    const unsigned grid = grid_of(energy_eval<8>);
     energy_eval<8><<<grid, kThreads, sm, st>>>(net, theta, w.wt, spins, bij, bond_j, w.z0, lp, w.off, ns, w.rows,
                                                w.contrib);
   }

@@ -647,6 +647,18 @@ size_t workspace_bytes(long long ns, int nblk, const int64_t* offs) {
   return round256(mb) + round256((size_t)mc * 8) + round256((size_t)mc * 4);
 }
 
+// Grid of the block-QGT launch: one persistent CTA per SM by default; SR_GRAM_CTAS=n sets
+// n CTAs (more than the SMs makes the kernel non-persistent, so that concurrent work on
+// other streams -- the pipelined step's block solves -- gets SMs as CTAs retire).
+long long gram_ctas() {
+  static long long v = -1;
+  if (v < 0) {
+    const char* e = getenv("SR_GRAM_CTAS");
+    v = e && atoll(e) > 0 ? atoll(e) : kNumSMs;
+  }
+  return v;
+}
+
 sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double2* A, long long lda, double2* S,
                        void* ws, size_t ws_bytes, cudaStream_t st) {
   if (ws_bytes < workspace_bytes(ns, nblk, offs) || !ws) {
@@ -709,7 +721,7 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
     CUtensorMap ma, mb2;
     SR_TRY(make_map(ma, E, Kp, nc, BM));
     SR_TRY(make_map(mb2, E, Kp, nc, BN));
-    const unsigned grid = (unsigned)std::min<long long>(tiles, kNumSMs);
+    const unsigned grid = (unsigned)std::min<long long>(tiles, gram_ctas());
     timer_begin("gram_i8", st);
     gram_i8<MODE_HERM><<<grid, kThreads, kSmem, st>>>(ma, mb2, P);
     timer_end(st);
