@@ -1,6 +1,6 @@
 // mlp.cu — stage (1) sr_jacobian and stage (2) sr_local_energy.
 //
-// The dense layers of both stages run on the FP64 tensor cores (dense_rows, net.cuh).
+// The dense layers of both stages run on the FP64 tensor cores (dense_z, net.cuh).
 // Stage 1 (§2 Eq. 2, O_i(x) = d_theta_i log psi(x)):
 //   jac_forward   rows = samples; z_l = W_l h_l + b_l, stores h_{l+1} = lncosh(z_l) and
 //                 tanh(z_l) per layer to [N_s][w] scratch, ln psi = sum_j h_L[j]
@@ -83,17 +83,20 @@ __global__ void __launch_bounds__(kThreads) jac_forward(NetDesc net, const doubl
     const int fout = net.w[l + 1];
     double2* hl = hs + net.aoff[l] * ns;
     double2* tl = ts + net.aoff[l] * ns;
-    dense_rows<RB>(wt + net.toff[l], theta + net.boff[l], net.w[l], fout, cur, ld,
-                   [&](int r, int j, double2 z) {
-                     double2 h, th;
-                     lncosh_tanh(z, h, th);
-                     nxt[r * ld + j] = h;
-                     const long long k = row0 + r;
-                     if (k < ns) {
-                       hl[k * fout + j] = h;
-                       tl[k * fout + j] = th;
-                     }
-                   });
+    dense_z<RB>(wt + net.toff[l], net.w[l], fout, cur, ld, nxt, ld);
+    __syncthreads();
+    const double2* bl = theta + net.boff[l];
+    for (int e = threadIdx.x; e < RB * fout; e += kThreads) {
+      const int r = e / fout, j = e - r * fout;
+      double2 h, th;
+      lncosh_tanh(cadd(bl[j], nxt[r * ld + j]), h, th);
+      nxt[r * ld + j] = h;
+      const long long k = row0 + r;
+      if (k < ns) {
+        hl[k * fout + j] = h;
+        tl[k * fout + j] = th;
+      }
+    }
     __syncthreads();
     double2* tmp = cur;
     cur = nxt;
@@ -138,16 +141,18 @@ __global__ void __launch_bounds__(kThreads) jac_backward(NetDesc net, const doub
   for (int l = net.L - 1; l >= 1; l--) {
     const int nout = net.w[l];
     double2* tprev = ts + net.aoff[l - 1] * ns;
-    dense_rows<RB>(theta + net.woff[l], nullptr, net.w[l + 1], nout, cur, ld,
-                   [&](int r, int i, double2 g) {
-                     const long long k = row0 + r;
-                     double2 d = make_double2(0.0, 0.0);
-                     if (k < ns) {
-                       d = cmul(tprev[k * nout + i], g);
-                       tprev[k * nout + i] = d;
-                     }
-                     nxt[r * ld + i] = d;
-                   });
+    dense_z<RB>(theta + net.woff[l], net.w[l + 1], nout, cur, ld, nxt, ld);
+    __syncthreads();
+    for (int e = threadIdx.x; e < RB * nout; e += kThreads) {
+      const int r = e / nout, i = e - r * nout;
+      const long long k = row0 + r;
+      double2 d = make_double2(0.0, 0.0);
+      if (k < ns) {
+        d = cmul(tprev[k * nout + i], nxt[r * ld + i]);
+        tprev[k * nout + i] = d;
+      }
+      nxt[r * ld + i] = d;
+    }
     __syncthreads();
     double2* tmp = cur;
     cur = nxt;
@@ -271,6 +276,13 @@ __global__ void energy_rows(const int8_t* __restrict__ spins, long long ns, int 
   }
 }
 
+#ifndef SR_ENERGY_MG
+#define SR_ENERGY_MG 1
+#endif
+// row tiles per weight fragment in energy_eval (dense_z); measured 1 / 2 / 4: configs[1]
+// 0.721 / 0.751 / 0.747 ms, configs[2] 35.4 / 33.2 / 33.2 ms
+constexpr int kEnergyMG = SR_ENERGY_MG;
+
 // Persistent over tiles of RB connected rows: ln psi(x') then 2 J exp(ln psi(x') - ln psi(x)).
 template <int RB>
 __global__ void __launch_bounds__(kThreads) energy_eval(NetDesc net, const double2* __restrict__ theta,
@@ -317,8 +329,14 @@ __global__ void __launch_bounds__(kThreads) energy_eval(NetDesc net, const doubl
     }
     __syncthreads();
     for (int l = 1; l < net.L; l++) {
-      auto epi = [&](int r, int j, double2 z) { nxt[r * ld + j] = lncosh(z); };
-      dense_rows<RB>(wt + net.toff[l], theta + net.boff[l], net.w[l], net.w[l + 1], cur, ld, epi);
+      const int fout = net.w[l + 1];
+      dense_z<RB, (RB / 8 < kEnergyMG ? RB / 8 : kEnergyMG)>(wt + net.toff[l], net.w[l], fout, cur, ld, nxt, ld);
+      __syncthreads();
+      const double2* bl = theta + net.boff[l];
+      for (int e = threadIdx.x; e < RB * fout; e += kThreads) {
+        const int r = e / fout, j = e - r * fout;
+        nxt[r * ld + j] = lncosh(cadd(bl[j], nxt[r * ld + j]));
+      }
       __syncthreads();
       double2* tmp = cur;
       cur = nxt;
@@ -354,8 +372,6 @@ __global__ void energy_reduce(const double* __restrict__ diag, const long long* 
   }
 }
 
-size_t tile_smem(const NetDesc& net, int rb);
-int rows_per_tile(const NetDesc& net) { return tile_smem(net, 32) <= 200 * 1024 ? 32 : 16; }
 size_t tile_smem(const NetDesc& net, int rb) {
   return (size_t)2 * rb * act_ld(net.wmax) * sizeof(double2);
 }
@@ -399,17 +415,6 @@ EnWs carve_en(Arena& a, const NetDesc& net, long long ns, long long nb) {
 
 }  // namespace
 
-// Row tile of the Jacobian kernels: the largest of 32/16/8 rows (shared memory permitting)
-// that still gives jac_min_ctas() CTAs; SR_JAC_MIN_CTAS overrides for tuning.
-long long jac_min_ctas() {
-  static long long v = -1;
-  if (v < 0) {
-    const char* e = getenv("SR_JAC_MIN_CTAS");
-    v = e ? atoll(e) : kNumSMs;
-  }
-  return v;
-}
-
 template <int RB>
 sr_status launch_jac(const NetDesc& net, const double2* theta, const JacWs& w, const int8_t* spins, long long ns,
                      double* log_psi, unsigned grid, size_t sm, cudaStream_t st) {
@@ -438,19 +443,10 @@ sr_status jacobian_impl(const NetDesc& net, const double* theta_d, const int8_t*
   const double2* theta = reinterpret_cast<const double2*>(theta_d);
   transpose_weights<<<64, kThreads, 0, st>>>(net, theta, w.wt);
   SR_LAUNCHED();
-  // configs[1]: 4096 rows -> 16-row tiles, 256 CTAs (measured: 0.279 ms vs 0.285 with 8 rows
-  // and 0.336 with 32)
-  int rb = rows_per_tile(net);
-  while (rb > 8 && (ns + rb - 1) / rb < jac_min_ctas()) rb /= 2;
-  const size_t sm = tile_smem(net, rb);
-  const unsigned grid = (unsigned)((ns + rb - 1) / rb);
-  if (rb == 32) {
-    SR_TRY(launch_jac<32>(net, theta, w, spins, ns, log_psi, grid, sm, st));
-  } else if (rb == 16) {
-    SR_TRY(launch_jac<16>(net, theta, w, spins, ns, log_psi, grid, sm, st));
-  } else {
-    SR_TRY(launch_jac<8>(net, theta, w, spins, ns, log_psi, grid, sm, st));
-  }
+  // 8-row tiles (measured best with the DMMA dense layers: configs[1] 0.259 ms vs 0.279 / 0.336
+  // with 16 / 32 rows; configs[2] 3.70 ms vs 5.35 with 32 rows)
+  constexpr int rb = 8;
+  SR_TRY(launch_jac<rb>(net, theta, w, spins, ns, log_psi, (unsigned)((ns + rb - 1) / rb), tile_smem(net, rb), st));
   dim3 og((unsigned)ns, (unsigned)net.L);
   jac_outer<<<og, kThreads, 0, st>>>(net, spins, w.hs, w.ts, ns, reinterpret_cast<double2*>(O), ldo);
   SR_LAUNCHED();

@@ -36,57 +36,59 @@ __device__ __forceinline__ void net_dmma(double& c0, double& c1, double a, doubl
       : "d"(a), "d"(b));
 }
 
-// z[r][j] = bias[j] + sum_i hin[r][i] M[i][j] for the rows r < RB held in shared memory
-// (ld ldin = act_ld(.)), M row-major [n_in][n_out] complex in global memory (L2/L1
-// resident), on the FP64 tensor cores: each complex 8x8x4 product is four real
-// mma.sync.m8n8k4.f64 (SASS DMMA) into three accumulators (Re*Re, Im*Im, cross terms), so
-// Re z = rr - ii.  Warp g owns the 8-column n-tiles g, g+8, ... and all RB/8 row tiles of
-// each; the B fragment (M[k0 + lane%4][n0 + lane/4]) is loaded once per k step and used
-// for every row tile.  Ragged n_in / n_out are zero-padded in the fragments.
-// epi(r, j, z) is called for every r < RB, j < n_out.
-template <int RB, typename Epi>
-__device__ __forceinline__ void dense_rows(const double2* __restrict__ M, const double2* __restrict__ bias,
-                                           int n_in, int n_out, const double2* hin, int ldin, Epi epi) {
-  static_assert(RB % 8 == 0, "RB must be a multiple of 8");
-  constexpr int MT = RB / 8;
+// z[r][j] = sum_i hin[r][i] M[i][j] for the rows r < RB held in shared memory (ld ldin =
+// act_ld(.)), written to zout[r][j] (shared memory, ld ldz), M row-major [n_in][n_out]
+// complex in global memory (L2/L1 resident), on the FP64 tensor cores: each complex 8x8x4
+// product is four real mma.sync.m8n8k4.f64 (SASS DMMA) into four independent accumulators,
+// z = (rr - ii) + i (ri + ir).  Work units (MG 8-row tiles, one 8-column tile)
+// go round robin over the warps; the B fragment M[k0 + lane%4][n0 + lane/4] is loaded once
+// per k step for the MG row tiles of a unit (MG > 1 cuts the L2 weight traffic when the
+// weights do not stay in L1), and units of one column tile sit on consecutive warps.  Ragged n_in / n_out are
+// zero-padded in the fragments.  No barrier inside: the caller synchronises before
+// reading zout (and the elementwise activation runs as a separate, balanced pass).
+template <int RB, int MG = 1>
+__device__ __forceinline__ void dense_z(const double2* __restrict__ M, int n_in, int n_out, const double2* hin,
+                                        int ldin, double2* zout, int ldz) {
+  static_assert(RB % (8 * MG) == 0, "RB must be a multiple of 8 MG");
+  constexpr int MU = RB / (8 * MG);          // row-tile groups; a unit is MG row tiles x 8 columns
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int gr = lane >> 2, gc = lane & 3;   // fragment row / column-in-group
-  const int nt_count = (n_out + 7) >> 3;
+  const int units = MU * ((n_out + 7) >> 3);
   const int k_full = n_in & ~3;
-  for (int nt = warp; nt < nt_count; nt += nwarps) {
+  for (int u = warp; u < units; u += nwarps) {
+    const int mu = u % MU, nt = u / MU;
     const int n = nt * 8 + gr;                 // B-fragment column of this lane
     const bool n_ok = n < n_out;
-    double rr[MT][2], ii[MT][2], ri[MT][2];
+    double rr[MG][2], ii[MG][2], ri[MG][2], ir[MG][2];
 #pragma unroll
-    for (int m = 0; m < MT; m++) rr[m][0] = rr[m][1] = ii[m][0] = ii[m][1] = ri[m][0] = ri[m][1] = 0.0;
+    for (int g = 0; g < MG; g++)
+      rr[g][0] = rr[g][1] = ii[g][0] = ii[g][1] = ri[g][0] = ri[g][1] = ir[g][0] = ir[g][1] = 0.0;
     const double2* mcol = M + (n_ok ? n : 0);
-    const double2* arow = hin + gr * ldin + gc;
+    const double2* arow = hin + (mu * MG * 8 + gr) * ldin + gc;
     auto kstep = [&](int k0, bool tail) {
       const int k = k0 + gc;
       const bool k_ok = !tail || k < n_in;
       const double2 b = (n_ok && k_ok) ? __ldg(mcol + (long long)k * n_out) : make_double2(0.0, 0.0);
 #pragma unroll
-      for (int m = 0; m < MT; m++) {
-        const double2 a = k_ok ? arow[m * 8 * ldin + k0] : make_double2(0.0, 0.0);
-        net_dmma(rr[m][0], rr[m][1], a.x, b.x);
-        net_dmma(ii[m][0], ii[m][1], a.y, b.y);
-        net_dmma(ri[m][0], ri[m][1], a.x, b.y);
-        net_dmma(ri[m][0], ri[m][1], a.y, b.x);
+      for (int g = 0; g < MG; g++) {   // the B fragment serves MG row tiles
+        const double2 a = k_ok ? arow[g * 8 * ldin + k0] : make_double2(0.0, 0.0);
+        net_dmma(rr[g][0], rr[g][1], a.x, b.x);
+        net_dmma(ii[g][0], ii[g][1], a.y, b.y);
+        net_dmma(ri[g][0], ri[g][1], a.x, b.y);
+        net_dmma(ir[g][0], ir[g][1], a.y, b.x);
       }
     };
-#pragma unroll 4
+#pragma unroll 8
     for (int k0 = 0; k0 < k_full; k0 += 4) kstep(k0, false);
     if (k_full < n_in) kstep(k_full, true);
 #pragma unroll
-    for (int e = 0; e < 2; e++) {
-      const int j = nt * 8 + 2 * gc + e;
-      if (j < n_out) {
-        const double2 b0 = bias ? bias[j] : make_double2(0.0, 0.0);
+    for (int g = 0; g < MG; g++)
 #pragma unroll
-        for (int m = 0; m < MT; m++)
-          epi(m * 8 + gr, j, make_double2(b0.x + (rr[m][e] - ii[m][e]), b0.y + ri[m][e]));
+      for (int e = 0; e < 2; e++) {
+        const int j = nt * 8 + 2 * gc + e;
+        if (j < n_out)
+          zout[((mu * MG + g) * 8 + gr) * ldz + j] = make_double2(rr[g][e] - ii[g][e], ri[g][e] + ir[g][e]);
       }
-    }
   }
 }
 
