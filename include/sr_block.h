@@ -85,6 +85,21 @@ SR_API void sr_reset_launch_count(void);
  * (their count in *launches, may be NULL), then forgets them. */
 SR_API void sr_kernel_timer(int enable);
 SR_API double sr_kernel_time_ms(const char* kernel, int64_t* launches);
+/* sr_kernel_timeline — every pending timer record (all names) as text lines
+ * "name stream_index begin_ms end_ms\n", times relative to the first record's begin event,
+ * stream_index numbering the distinct launching streams in order of first use.  With buf
+ * non-NULL and bytes > 0, writes at most bytes-1 characters plus a NUL and consumes the
+ * records; with buf NULL only queries.  Returns the size needed including the NUL.  Host-side diagnostics only. */
+SR_API size_t sr_kernel_timeline(char* buf, size_t bytes);
+/* sr_trace_buffer — device-side trace of the Cholesky / int8-engine kernels (diagnostics;
+ * works inside CUDA-graph replays, where events between launches are unavailable).
+ * records: device buffer of `capacity` 40-byte records, zeroed by the caller, or NULL to
+ * turn tracing off.  Record 0's first uint64 counts appended records; each record i >= 1 is
+ * {uint64 gridid, uint64 t_begin_ns, uint64 t_end_ns (globaltimer), int32 kind, int32 tag,
+ * int32 sm, int32 0}, one per CTA, written by its thread 0 (kinds: paper_2510_08430_b200/
+ * _lib.py TRACE_KINDS).  Appends beyond capacity are dropped.  Process-wide; the buffer
+ * must outlive every launch made while it is installed. */
+SR_API sr_status sr_trace_buffer(void* records, int64_t capacity);
 
 /* ---------------------------------------------------------------- stage (1) ---
  * sr_jacobian — PAPER.md §2 Eq. 2 "O_i(x) = d_{theta_i} log psi_theta(x)".
@@ -247,7 +262,11 @@ SR_API sr_status sr_step(int n_layers, const int32_t* widths /*host*/, const dou
  * bond_j_h in; dtheta_h, energy_h out).  Copies in, runs the step, copies out, and
  * synchronises `stream` before returning.  Host buffers should be pinned for
  * asynchronous copies.  Device workspace as for sr_step plus
- * sr_step_host_extra_bytes() for the staged inputs/outputs. */
+ * sr_step_host_extra_bytes() for the staged inputs/outputs.  The device part of the step
+ * is captured into a CUDA graph on the first call for a given (workspace, widths,
+ * n_samples, n_bonds, lambda, Gram engine) and replayed on later calls (up to 4 cached;
+ * environment SR_STEP_GRAPH=0 disables it); the workspace must not be freed while its
+ * graph is cached unless the same address is never passed again. */
 SR_API size_t sr_step_host_extra_bytes(int n_layers, const int32_t* widths /*host*/,
                                        int64_t n_samples, int64_t n_bonds);
 SR_API sr_status sr_step_host(int n_layers, const int32_t* widths /*host*/,

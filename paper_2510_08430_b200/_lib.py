@@ -31,6 +31,8 @@ SIGNATURES = {
     "sr_reset_launch_count": (None, []),
     "sr_kernel_timer": (None, [_i32]),
     "sr_kernel_time_ms": (_dbl, [C.c_char_p, _I64P]),
+    "sr_kernel_timeline": (C.c_size_t, [C.c_char_p, C.c_size_t]),
+    "sr_trace_buffer": (_i32, [C.c_void_p, _i64]),
     "sr_jacobian_workspace_bytes": (_sz, [_i32, _I32P, _i64]),
     "sr_jacobian": (_i32, [_i32, _I32P, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _sz, _vp]),
     "sr_local_energy_workspace_bytes": (_sz, [_i32, _I32P, _i64, _i64]),
@@ -320,6 +322,43 @@ def sr_reset_launch_count():
 
 def sr_kernel_timer(enable):
     load().sr_kernel_timer(1 if enable else 0)
+
+
+TRACE_KINDS = {1: "diag", 2: "trsm", 3: "skinny_sub", 4: "gram", 5: "trail", 6: "rhs", 7: "back", 8: "back_rest",
+               9: "split_rows", 10: "init", 11: "split", 12: "colmax", 13: "output"}
+
+
+def sr_trace_buffer(records):
+    """Install (a zeroed uint8 CUDA tensor of 40-byte records) or remove (None) the device trace."""
+    if records is None:
+        _check(load().sr_trace_buffer(None, 0), "sr_trace_buffer")
+    else:
+        _check(load().sr_trace_buffer(_ptr(records), records.numel() // 40), "sr_trace_buffer")
+
+
+def sr_trace_records(records):
+    """Decode a trace buffer: list of (gridid, kind name, tag, sm, t0_ns, t1_ns)."""
+    import numpy as np
+    raw = records.cpu().numpy().view(np.uint8)
+    n = int(raw[:8].view(np.uint64)[0])
+    dt = np.dtype([("grid", "<u8"), ("t0", "<u8"), ("t1", "<u8"), ("kind", "<i4"), ("tag", "<i4"), ("sm", "<i4"),
+                   ("pad", "<i4")])
+    rec = raw[40:40 * (1 + min(n, raw.size // 40 - 1))].view(dt)
+    return [(int(r["grid"]), TRACE_KINDS.get(int(r["kind"]), str(r["kind"])), int(r["tag"]), int(r["sm"]),
+             int(r["t0"]), int(r["t1"])) for r in rec]
+
+
+def sr_kernel_timeline():
+    """Pending kernel-timer records as (name, stream_index, begin_ms, end_ms) tuples."""
+    lib = load()
+    n = lib.sr_kernel_timeline(None, 0)
+    buf = C.create_string_buffer(n)
+    lib.sr_kernel_timeline(buf, n)
+    out = []
+    for line in buf.value.decode().splitlines():
+        name, sid, a, b = line.split()
+        out.append((name, int(sid), float(a), float(b)))
+    return out
 
 
 def sr_kernel_time_ms(kernel):

@@ -2,6 +2,8 @@
 // Argument checking, workspace carving and stage sequencing only; every arithmetic step
 // of the path runs in the kernels of mlp.cu, center.cu, gram.cuh and chol.cu.
 #include <algorithm>
+#include <cstdio>
+#include <cstring>
 #include <vector>
 
 #include "chol.cuh"
@@ -21,6 +23,7 @@ int gram_engine() { return g_gram_engine; }
 struct TimedLaunch {
   std::string name;
   cudaEvent_t a, b;
+  cudaStream_t st;
 };
 bool g_timer = false;
 std::vector<TimedLaunch> g_timed;
@@ -43,7 +46,7 @@ void timer_begin(const char* kernel, cudaStream_t st) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cs);
   if (cs != cudaStreamCaptureStatusNone) return;
-  TimedLaunch t{kernel, timer_event(), timer_event()};
+  TimedLaunch t{kernel, timer_event(), timer_event(), st};
   cudaEventRecord(t.a, st);
   g_timed.push_back(t);
   g_timer_open = true;
@@ -283,6 +286,69 @@ sr_status step_impl(const StepLayout& L, const double* theta, const int8_t* spin
   return SR_OK;
 }
 
+// CUDA-graph cache of sr_step_host: the ~900 launches of a step are captured once per
+// (workspace, shapes, lambda, engine) and replayed, so the host-buffer path pays one graph
+// launch instead of the per-kernel launch overhead.  The step reads its inputs from fixed
+// places in the workspace (sr_step_host copies them there first), so a replay is exact.
+// SR_STEP_GRAPH=0 turns it off.
+struct StepGraphKey {
+  const void* ws;
+  std::vector<int32_t> widths;
+  long long ns, nb;
+  double lam;
+  int engine;
+  bool operator==(const StepGraphKey& o) const {
+    return ws == o.ws && widths == o.widths && ns == o.ns && nb == o.nb && lam == o.lam && engine == o.engine;
+  }
+};
+struct StepGraph {
+  StepGraphKey key;
+  cudaGraphExec_t exec;
+};
+std::vector<StepGraph> g_step_graphs;
+bool step_graph_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SR_STEP_GRAPH");
+    v = e ? atoi(e) != 0 : 1;
+  }
+  return v != 0;
+}
+
+sr_status step_graphed(const StepLayout& L, const StepGraphKey& key, const double* theta, const int8_t* spins,
+                       long long ns, long long nb, const int32_t* bij, const double* bj, double lam, double* dtheta,
+                       double* energy, char* ws, cudaStream_t st) {
+  if (!step_graph_enabled())
+    return step_impl(L, theta, spins, ns, nb, bij, bj, lam, dtheta, energy, ws, st);
+  for (StepGraph& g : g_step_graphs)
+    if (g.key == key) {
+      SR_CUDA(cudaGraphLaunch(g.exec, st));
+      return SR_OK;
+    }
+  static cudaStream_t cap = nullptr;
+  if (!cap) SR_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  SR_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+  const sr_status r = step_impl(L, theta, spins, ns, nb, bij, bj, lam, dtheta, energy, ws, cap);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(cap, &graph);
+  cudaGraphExec_t exec = nullptr;
+  if (r != SR_OK || ec != cudaSuccess || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    if (r != SR_OK) return r;
+    set_error(std::string("sr_step_host: graph capture failed: ") + cudaGetErrorString(ec));
+    return SR_ERR_CUDA;
+  }
+  cudaGraphDestroy(graph);
+  if (g_step_graphs.size() >= 4) {
+    cudaGraphExecDestroy(g_step_graphs.front().exec);
+    g_step_graphs.erase(g_step_graphs.begin());
+  }
+  g_step_graphs.push_back({key, exec});
+  SR_CUDA(cudaGraphLaunch(exec, st));
+  return SR_OK;
+}
+
 }  // namespace
 }  // namespace sr
 
@@ -410,6 +476,42 @@ SR_API sr_status sr_block_qgt_i8(int64_t n_samples, int n_blocks, const int64_t*
 }
 
 SR_API void sr_kernel_timer(int enable) { g_timer = enable != 0; }
+
+SR_API sr_status sr_trace_buffer(void* records, int64_t capacity) {
+  SR_CHECK_ARG(records == nullptr || capacity >= 2, "capacity must be >= 2 records");
+  TraceDev t{static_cast<TraceRec*>(records), records ? capacity : 0};
+  SR_CUDA(trace_install_chol(t));
+  SR_CUDA(trace_install_ozaki(t));
+  return SR_OK;
+}
+
+SR_API size_t sr_kernel_timeline(char* buf, size_t bytes) {
+  std::string out;
+  std::vector<cudaStream_t> streams;
+  cudaEvent_t origin = g_timed.empty() ? nullptr : g_timed.front().a;
+  for (TimedLaunch& t : g_timed) {
+    cudaEventSynchronize(t.b);
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, origin, t.a);
+    cudaEventElapsedTime(&b, origin, t.b);
+    size_t sid = std::find(streams.begin(), streams.end(), t.st) - streams.begin();
+    if (sid == streams.size()) streams.push_back(t.st);
+    char line[160];
+    snprintf(line, sizeof line, "%s %zu %.4f %.4f\n", t.name.c_str(), sid, a, b);
+    out += line;
+  }
+  if (buf && bytes) {   // records are consumed only when they are returned
+    for (TimedLaunch& t : g_timed) {
+      g_event_pool.push_back(t.a);
+      g_event_pool.push_back(t.b);
+    }
+    g_timed.clear();
+    const size_t n = std::min(bytes - 1, out.size());
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return out.size() + 1;
+}
 
 SR_API double sr_kernel_time_ms(const char* kernel, int64_t* launches) {
   double ms = 0.0;
@@ -604,7 +706,9 @@ SR_API sr_status sr_step_host(int n_layers, const int32_t* widths, const double*
     SR_CUDA(cudaMemcpyAsync(bij, bonds_ij_h, (size_t)n_bonds * 2 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     SR_CUDA(cudaMemcpyAsync(bj, bond_j_h, (size_t)n_bonds * sizeof(double), cudaMemcpyHostToDevice, st));
   }
-  SR_TRY(step_impl(L, theta, spins, n_samples, n_bonds, bij, bj, lambda, dtheta, energy, ws, st));
+  StepGraphKey key{workspace, std::vector<int32_t>(widths, widths + n_layers + 1), n_samples, n_bonds, lambda,
+                   g_gram_engine};
+  SR_TRY(step_graphed(L, key, theta, spins, n_samples, n_bonds, bij, bj, lambda, dtheta, energy, ws, st));
   SR_CUDA(cudaMemcpyAsync(dtheta_h, dtheta, np * c16, cudaMemcpyDeviceToHost, st));
   if (energy_h) SR_CUDA(cudaMemcpyAsync(energy_h, energy, c16, cudaMemcpyDeviceToHost, st));
   SR_CUDA(cudaStreamSynchronize(st));

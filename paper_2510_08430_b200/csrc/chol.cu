@@ -36,6 +36,7 @@ using cholk::kDiagSmem;
 constexpr int kStrip = SR_KSTRIP;   // panels per strip (deferred trailing update with K = 64 kStrip)
 
 __global__ void chol_init(CholSet cs, double lam, int inplace, int b0) {
+  TraceScope trace_(TR_INIT, b0);
   const int b = b0 + blockIdx.y;
   const CholBlock& B = cs.b[b];
   const long long n = B.n, np = B.npad;
@@ -63,6 +64,7 @@ __global__ void chol_init(CholSet cs, double lam, int inplace, int b0) {
 // b_i -= sum_{c in [c0, c1)} L[i][c] y[c] for rows i >= c1 (the strip's panels applied to the
 // right-hand side of every later row at once; one warp per row).
 __global__ void chol_rhs_update(const CholBlock B, long long c0, long long c1) {
+  TraceScope trace_(TR_RHS, (int)(B.row_base / 64) * 4096 + (int)(c0 / 64));
   const long long np = B.npad;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (long long r = c1 + (long long)blockIdx.x * 8 + warp; r < np; r += (long long)gridDim.x * 8) {
@@ -97,6 +99,7 @@ static_assert(kStrip <= 8, "the back-substitution cluster holds one CTA per stri
 constexpr size_t kBackSmem = (size_t)2 * NB * NB * sizeof(double2);   // 128 KB
 
 __global__ void __cluster_dims__(kStrip, 1, 1) __launch_bounds__(256) chol_back_strip(const CholBlock B, int p0, int pend) {
+  TraceScope trace_(TR_BACK, (int)(B.row_base / 64) * 4096 + p0);
   extern __shared__ __align__(16) double2 bsm[];   // [2][64][64] streamed blocks
   __shared__ double2 xb[2][NB];
   __shared__ double2 ys[NB];
@@ -164,6 +167,7 @@ __global__ void __cluster_dims__(kStrip, 1, 1) __launch_bounds__(256) chol_back_
 // One CTA per 32 columns: warp w sums rows w, w + 8, ... of the strip (8 loads in flight
 // per thread: the column GEMV is latency-bound with fewer), then a fixed-order reduction.
 __global__ void __launch_bounds__(256) chol_back_rest(const CholBlock B, int p0, int pend) {
+  TraceScope trace_(TR_BACK_REST, (int)(B.row_base / 64) * 4096 + p0);
   __shared__ double2 xs[kStrip * NB];
   __shared__ double2 red[8][33];
   const long long np = B.npad;
@@ -195,6 +199,7 @@ __global__ void __launch_bounds__(256) chol_back_rest(const CholBlock B, int p0,
 }
 
 __global__ void chol_output(CholSet cs, double sign) {
+  TraceScope trace_(TR_OUTPUT, 0);
   const CholBlock& B = cs.b[blockIdx.y];
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < B.n;
        r += (long long)gridDim.x * blockDim.x)
@@ -237,6 +242,30 @@ int trail_ctas(int nblocks) {
   return 0;   // measured: capping the grid slows the 3-block solve (trailing throughput bound)
 }
 
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+// Off-chain in-strip updates (s2 / s3 jobs) on 64x64-tile CTAs (the FP64 engine's
+// tile_kernel, weights of B amortised over 64 rows) instead of the 16-row skinny kernel;
+// SR_INNER_TILES=0/1.
+bool inner_tiles() {
+  static const int v = env_int("SR_INNER_TILES", 0);
+  return v != 0;
+}
+
+// Trailing-update lookahead (see solve_block); SR_LOOKAHEAD=0 turns it off, SR_TRAIL_B_TPC
+// sets the tiles per CTA of the off-chain part.
+bool lookahead() {
+  static const int v = env_int("SR_LOOKAHEAD", 0);   // measured 35.3 vs 34.6 ms at configs[1] (the GPU is full during the solve)
+  return v != 0;
+}
+int trail_b_tpc() {
+  static const int v = std::max(1, env_int("SR_TRAIL_B_TPC", 2));
+  return v;
+}
+
 // Programmatic dependent launch along the panel chain (diag -> TRSM -> next tile -> diag);
 // SR_PDL=0 turns it off (A/B measurements).
 bool pdl_chain() {
@@ -251,15 +280,29 @@ bool pdl_chain() {
 // Factorisation + substitutions of ONE block on one stream (two-level blocking, see header).
 // Side streams of the block: Q.s2 / Q.s3 with events Q.ea / Q.eb / Q.ec.  Within a strip the
 // panel chain on `st` runs diag(p) -> TRSM(p) -> the update of the next DIAGONAL tile
-// (p+1, p+1) by panel p -> diag(p+1): that tile is all diag(p+1) reads.  The rest of column
-// p+1 (rows below the tile) takes panel p's update on s3 meanwhile, joined before TRSM(p+1);
-// the strip's later columns take it on s2, joined before the next update that writes the
-// same column.
+// (p+1, p+1) by panel p -> diag(p+1): that tile is all diag(p+1) reads.  Panel p's other
+// in-strip updates run off the chain: on s3 the rest of column p+1 and all of column p+2
+// (joined into st before TRSM(p+1)), on s2 the columns >= p+3.  Ordering of the writers of
+// one column: s3's job(p) waits for the last s2 job (which wrote columns >= p+2), and the
+// chain reaches every column through s3 (ec before each TRSM), so the chain itself never
+// waits on s2 -- s2's job(p-1) has two panel steps to finish before s3's job(p+1) needs it.
 struct BlockStreams {
-  cudaStream_t s2, s3;
-  cudaEvent_t ea, eb, ec;
+  cudaStream_t s2, s3, s4;
+  cudaEvent_t ea, eb, ec, es, et;
 };
-sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q) {
+// Stagger of equal-size blocks (SR_STAGGER=k, k >= 1): block b starts once the previous
+// block of the same size has factored k panels, so their strip-end trailing updates (full-
+// GPU kernels on the chain) alternate instead of coinciding.  0 = off.
+int stagger_panels() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SR_STAGGER");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q, cudaEvent_t stagger_rec = nullptr) {
   const CholBlock& B = cs.b[b];
   // Two-level blocking: strips of kStrip panels.  Inside a strip each panel p is factored
   // (chol_diag), its column solved (TRSM), the RHS updated, and only the strip's own later
@@ -267,6 +310,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
   // per strip with K = 64 * kStrip, which is where the flops are (4x the arithmetic
   // intensity of a per-panel update, 4x fewer passes over the trailing matrix).
   const bool i8 = gram_engine() == SR_GRAM_INT8;
+  bool pending_b = false;   // a lookahead (b) update on s4 not yet joined into st
   for (int p0 = 0; p0 < B.P; p0 += kStrip) {
     const int pend = std::min(p0 + kStrip, B.P);
     for (int p = p0; p < pend; p++) {
@@ -275,6 +319,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
       else chol_diag<<<1, 256, kDiagSmem, st>>>(B, cs.info, p, p0);
       timer_end(st);
       SR_LAUNCHED();
+      if (stagger_rec && p + 1 == stagger_panels()) SR_CUDA(cudaEventRecord(stagger_rec, st));
       // the previous panel's update of this column below the diagonal tile (s3) must be
       // complete before TRSM(p) (and joined into st in any case)
       if (p > p0) SR_CUDA(cudaStreamWaitEvent(st, Q.ec, 0));
@@ -292,29 +337,36 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
           if (rows > NB)
             gram::add_prob(next_rows, lrows + (long long)NB * B.npad, B.npad, lrows, B.npad,
                            cblk + (long long)NB * B.npad, B.npad, rows - NB, NB, NB, false);
+        } else if (jj == p + 2) {   // two-column lookahead on s3 (see the ordering note above)
+          gram::add_prob(next_rows, lrows, B.npad, lrows, B.npad, cblk, B.npad, rows, NB, NB, false);
         } else {
           gram::add_prob(inner_rest, lrows, B.npad, lrows, B.npad, cblk, B.npad, rows, NB, NB, false);
         }
       }
       timer_begin("chol_trsm", st);
-      SR_TRY((gram::launch_skinny<gram::STORE>(trsm, st, pdl_chain())));
+      static const bool pdl_trsm = env_int("SR_PDL_TRSM", 1) != 0;
+      SR_TRY((gram::launch_skinny<gram::STORE>(trsm, st, pdl_chain() && pdl_trsm)));
       timer_end(st);
       const bool side = next_tile.count > 0;
       if (side) SR_CUDA(cudaEventRecord(Q.ea, st));           // L column p ready for s2 / s3
-      // the next-column updates write column p+1, which panel p-1's rest update (s2) also writes
-      if (p > p0 && p + 1 < pend) SR_CUDA(cudaStreamWaitEvent(st, Q.eb, 0));
       timer_begin("chol_inner", st);
       if (side) SR_TRY((gram::launch_skinny<gram::SUB>(next_tile, st, pdl_chain())));
       timer_end(st);
-      if (side) {
+      if (side && next_rows.count) {
         SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.ea, 0));
         if (p > p0) SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.eb, 0));
-        SR_TRY((gram::launch_skinny<gram::SUB>(next_rows, Q.s3)));
+        timer_begin("chol_next_rows", Q.s3);
+        if (inner_tiles()) SR_TRY((gram::launch<gram::NH, gram::SUB>(next_rows, Q.s3)));
+        else SR_TRY((gram::launch_skinny<gram::SUB>(next_rows, Q.s3)));
+        timer_end(Q.s3);
         SR_CUDA(cudaEventRecord(Q.ec, Q.s3));
       }
       if (inner_rest.count) {
         SR_CUDA(cudaStreamWaitEvent(Q.s2, Q.ea, 0));
-        SR_TRY((gram::launch_skinny<gram::SUB>(inner_rest, Q.s2)));
+        timer_begin("chol_inner_rest", Q.s2);
+        if (inner_tiles()) SR_TRY((gram::launch<gram::NH, gram::SUB>(inner_rest, Q.s2)));
+        else SR_TRY((gram::launch_skinny<gram::SUB>(inner_rest, Q.s2)));
+        timer_end(Q.s2);
         SR_CUDA(cudaEventRecord(Q.eb, Q.s2));
       }
     }
@@ -329,7 +381,25 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
     if (m > 0) {   // deferred trailing update of the strip, K = 64 * (pend - p0)
       const double2* lp = B.Fm + (long long)pend * NB * B.npad + (long long)p0 * NB;
       double2* trailing = B.Fm + (long long)pend * NB * B.npad + (long long)pend * NB;
-      if (i8) {   // int8 digit-slice tcgen05 engine (ozaki.cu), lower triangle
+      const long long K = (long long)(pend - p0) * NB;
+      const long long look = (long long)kStrip * NB;   // the next strip's columns
+      if (i8 && lookahead() && m > look) {
+        // Lookahead: the chain needs only the next strip's columns (a), so the rest of the
+        // trailing matrix (b) is updated on s4 (lowest priority, non-persistent grid) while
+        // the next strip factors.  (b) reads the digit slices and writes columns beyond the
+        // next strip, so the next strip-end split waits for it (et), which also keeps one
+        // addend per element per launch in a fixed order (deterministic).
+        if (pending_b) SR_CUDA(cudaStreamWaitEvent(st, Q.et, 0));
+        SR_TRY(oz::trail_split_i8(lp, B.npad, m, K, B.tws, B.tws_bytes, st));
+        SR_CUDA(cudaEventRecord(Q.es, st));
+        SR_TRY(oz::trail_apply_i8(m, K, trailing, B.npad, B.tws, 0, kStrip, trail_ctas(cs.count), st));
+        SR_CUDA(cudaStreamWaitEvent(Q.s4, Q.es, 0));
+        SR_TRY(oz::trail_apply_i8(m, K, trailing, B.npad, B.tws, look, 0, -trail_b_tpc(), Q.s4));
+        SR_CUDA(cudaEventRecord(Q.et, Q.s4));
+        pending_b = true;
+      } else if (i8) {   // int8 digit-slice tcgen05 engine (ozaki.cu), lower triangle
+        if (pending_b) SR_CUDA(cudaStreamWaitEvent(st, Q.et, 0));
+        pending_b = false;
         SR_TRY(oz::trail_update_i8(lp, B.npad, m, (long long)(pend - p0) * NB, trailing, B.npad, B.tws, B.tws_bytes,
                                    trail_ctas(cs.count), st));
       } else {
@@ -342,6 +412,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
       }
     }
   }
+  if (pending_b) SR_CUDA(cudaStreamWaitEvent(st, Q.et, 0));
   for (int p0 = (B.P - 1) / kStrip * kStrip; p0 >= 0; p0 -= kStrip) {
     const int pend = std::min(p0 + kStrip, B.P);
     timer_begin("chol_back", st);
@@ -364,7 +435,7 @@ constexpr int kSideStreams = 8;
 struct SidePool {
   cudaStream_t s[kSideStreams];
   BlockStreams q[kSideStreams];
-  cudaEvent_t fork, join[kSideStreams];
+  cudaEvent_t fork, join[kSideStreams], stag[kSideStreams];
   bool ok = false;
 };
 sr_status side_pool(SidePool*& out) {
@@ -374,10 +445,17 @@ sr_status side_pool(SidePool*& out) {
     SR_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     for (int i = 0; i < kSideStreams; i++) {
       BlockStreams& q = pool.q[i];
+      // the panel chain (s) ahead of the block's off-chain in-strip updates (s3, then s2):
+      // when an SM frees up, the chain's next kernel is placed first
+      const int side_prio = env_int("SR_SIDE_PRIO", 1);
       SR_CUDA(cudaStreamCreateWithPriority(&pool.s[i], cudaStreamNonBlocking, hi));
-      SR_CUDA(cudaStreamCreateWithPriority(&q.s2, cudaStreamNonBlocking, hi));
-      SR_CUDA(cudaStreamCreateWithPriority(&q.s3, cudaStreamNonBlocking, hi));
+      SR_CUDA(cudaStreamCreateWithPriority(&q.s2, cudaStreamNonBlocking, side_prio ? std::min(lo, hi + 2) : hi));
+      SR_CUDA(cudaStreamCreateWithPriority(&q.s3, cudaStreamNonBlocking, side_prio ? std::min(lo, hi + 1) : hi));
+      SR_CUDA(cudaStreamCreateWithPriority(&q.s4, cudaStreamNonBlocking, lo));
+      SR_CUDA(cudaEventCreateWithFlags(&q.es, cudaEventDisableTiming));
+      SR_CUDA(cudaEventCreateWithFlags(&q.et, cudaEventDisableTiming));
       SR_CUDA(cudaEventCreateWithFlags(&pool.join[i], cudaEventDisableTiming));
+      SR_CUDA(cudaEventCreateWithFlags(&pool.stag[i], cudaEventDisableTiming));
       SR_CUDA(cudaEventCreateWithFlags(&q.ea, cudaEventDisableTiming));
       SR_CUDA(cudaEventCreateWithFlags(&q.eb, cudaEventDisableTiming));
       SR_CUDA(cudaEventCreateWithFlags(&q.ec, cudaEventDisableTiming));
@@ -420,9 +498,11 @@ sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStr
   if (cs.count == 1 && !ready) {
     SR_CUDA(cudaStreamWaitEvent(pool->q[0].s2, pool->fork, 0));
     SR_CUDA(cudaStreamWaitEvent(pool->q[0].s3, pool->fork, 0));
+    SR_CUDA(cudaStreamWaitEvent(pool->q[0].s4, pool->fork, 0));
     SR_TRY(solve_block(cs, 0, st, pool->q[0]));
   } else {
     // independent blocks on side streams, forked from and joined back into `st`
+    bool prev_stagger = false;
     for (int b = 0; b < cs.count; b++) {
       const int i = b % kSideStreams;
       cudaStream_t sb = pool->s[i];
@@ -432,11 +512,17 @@ sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStr
       SR_CUDA(cudaStreamWaitEvent(sb, go, 0));
       SR_CUDA(cudaStreamWaitEvent(pool->q[i].s2, go, 0));
       SR_CUDA(cudaStreamWaitEvent(pool->q[i].s3, go, 0));
+      SR_CUDA(cudaStreamWaitEvent(pool->q[i].s4, go, 0));
       if (ready) {
         chol_init<<<init_grid(cs.b[b], 1), 256, 0, sb>>>(cs, lam, inplace ? 1 : 0, b);
         SR_LAUNCHED();
       }
-      SR_TRY(solve_block(cs, b, sb, pool->q[i]));
+      // stagger: wait for the previous equal-size block's first panels (see stagger_panels)
+      const bool stag = stagger_panels() > 0 && b + 1 < cs.count && cs.b[b + 1].npad == cs.b[b].npad &&
+                        cs.b[b].P > stagger_panels();
+      if (b > 0 && prev_stagger) SR_CUDA(cudaStreamWaitEvent(sb, pool->stag[(b - 1) % kSideStreams], 0));
+      SR_TRY(solve_block(cs, b, sb, pool->q[i], stag ? pool->stag[b % kSideStreams] : nullptr));
+      prev_stagger = stag;
     }
     for (int i = 0; i < std::min(cs.count, kSideStreams); i++) {
       SR_CUDA(cudaEventRecord(pool->join[i], pool->s[i]));
@@ -453,5 +539,7 @@ sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStr
   }
   return SR_OK;
 }
+
+cudaError_t trace_install_chol(TraceDev t) { return trace_install_local(t); }
 
 }  // namespace sr

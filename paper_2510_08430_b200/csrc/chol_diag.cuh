@@ -172,6 +172,7 @@ __device__ __forceinline__ void syrk_mma(double2* T, int o, int wi, int nw, int 
 __device__ __forceinline__ void syrk_diag_mma(double2* T, int o, int lane) { syrk_tile(T, o, o + 8, o + 8, lane); }
 
 __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, int p, int p0) {
+  TraceScope trace_(TR_DIAG, (int)(B.row_base / 64) * 4096 + p);
   extern __shared__ double2 dsm[];
   double2* T = dsm;              // [64][LDT]: A (lower) -> L
   double2* X = dsm + NB * LDT;   // [64][LDT]: Linv (lower)

@@ -81,6 +81,64 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// ----------------------------------------------------------------------------
+// Device trace (sr_trace_buffer; diagnostics): when a buffer is installed, thread 0 of
+// every CTA of a traced kernel appends {gridid, kind, tag, globaltimer at entry, at exit,
+// SM id} to it, so the host can rebuild the timeline of a CUDA-graph replay (launch
+// order, overlap, critical path) without events between the launches.  The pointer lives
+// in each translation unit's own __device__ copy (no relocatable device code), installed
+// by trace_install_<unit>() from capi.cu.
+// ----------------------------------------------------------------------------
+struct TraceRec {
+  unsigned long long grid, t0, t1;
+  int kind, tag, sm, pad;
+};
+struct TraceDev {
+  TraceRec* rec;              // rec[0].grid is the append counter; records from rec[1]
+  long long cap;              // capacity in records (including rec[0])
+};
+static __device__ TraceDev g_trace_dev;
+__device__ __forceinline__ unsigned long long trace_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct TraceScope {
+  unsigned long long t0;
+  int kind, tag;
+  __device__ __forceinline__ TraceScope(int k, int g) : t0(0), kind(k), tag(g) {
+    if (g_trace_dev.rec && threadIdx.x == 0) t0 = trace_clock();
+  }
+  __device__ __forceinline__ ~TraceScope() {
+    TraceDev d = g_trace_dev;
+    if (d.rec && threadIdx.x == 0) {
+      const unsigned long long i = atomicAdd(&d.rec[0].grid, 1ULL) + 1;
+      if ((long long)i < d.cap) {
+        unsigned long long gid;
+        unsigned int smid;
+        asm volatile("mov.u64 %0, %%gridid;" : "=l"(gid));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        TraceRec r;
+        r.grid = gid;
+        r.t0 = t0;
+        r.t1 = trace_clock();
+        r.kind = kind;
+        r.tag = tag;
+        r.sm = (int)smid;
+        r.pad = 0;
+        d.rec[i] = r;
+      }
+    }
+  }
+};
+static inline cudaError_t trace_install_local(TraceDev t) { return cudaMemcpyToSymbol(g_trace_dev, &t, sizeof t); }
+cudaError_t trace_install_chol(TraceDev t);
+cudaError_t trace_install_ozaki(TraceDev t);
+enum TraceKind {
+  TR_DIAG = 1, TR_TRSM = 2, TR_SKINNY_SUB = 3, TR_GRAM = 4, TR_TRAIL = 5, TR_RHS = 6, TR_BACK = 7,
+  TR_BACK_REST = 8, TR_SPLIT_ROWS = 9, TR_INIT = 10, TR_SPLIT = 11, TR_COLMAX = 12, TR_OUTPUT = 13
+};
+
 #define SR_TRY(call)                 \
   do {                               \
     sr_status s_ = (call);           \

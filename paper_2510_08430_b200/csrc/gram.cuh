@@ -305,6 +305,7 @@ constexpr size_t kSkinnySmem = (size_t)(SK_TM + 64) * SK_LD * sizeof(double2);  
 
 template <int EP>
 __global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_constant__ ProbSet ps) {
+  TraceScope trace_(EP == STORE ? TR_TRSM : TR_SKINNY_SUB, (int)ps.p[0].M);
   extern __shared__ __align__(16) double2 smem[];
   double2* sa = smem;
   double2* sb = smem + SK_TM * SK_LD;

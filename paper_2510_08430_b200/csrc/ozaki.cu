@@ -67,6 +67,7 @@ struct Blk {
   long long ldc;
   long long tile_begin;  // first global tile index (tiles come in Re/Im pairs)
   int n, RT, CT;
+  int jlim;              // > 0: only column tiles J < jlim (a lower trapezoid, row-major); 0: all
 };
 // Epilogues: MODE_HERM writes S = G with its conjugate mirror (stage 4); MODE_SUB applies
 // C -= G to the lower triangle i >= j (Cholesky trailing update, chol.cu).
@@ -167,6 +168,20 @@ __device__ __forceinline__ void decode(const Params& P, long long t, int& b, int
   pass = (int)(u & 1);
   u >>= 1;
   const int RT = P.b[b].RT, CT = P.b[b].CT;
+  if (P.b[b].jlim > 0) {   // trapezoid: row I holds min(CT, 2I + 2, jlim) tiles
+    const int jl = min(CT, P.b[b].jlim);
+    for (int i = 0; i < RT; i++) {
+      const int c = min(jl, 2 * i + 2);
+      if (u < c) {
+        I = i;
+        J = (int)u;
+        return;
+      }
+      u -= c;
+    }
+    I = J = 0;
+    return;
+  }
   for (int I0 = 0; I0 < RT; I0 += kBand) {
     const int I1 = min(RT, I0 + kBand), h = I1 - I0;
     long long cnt = 0;
@@ -199,6 +214,7 @@ __device__ __forceinline__ void decode(const Params& P, long long t, int& b, int
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     gram_i8(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b, const Params P) {
+  TraceScope trace_(MODE == MODE_HERM ? TR_GRAM : TR_TRAIL, P.b[0].n);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -411,6 +427,7 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 constexpr unsigned long long kInfBits = 0x7FF0000000000000ULL;
 __global__ void oz_colmax(const double2* __restrict__ A, long long lda, long long c0, int n, long long K,
                           int rows_per, unsigned long long* __restrict__ mx) {
+  TraceScope trace_(TR_COLMAX, 0);
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const long long k0 = (long long)blockIdx.y * rows_per, k1 = min(K, k0 + rows_per);
@@ -472,6 +489,7 @@ constexpr size_t kSplitSmem = (size_t)3 * kSlices * 32 * kSplitRow;
 __global__ void __launch_bounds__(256) oz_split(const double2* __restrict__ A, long long lda, long long c0, int n,
                                                 long long K, long long Kp, const unsigned long long* __restrict__ mx,
                                                 int8_t* __restrict__ E, int* __restrict__ expo) {
+  TraceScope trace_(TR_SPLIT, 0);
   extern __shared__ uint8_t ssm[];
   const int t = threadIdx.x, jl = t & 31, kg = t >> 5;
   const int j = blockIdx.x * 32 + jl;
@@ -519,6 +537,7 @@ __global__ void __launch_bounds__(256) oz_split(const double2* __restrict__ A, l
 // One warp per row: row maximum by shuffles, then 8 consecutive k per lane per pass.
 __global__ void __launch_bounds__(256) oz_split_rows(const double2* __restrict__ L, long long ldl, int m, int K,
                                                      int Kp, int8_t* __restrict__ E, int* __restrict__ expo) {
+  TraceScope trace_(TR_SPLIT_ROWS, 0);
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (i >= m) return;
@@ -606,10 +625,11 @@ sr_status set_attrs() {
   return SR_OK;
 }
 
-long long lower_tiles(int n) {
+long long lower_tiles(int n, int jlim = 0) {
   const int RT = (n + BM - 1) / BM, CT = (n + BN - 1) / BN;
+  const int jl = jlim > 0 ? std::min(CT, jlim) : CT;
   long long cnt = 0;
-  for (int i = 0; i < RT; i++) cnt += std::min(CT, 2 * i + 2);
+  for (int i = 0; i < RT; i++) cnt += std::min(jl, 2 * i + 2);
   return cnt;
 }
 
@@ -735,8 +755,8 @@ size_t trail_workspace_bytes(long long m, long long K) {
   return round256((size_t)kSlices * 3 * Kp * m) + round256((size_t)m * 4);
 }
 
-sr_status trail_update_i8(const double2* L, long long ldl, long long m, long long K, double2* C, long long ldc,
-                          void* ws, size_t ws_bytes, int max_ctas, cudaStream_t st) {
+sr_status trail_split_i8(const double2* L, long long ldl, long long m, long long K, void* ws, size_t ws_bytes,
+                         cudaStream_t st) {
   if (m <= 0 || K <= 0) return SR_OK;
   const long long Kp = pad_k(K);
   if (2 * Kp > kChunkK || m >= (1LL << 31) / kSlices) {
@@ -747,12 +767,22 @@ sr_status trail_update_i8(const double2* L, long long ldl, long long m, long lon
     set_error("trail_update_i8: workspace too small");
     return SR_ERR_WORKSPACE;
   }
-  SR_TRY(set_attrs());
   Arena a(ws, ws_bytes);
   int8_t* E = a.take<int8_t>((size_t)kSlices * 3 * Kp * m);
   int* expo = a.take<int>(m);
   oz_split_rows<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(L, ldl, (int)m, (int)K, (int)Kp, E, expo);
   SR_LAUNCHED();
+  return SR_OK;
+}
+
+sr_status trail_apply_i8(long long m, long long K, double2* C, long long ldc, void* ws, long long r0, int jlim,
+                         long long ctas, cudaStream_t st) {
+  if (m <= r0 || K <= 0) return SR_OK;
+  SR_TRY(set_attrs());
+  const long long Kp = pad_k(K);
+  Arena a(ws, trail_workspace_bytes(m, K));
+  int8_t* E = a.take<int8_t>((size_t)kSlices * 3 * Kp * m);
+  int* expo = a.take<int>(m);
   Params P{};
   P.nblk = 1;
   P.Kp = Kp;
@@ -760,18 +790,20 @@ sr_status trail_update_i8(const double2* L, long long ldl, long long m, long lon
   P.spc = kChunkK / BKB;
   P.expo = expo;
   Blk& B = P.b[0];
-  B.col0 = 0;
-  B.C = C;
+  B.col0 = r0;
+  B.C = C + r0 * ldc + r0;
   B.ldc = ldc;
-  B.n = (int)m;
+  B.n = (int)(m - r0);
   B.RT = (B.n + BM - 1) / BM;
   B.CT = (B.n + BN - 1) / BN;
+  B.jlim = jlim;
   B.tile_begin = 0;
-  P.total_tiles = 2 * lower_tiles(B.n);
+  P.total_tiles = 2 * lower_tiles(B.n, jlim);
   CUtensorMap ma, mb;
   SR_TRY(make_map(ma, E, Kp, m, BM));
   SR_TRY(make_map(mb, E, Kp, m, BN));
-  const unsigned grid = (unsigned)std::min<long long>(P.total_tiles, max_ctas > 0 ? max_ctas : kNumSMs);
+  const long long want = ctas > 0 ? ctas : ctas < 0 ? (P.total_tiles + (-ctas) - 1) / (-ctas) : kNumSMs;
+  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(P.total_tiles, want));
   timer_begin("trail_i8", st);
   gram_i8<MODE_SUB><<<grid, kThreads, kSmem, st>>>(ma, mb, P);
   timer_end(st);
@@ -779,5 +811,13 @@ sr_status trail_update_i8(const double2* L, long long ldl, long long m, long lon
   return SR_OK;
 }
 
+sr_status trail_update_i8(const double2* L, long long ldl, long long m, long long K, double2* C, long long ldc,
+                          void* ws, size_t ws_bytes, int max_ctas, cudaStream_t st) {
+  if (m <= 0 || K <= 0) return SR_OK;
+  SR_TRY(trail_split_i8(L, ldl, m, K, ws, ws_bytes, st));
+  return trail_apply_i8(m, K, C, ldc, ws, 0, 0, max_ctas, st);
+}
+
 }  // namespace oz
+cudaError_t trace_install_ozaki(TraceDev t) { return trace_install_local(t); }
 }  // namespace sr

@@ -23,6 +23,16 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
 size_t trail_workspace_bytes(long long m, long long K);
 sr_status trail_update_i8(const double2* L, long long ldl, long long m, long long K, double2* C, long long ldc,
                           void* ws, size_t ws_bytes, int max_ctas, cudaStream_t st);
+// The same update in parts (lookahead): trail_split_i8 scales and splits the rows of L
+// into the workspace once; trail_apply_i8 then applies C -= L L^H to the lower triangle of
+// the trailing square [r0, m) x [r0, m), with jlim > 0 only to its first 64 jlim columns
+// (a lower trapezoid).  ctas sets the grid: 0 = one CTA per SM (persistent), n > 0 = n
+// CTAs, n < 0 = one CTA per -n tiles (non-persistent: CTAs retire as they finish, so work
+// on higher-priority streams gets SMs meanwhile).  The workspace must hold the split of the same L.
+sr_status trail_split_i8(const double2* L, long long ldl, long long m, long long K, void* ws, size_t ws_bytes,
+                         cudaStream_t st);
+sr_status trail_apply_i8(long long m, long long K, double2* C, long long ldc, void* ws, long long r0, int jlim,
+                         long long ctas, cudaStream_t st);
 
 }  // namespace oz
 }  // namespace sr
