@@ -255,6 +255,11 @@ bool inner_tiles() {
   return v != 0;
 }
 
+int side_tm() {
+  static const int v = env_int("SR_SIDE_TM", 16);
+  return v;
+}
+
 // Trailing-update lookahead (see solve_block); SR_LOOKAHEAD=0 turns it off, SR_TRAIL_B_TPC
 // sets the tiles per CTA of the off-chain part.
 bool lookahead() {
@@ -357,6 +362,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
         if (p > p0) SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.eb, 0));
         timer_begin("chol_next_rows", Q.s3);
         if (inner_tiles()) SR_TRY((gram::launch<gram::NH, gram::SUB>(next_rows, Q.s3)));
+        else if (side_tm() == 32) SR_TRY((gram::launch_skinny<gram::SUB, 32>(next_rows, Q.s3)));
         else SR_TRY((gram::launch_skinny<gram::SUB>(next_rows, Q.s3)));
         timer_end(Q.s3);
         SR_CUDA(cudaEventRecord(Q.ec, Q.s3));
@@ -365,6 +371,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
         SR_CUDA(cudaStreamWaitEvent(Q.s2, Q.ea, 0));
         timer_begin("chol_inner_rest", Q.s2);
         if (inner_tiles()) SR_TRY((gram::launch<gram::NH, gram::SUB>(inner_rest, Q.s2)));
+        else if (side_tm() == 32) SR_TRY((gram::launch_skinny<gram::SUB, 32>(inner_rest, Q.s2)));
         else SR_TRY((gram::launch_skinny<gram::SUB>(inner_rest, Q.s2)));
         timer_end(Q.s2);
         SR_CUDA(cudaEventRecord(Q.eb, Q.s2));

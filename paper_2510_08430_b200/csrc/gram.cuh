@@ -298,13 +298,15 @@ inline sr_status launch(const ProbSet& ps, cudaStream_t st) {
 // pipeline latency (~20 us) sits on the critical path; here a CTA owns 16 full rows
 // (all 64 columns, so the in-place TRSM reads its rows before anyone writes them), the whole
 // K = 64 is staged in two cp.async halves, and 4 warps each take 16 columns.
-constexpr int SK_TM = 16;
+// The off-chain in-strip updates use 32-row CTAs (TM = 32: B staged once per 32 rows).
 constexpr int SK_LD = 68;   // 1088 B per row (mod 128 = 64: conflict-free LDS.128 fragments)
 constexpr int SK_THREADS = 128;
-constexpr size_t kSkinnySmem = (size_t)(SK_TM + 64) * SK_LD * sizeof(double2);   // 87 KB
+template <int TM>
+constexpr size_t skinny_smem() { return (size_t)(TM + 64) * SK_LD * sizeof(double2); }   // 87 / 104 KB
 
-template <int EP>
+template <int EP, int SK_TM = 16>
 __global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_constant__ ProbSet ps) {
+  constexpr int MI = SK_TM / 8;
   TraceScope trace_(EP == STORE ? TR_TRSM : TR_SKINNY_SUB, (int)ps.p[0].M);
   extern __shared__ __align__(16) double2 smem[];
   double2* sa = smem;
@@ -336,9 +338,9 @@ __global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_cons
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lr = lane >> 2, lk = lane & 3;
-  double acc_r[2][2][2], acc_i[2][2][2];
+  double acc_r[MI][2][2], acc_i[MI][2][2];
 #pragma unroll
-  for (int a = 0; a < 2; a++)
+  for (int a = 0; a < MI; a++)
 #pragma unroll
     for (int b = 0; b < 2; b++) {
       acc_r[a][b][0] = acc_r[a][b][1] = 0.0;
@@ -350,9 +352,9 @@ __global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_cons
     __syncthreads();
 #pragma unroll
     for (int k4 = 32 * h; k4 < 32 * h + 32; k4 += 4) {
-      double ar[2], ai[2], nai[2], br[2], bi[2];
+      double ar[MI], ai[MI], nai[MI], br[2], bi[2];
 #pragma unroll
-      for (int mi = 0; mi < 2; mi++) {
+      for (int mi = 0; mi < MI; mi++) {
         const double2 v = sa[(mi * 8 + lr) * SK_LD + k4 + lk];
         ar[mi] = v.x;
         ai[mi] = v.y;
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_cons
         bi[ni] = -v.y;   // b(k,n) = conj(B[n][k])
       }
 #pragma unroll
-      for (int mi = 0; mi < 2; mi++)
+      for (int mi = 0; mi < MI; mi++)
 #pragma unroll
         for (int ni = 0; ni < 2; ni++) {
           dmma(acc_r[mi][ni][0], acc_r[mi][ni][1], ar[mi], br[ni]);
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_cons
     }
   }
 #pragma unroll
-  for (int mi = 0; mi < 2; mi++)
+  for (int mi = 0; mi < MI; mi++)
 #pragma unroll
     for (int ni = 0; ni < 2; ni++) {
       const int m = m0 + mi * 8 + lr;
@@ -393,8 +395,9 @@ __global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_cons
 }
 
 // Launch a set of NH problems with N <= 64 and K <= 64 (not lower) on the skinny kernel.
-template <int EP>
+template <int EP, int SK_TM = 16>
 inline sr_status launch_skinny(ProbSet ps, cudaStream_t st, bool pdl = false) {
+  constexpr size_t kSkinnySmem = skinny_smem<SK_TM>();
   static_assert(EP == SUB || EP == STORE, "skinny epilogues: SUB or STORE");
   long long total = 0;
   for (int i = 0; i < ps.count; i++) {
@@ -405,11 +408,12 @@ inline sr_status launch_skinny(ProbSet ps, cudaStream_t st, bool pdl = false) {
   if (total == 0) return SR_OK;
   static bool attr_set = false;
   if (!attr_set) {
-    SR_CUDA(cudaFuncSetAttribute(skinny_kernel<EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSkinnySmem));
+    SR_CUDA(cudaFuncSetAttribute(skinny_kernel<EP, SK_TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSkinnySmem));
     attr_set = true;
   }
-  if (pdl) SR_CUDA(launch_pdl(skinny_kernel<EP>, dim3((unsigned)total), dim3(SK_THREADS), kSkinnySmem, st, ps));
-  else skinny_kernel<EP><<<(unsigned)total, SK_THREADS, kSkinnySmem, st>>>(ps);
+  if (pdl) SR_CUDA(launch_pdl(skinny_kernel<EP, SK_TM>, dim3((unsigned)total), dim3(SK_THREADS), kSkinnySmem, st, ps));
+  else skinny_kernel<EP, SK_TM><<<(unsigned)total, SK_THREADS, kSkinnySmem, st>>>(ps);
   SR_LAUNCHED();
   return SR_OK;
 }

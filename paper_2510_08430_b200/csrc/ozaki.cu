@@ -502,13 +502,16 @@ __global__ void __launch_bounds__(256) oz_split(const double2* __restrict__ A, l
   }
   uint64_t pk[3][kSlices];
   {
+    const int ks = 54 - e;   // scaling by 2^ks: one exact multiply unless 2^ks is not a normal double
+    const bool fast = ks >= -1022 && ks <= 1023;
+    const double sc = fast ? __longlong_as_double((long long)(ks + 1023) << 52) : 0.0;
     uint64_t ur[8], ui[8], un[8];
 #pragma unroll
     for (int r = 0; r < 8; r++) {
       const long long k = k0 + kg * 8 + r;
       double2 v = make_double2(0.0, 0.0);
       if (j < n && k < K) v = A[k * lda + c0 + j];
-      const long long xr = llrint(scalbn(v.x, 54 - e)), xi = llrint(scalbn(v.y, 54 - e));
+      const long long xr = llrint(fast ? v.x * sc : scalbn(v.x, ks)), xi = llrint(fast ? v.y * sc : scalbn(v.y, ks));
       ur[r] = digit_bytes(xr);
       ui[r] = digit_bytes(xi);
       un[r] = digit_bytes(-xr);
@@ -549,6 +552,9 @@ __global__ void __launch_bounds__(256) oz_split_rows(const double2* __restrict__
   int e = column_exponent(mx);
   if (lane == 0) expo[i] = e;
   if (e == kNonFinite) e = 0;
+  const int ks = 54 - e;   // scaling by 2^ks as in oz_split
+  const bool fast = ks >= -1022 && ks <= 1023;
+  const double sc = fast ? __longlong_as_double((long long)(ks + 1023) << 52) : 0.0;
   for (int k0 = lane * 8; k0 < Kp; k0 += 256) {
     uint64_t pk[3][kSlices];
     {
@@ -557,7 +563,7 @@ __global__ void __launch_bounds__(256) oz_split_rows(const double2* __restrict__
       for (int r = 0; r < 8; r++) {
         const int k = k0 + r;
         const double2 v = k < K ? row[k] : make_double2(0.0, 0.0);
-        const long long xr = llrint(scalbn(v.x, 54 - e)), xi = llrint(scalbn(-v.y, 54 - e));
+        const long long xr = llrint(fast ? v.x * sc : scalbn(v.x, ks)), xi = llrint(fast ? -v.y * sc : scalbn(-v.y, ks));
         ur[r] = digit_bytes(xr);
         ui[r] = digit_bytes(xi);
         un[r] = digit_bytes(-xr);

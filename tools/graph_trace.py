@@ -26,10 +26,11 @@ for _ in range(3):
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-step.replay()
+for _ in range(10):
+    step.replay()
 e1.record()
 torch.cuda.synchronize()
-print(f"{w.name}: graph step {e0.elapsed_time(e1):.3f} ms (untraced)")
+print(f"{w.name}: graph step {e0.elapsed_time(e1) / 10:.3f} ms (untraced, mean of 10 replays)")
 buf = torch.zeros(40 * 4_000_000, dtype=torch.uint8, device=dev)
 sr.sr_trace_buffer(buf)
 step.replay()
@@ -70,3 +71,30 @@ for blk, ds in sorted(diags.items()):
             inside = [(a, b, k, tag) for a, b, k, tag, n in L if a >= ds[i][0] and a < b0 and k != "diag"]
             desc = " ".join(f"{k}[{tag}]@{a - a0:.0f}+{b - a:.0f}" for a, b, k, tag in inside[:8])
             print(f"  p={ds[i][2]:3d} diag {ds[i][1] - ds[i][0]:5.1f} gap {b0 - a0:6.1f} | {desc}")
+
+# SM occupancy over the solve window: per SM, the union of its CTA intervals
+t_a = min(t0 for g, k, tag, sm, t0, t1 in recs if k == "diag")
+t_b = max(t1 for g, k, tag, sm, t0, t1 in recs if k in ("back", "back_rest", "output"))
+per_sm = collections.defaultdict(list)
+for g, k, tag, sm, t0, t1 in recs:
+    if t1 > t_a and t0 < t_b:
+        per_sm[sm].append((max(t0, t_a), min(t1, t_b), k))
+busy_all, by_kind = [], collections.Counter()
+for sm, iv in per_sm.items():
+    iv.sort()
+    busy, cur_a, cur_b = 0, None, None
+    for a, b, k in iv:
+        by_kind[k] += b - a
+        if cur_b is None or a > cur_b:
+            if cur_b is not None:
+                busy += cur_b - cur_a
+            cur_a, cur_b = a, b
+        else:
+            cur_b = max(cur_b, b)
+    if cur_b is not None:
+        busy += cur_b - cur_a
+    busy_all.append(busy / (t_b - t_a))
+n_sm = 148
+print(f"solve window {(t_b - t_a) / 1e3:.0f} us: SMs with work {len(busy_all)}, mean busy fraction "
+      f"{sum(busy_all) / n_sm:.2f} (union of CTA lifetimes per SM); CTA-time by kind (SM-us): "
+      + ", ".join(f"{k} {v / 1e3:.0f}" for k, v in by_kind.most_common()))
