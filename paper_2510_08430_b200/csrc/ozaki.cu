@@ -161,6 +161,7 @@ __device__ __forceinline__ double pow2_scale(double v, int k) {
 // Global tile t -> (block, row panel I, column panel J, pass).  Within a block the lower
 // triangle tiles (J <= 2I + 1, i.e. some i >= j) are rasterised in bands of kBand row
 // panels, column-major inside a band, and come in (Re, Im) pairs sharing the A panel.
+template <int R = 2>
 __device__ __forceinline__ void decode(const Params& P, long long t, int& b, int& I, int& J, int& pass) {
   b = 0;
   while (b + 1 < P.nblk && t >= P.b[b + 1].tile_begin) b++;
@@ -171,7 +172,7 @@ __device__ __forceinline__ void decode(const Params& P, long long t, int& b, int
   if (P.b[b].jlim > 0) {   // trapezoid: row I holds min(CT, 2I + 2, jlim) tiles
     const int jl = min(CT, P.b[b].jlim);
     for (int i = 0; i < RT; i++) {
-      const int c = min(jl, 2 * i + 2);
+      const int c = min(jl, R * i + R);
       if (u < c) {
         I = i;
         J = (int)u;
@@ -185,12 +186,12 @@ __device__ __forceinline__ void decode(const Params& P, long long t, int& b, int
   for (int I0 = 0; I0 < RT; I0 += kBand) {
     const int I1 = min(RT, I0 + kBand), h = I1 - I0;
     long long cnt = 0;
-    for (int i = I0; i < I1; i++) cnt += min(CT, 2 * i + 2);
+    for (int i = I0; i < I1; i++) cnt += min(CT, R * i + R);
     if (u >= cnt) {
       u -= cnt;
       continue;
     }
-    const int full = min(CT, 2 * I0);
+    const int full = min(CT, R * I0);
     if (u < (long long)full * h) {
       J = (int)(u / h);
       I = I0 + (int)(u % h);
@@ -198,7 +199,7 @@ __device__ __forceinline__ void decode(const Params& P, long long t, int& b, int
     }
     u -= (long long)full * h;
     for (int j = full; j < CT; j++) {
-      const int lo = max(I0, j >> 1);
+      const int lo = max(I0, j / R);
       const int c = I1 - lo;
       if (u < c) {
         J = j;
@@ -418,6 +419,276 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// ---------------------------------------------------------------- CTA-pair variant
+// gram_i8_2sm: the same product on CTA pairs (cluster of 2, tcgen05 cta_group::2): a pair
+// computes a 256 x 64 tile, each CTA holding its own 128 rows of A (and of the result in
+// its TMEM), and the B operand of every MMA split between the two CTAs by N (the first N/2
+// rows of B from the leader's shared memory, the rest from the peer's).  B reaches each SM
+// once instead of twice, so the shared-memory traffic per K step and SM drops from 138 KB
+// (TMA writes 42 + MMA reads 96) to 116 KB (40 + 48 + 28), below the tensor time of the
+// step.  Slice pairs per K step (12 MMAs, N = 64 k, k in {1, 2, 4} so that every N/2
+// boundary falls on a slice or half-slice boundary):
+//   region  rows  leader holds        peer holds           used by (p, q..)
+//   R0      128   slices 0,1          slices 2,3           (p, 0..3) for p <= 3
+//   R1       64   slice 4             slice 5              (p, 4..5) for p <= 1
+//   R2       64   slice 0             slice 1              (p, 0..1) for p = 4, 5
+//   H0..H3   32   rows 0-31 of 0,2,4,6  rows 32-63 of 0,2,4,6  (p, q) single: (6,0) (4,2) (2,4) (0,6)
+constexpr int kR0 = 128, kR1 = 64, kR2 = 64, kH = 32;
+constexpr int kB2Rows = kR0 + kR1 + kR2 + 4 * kH;                    // 384
+constexpr int kStage2 = kSlices * kASlice + kB2Rows * BKB;          // 81920
+constexpr size_t kSmem2 = (size_t)kStages * kStage2 + 1024 + 256;
+constexpr uint32_t idesc2_n(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar_cluster) : "memory");
+}
+// TMA into this CTA's shared memory, completing on the (leader's) barrier at a shared::cluster address.
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.cta_group::2 [%0], [%1, {%2, "
+      "%3, %4}], [%5];\n" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t acc,
+                                            uint32_t idesc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {   // arrives on `bar` in both CTAs of the pair
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(bar),
+      "h"((unsigned short)3)
+      : "memory");
+}
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gram_i8_2sm(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b2,
+                const __grid_constant__ CUtensorMap tm_b1, const __grid_constant__ CUtensorMap tm_h,
+                const Params P) {
+  TraceScope trace_(MODE == MODE_HERM ? TR_GRAM : TR_TRAIL, P.b[0].n);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStage2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
+  const uint32_t tfull = smem_u32(bars + 2 * kStages), tempty = smem_u32(bars + 2 * kStages + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const long long cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const uint32_t full0_lead = mapa_shared(full0, 0), tempty_lead = mapa_shared(tempty, 0);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 2 * kEpiWarps);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm_b2) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm_b1) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm_h) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();   // both CTAs' barriers initialised and TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t smem_base = smem_u32(smem);
+
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer (both CTAs; completion on the leader's barrier)
+      int s = 0;
+      uint32_t ph = 0;
+      for (long long t = cid; t < P.total_tiles; t += ncl) {
+        int b, I, J, pass;
+        decode<4>(P, t, b, I, J, pass);
+        const int rowA = (int)(P.b[b].col0 + (long long)(2 * I + (int)rank) * BM);
+        const int rowB = (int)(P.b[b].col0 + (long long)J * BN);
+        const int kB = pass ? (int)P.Kp : 0;
+        for (int kk = 0; kk < P.kstages; kk++) {
+          mbar_wait(empty0 + 8 * s, ph ^ 1);
+          if (rank == 0) mbar_expect_tx(full0 + 8 * s, 2 * kStage2);
+          const uint32_t sa = smem_base + s * kStage2, sb = sa + kSlices * kASlice;
+          const uint32_t fb = full0_lead + 8 * s;
+          const int kc = kk * BKB;
+          tma_load_3d_pair(sa, &tm_a, kc, rowA, 0, fb);
+          tma_load_3d_pair(sb, &tm_b2, kB + kc, rowB, rank ? 2 : 0, fb);                       // R0
+          tma_load_3d_pair(sb + kR0 * BKB, &tm_b1, kB + kc, rowB, rank ? 5 : 4, fb);          // R1
+          tma_load_3d_pair(sb + (kR0 + kR1) * BKB, &tm_b1, kB + kc, rowB, rank ? 1 : 0, fb);  // R2
+#pragma unroll
+          for (int h = 0; h < 4; h++)                                                            // H0..H3
+            tma_load_3d_pair(sb + (kR0 + kR1 + kR2 + h * kH) * BKB, &tm_h, kB + kc, rowB + (int)rank * kH, 2 * h, fb);
+          if (++s == kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {   // ---------------- MMA issuer (leader CTA only)
+      int s = 0;
+      uint32_t ph = 0, acc_ph = 0;
+      for (long long t = cid; t < P.total_tiles; t += ncl) {
+        for (int kk = 0; kk < P.kstages; kk++) {
+          const int kin = kk % P.spc;
+          if (kin == 0) {   // accumulators drained by both CTAs' epilogues?
+            mbar_wait(tempty, acc_ph ^ 1);
+            acc_ph ^= 1;
+            tc_fence_after();
+          }
+          mbar_wait(full0 + 8 * s, ph);
+          tc_fence_after();
+          const uint32_t sa = smem_base + s * kStage2, sb = sa + kSlices * kASlice;
+          const uint32_t r0 = sb, r1 = sb + kR0 * BKB, r2 = r1 + kR1 * BKB, h0 = r2 + kR2 * BKB;
+#pragma unroll
+          for (int ks = 0; ks < BKB / 32; ks++) {
+            const uint32_t ko = ks * 32;
+            const uint32_t first = (kin > 0 || ks > 0) ? 1u : 0u;
+            // D column of digit diagonal d: 64 d.  A slice p: sa + p * kASlice.
+#pragma unroll
+            for (int p = 0; p < kSlices; p++) {
+              const uint64_t ad = sdesc(sa + p * kASlice + ko);
+              const uint32_t acc = (first || p > 0) ? 1u : 0u;
+              if (p <= 3) mma_i8_pair(tmem + 64 * p, ad, sdesc(r0 + ko), acc, idesc2_n(256));         // q 0..3
+              if (p <= 1) mma_i8_pair(tmem + 64 * (p + 4), ad, sdesc(r1 + ko), acc, idesc2_n(128));   // q 4..5
+              if (p == 4 || p == 5) mma_i8_pair(tmem + 64 * p, ad, sdesc(r2 + ko), acc, idesc2_n(128));   // q 0..1
+              if (p == 4) mma_i8_pair(tmem + 64 * 6, ad, sdesc(h0 + 1 * kH * BKB + ko), acc, idesc2_n(64));   // q 2
+              if (p == 2) mma_i8_pair(tmem + 64 * 6, ad, sdesc(h0 + 2 * kH * BKB + ko), acc, idesc2_n(64));   // q 4
+              if (p == 0) mma_i8_pair(tmem + 64 * 6, ad, sdesc(h0 + 3 * kH * BKB + ko), acc, idesc2_n(64));   // q 6
+              if (p == 6) mma_i8_pair(tmem + 64 * 6, ad, sdesc(h0 + ko), acc, idesc2_n(64));                  // q 0
+            }
+          }
+          tc_commit_pair(empty0 + 8 * s);   // frees the stage in both CTAs when these MMAs complete
+          if (kin == P.spc - 1 || kk == P.kstages - 1) tc_commit_pair(tfull);
+          if (++s == kStages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else {   // ---------------- epilogue (both CTAs, own 128 rows): TMEM -> FP64 recombination -> S
+    const int q4 = warp & 3;             // TMEM lane quarter this warp may access
+    const int rl = q4 * 32 + lane;       // tile row of this thread
+    const int c0 = ((warp - 2) >> 2) * (BN / 2);   // first of this warp's 32 tile columns
+    const int nchunks = (P.kstages + P.spc - 1) / P.spc;
+    uint32_t c = 0;
+    for (long long t = cid; t < P.total_tiles; t += ncl) {
+      int b, I, J, pass;
+      decode<4>(P, t, b, I, J, pass);
+      I = 2 * I + rank;   // this CTA's 128-row half of the 256-row tile
+      const Blk& B = P.b[b];
+      const int n = B.n;
+      const int i = I * BM + rl;
+      const bool row_ok = i < n;
+      const int ei = row_ok ? P.expo[B.col0 + i] : 0;
+      double* Cb = reinterpret_cast<double*>(B.C);
+      const long long ldc = B.ldc;
+      for (int ch = 0; ch < nchunks; ch++, c++) {
+        mbar_wait(tfull, c & 1);
+        tc_fence_after();
+        // Phase 1: TMEM -> registers, the seven digit-diagonal sums combined by Horner
+        // (exact int32 -> FP64), then TMEM is released so the next tile's MMAs overlap
+        // phase 2 (scaling and the global writes).
+        double vals[BN / 2];
+#pragma unroll
+        for (int cc = 0; cc < BN / 16; cc++) {
+          uint32_t g[kSlices][8];
+#pragma unroll
+          for (int tt = 0; tt < kSlices; tt++)
+            tmem_ld8(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(tt * BN + c0 + cc * 8), g[tt]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 8; e++) {
+            double v = (double)(int)g[0][e];
+#pragma unroll
+            for (int tt = 1; tt < kSlices; tt++) v = fma(v, 256.0, (double)(int)g[tt][e]);
+            vals[cc * 8 + e] = v;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_lead);   // the leader's MMA issuer waits for both CTAs
+        // Phase 2 (column exponents fetched once per lane, broadcast by shuffles)
+        const int jl = J * BN + c0 + lane;
+        const int ej_lane = jl < n ? P.expo[B.col0 + jl] : 0;
+        const int jb = J * BN + c0;
+        double* dp = Cb + 2 * ((long long)i * ldc + jb) + pass;   // C[i][j], j = jb + e
+        double* mp = Cb + 2 * ((long long)jb * ldc + i) + pass;   // C[j][i]
+        const long long mstep = 2 * ldc;
+#pragma unroll
+        for (int e = 0; e < BN / 2; e++, mp += mstep) {
+          const int ej = __shfl_sync(0xffffffffu, ej_lane, e);
+          const int j = jb + e;
+          if (!row_ok || j >= n || j > i) continue;
+          // a non-finite input column poisons its row and column of the result, as in FP64
+          const double val = (ei == kNonFinite || ej == kNonFinite) ? __longlong_as_double(0x7FF8000000000000LL)
+                                                                     : pow2_scale(vals[e], ei + ej - 60);
+          if (MODE == MODE_SUB) {
+            // C -= G on the lower triangle by a fire-and-forget reduction in L2
+            // (red.global.add.f64): each element receives exactly one addend per launch
+            // (Re pass -> .x, Im pass -> .y), so the result is deterministic.
+            atomicAdd(dp + 2 * e, -val);
+            continue;
+          }
+          if (nchunks == 1) {
+            if (i == j) {
+              dp[2 * e] = pass ? 0.0 : val;
+            } else {
+              dp[2 * e] = val;
+              *mp = pass ? -val : val;
+            }
+            continue;
+          }
+          double acc = val;
+          if (ch > 0) acc += dp[2 * e];
+          if (ch + 1 < nchunks) {
+            dp[2 * e] = acc;
+          } else if (i == j) {
+            dp[2 * e] = pass ? 0.0 : acc;
+          } else {
+            dp[2 * e] = acc;
+            *mp = pass ? -acc : acc;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+  }
+}
+
 // Column maxima of max(|Re|, |Im|) over samples, as the bit patterns of |x|: for
 // non-negative doubles the order of the patterns is the order of the values, and Inf / NaN
 // patterns exceed every finite one, so a non-finite entry marks its column (kNonFinite).
@@ -601,12 +872,12 @@ sr_status get_encode(EncodeFn& fn) {
   return SR_OK;
 }
 
-sr_status make_map(CUtensorMap& m, void* base, long long Kp, long long ncols, int rows) {
+sr_status make_map(CUtensorMap& m, void* base, long long Kp, long long ncols, int rows, int box_slices = kSlices) {
   EncodeFn enc;
   SR_TRY(get_encode(enc));
   const cuuint64_t dims[3] = {(cuuint64_t)(3 * Kp), (cuuint64_t)ncols, (cuuint64_t)kSlices};
   const cuuint64_t strides[2] = {(cuuint64_t)(3 * Kp), (cuuint64_t)(3 * Kp * ncols)};
-  const cuuint32_t box[3] = {(cuuint32_t)BKB, (cuuint32_t)rows, (cuuint32_t)kSlices};
+  const cuuint32_t box[3] = {(cuuint32_t)BKB, (cuuint32_t)rows, (cuuint32_t)box_slices};
   const cuuint32_t es[3] = {1, 1, 1};
   const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -625,17 +896,19 @@ sr_status set_attrs() {
   if (!attr) {
     SR_CUDA(cudaFuncSetAttribute(gram_i8<MODE_HERM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
     SR_CUDA(cudaFuncSetAttribute(gram_i8<MODE_SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+    SR_CUDA(cudaFuncSetAttribute(gram_i8_2sm<MODE_HERM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2));
+    SR_CUDA(cudaFuncSetAttribute(gram_i8_2sm<MODE_SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2));
     SR_CUDA(cudaFuncSetAttribute(oz_split, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSplitSmem));
     attr = true;
   }
   return SR_OK;
 }
 
-long long lower_tiles(int n, int jlim = 0) {
-  const int RT = (n + BM - 1) / BM, CT = (n + BN - 1) / BN;
+long long lower_tiles(int n, int jlim = 0, int R = 2) {
+  const int RT = (n + R * BN - 1) / (R * BN), CT = (n + BN - 1) / BN;
   const int jl = jlim > 0 ? std::min(CT, jlim) : CT;
   long long cnt = 0;
-  for (int i = 0; i < RT; i++) cnt += std::min(jl, 2 * i + 2);
+  for (int i = 0; i < RT; i++) cnt += std::min(jl, R * i + R);
   return cnt;
 }
 
@@ -676,6 +949,16 @@ size_t workspace_bytes(long long ns, int nblk, const int64_t* offs) {
 // Grid of the block-QGT launch: one persistent CTA per SM by default; SR_GRAM_CTAS=n sets
 // n CTAs (more than the SMs makes the kernel non-persistent, so that concurrent work on
 // other streams -- the pipelined step's block solves -- gets SMs as CTAs retire).
+// CTA-pair Gram kernel (gram_i8_2sm) for the block QGT: SR_GRAM_2SM=1 (experimental).
+bool gram_pairs() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SR_GRAM_2SM");
+    v = e ? atoi(e) != 0 : 0;
+  }
+  return v != 0;
+}
+
 long long gram_ctas() {
   static long long v = -1;
   if (v < 0) {
@@ -729,6 +1012,8 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
     P.kstages = (int)(2 * Kp / BKB);
     P.spc = kChunkK / BKB;
     P.expo = expo;
+    const bool pair = gram_pairs();
+    const int R = pair ? 4 : 2;   // 64-column tiles per row tile (256- or 128-row tiles)
     long long tiles = 0;
     for (int k = 0; k < P.nblk; k++) {
       const int b = G.b0 + k;
@@ -738,20 +1023,32 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
       B.C = S + soff;
       B.ldc = B.n;
       soff += (long long)B.n * B.n;
-      B.RT = (B.n + BM - 1) / BM;
+      B.RT = (B.n + R * BN - 1) / (R * BN);
       B.CT = (B.n + BN - 1) / BN;
       B.tile_begin = tiles;
-      tiles += 2 * lower_tiles(B.n);
+      tiles += 2 * lower_tiles(B.n, 0, R);
     }
     P.total_tiles = tiles;
     CUtensorMap ma, mb2;
     SR_TRY(make_map(ma, E, Kp, nc, BM));
-    SR_TRY(make_map(mb2, E, Kp, nc, BN));
-    const unsigned grid = (unsigned)std::min<long long>(tiles, gram_ctas());
-    timer_begin("gram_i8", st);
-    gram_i8<MODE_HERM><<<grid, kThreads, kSmem, st>>>(ma, mb2, P);
-    timer_end(st);
-    SR_LAUNCHED();
+    if (pair) {
+      CUtensorMap mbb2, mbb1, mbh;
+      SR_TRY(make_map(mbb2, E, Kp, nc, BN, 2));
+      SR_TRY(make_map(mbb1, E, Kp, nc, BN, 1));
+      SR_TRY(make_map(mbh, E, Kp, nc, BN / 2, 1));
+      const unsigned grid = 2 * (unsigned)std::min<long long>(tiles, kNumSMs / 2);
+      timer_begin("gram_i8", st);
+      gram_i8_2sm<MODE_HERM><<<grid, kThreads, kSmem2, st>>>(ma, mbb2, mbb1, mbh, P);
+      timer_end(st);
+      SR_LAUNCHED();
+    } else {
+      SR_TRY(make_map(mb2, E, Kp, nc, BN));
+      const unsigned grid = (unsigned)std::min<long long>(tiles, gram_ctas());
+      timer_begin("gram_i8", st);
+      gram_i8<MODE_HERM><<<grid, kThreads, kSmem, st>>>(ma, mb2, P);
+      timer_end(st);
+      SR_LAUNCHED();
+    }
   }
   return SR_OK;
 }

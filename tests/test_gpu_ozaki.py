@@ -220,3 +220,20 @@ def test_block_qgt_i8_non_finite_columns(sr):
         assert np.all(np.isnan(g[b])) and np.all(np.isnan(g[:, b]))
     ref = A[:, good].conj().T @ A[:, good]
     assert rel(g[np.ix_(good, good)], ref) < 1e-11
+
+
+def test_block_qgt_i8_cta_pairs():
+    """The CTA-pair variant of the Gram kernel (gram_i8_2sm, tcgen05 cta_group::2; selected by
+    SR_GRAM_2SM=1 at process start, measured slower and off by default) passes the same parity
+    cases: run them in a child process with the switch set."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SR_GRAM_2SM="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_ozaki.py"),
+                        "-k", "test_block_qgt_i8_parity or matches_fp64 or non_finite"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout

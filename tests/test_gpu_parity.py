@@ -272,6 +272,48 @@ def test_step_and_step_host(sr):
     sr.sr_step_host(w.widths, torch.from_numpy(theta_h).pin_memory(), torch.from_numpy(spins).pin_memory(),
                     torch.from_numpy(ij), torch.from_numpy(jj), w.lam, dh, eh, ws)
     assert torch.equal(dh, d.cpu()) and torch.equal(eh, en.cpu())
+    # second call replays the cached CUDA graph of the step (include/sr_block.h): new inputs
+    # are read from the workspace at replay time, so a different theta gives its own result
+    theta2 = theta_h * 1.01
+    sr.sr_step(w.widths, T(theta2), T(spins), T(ij), T(jj), w.lam, d, en, ws)
+    sr.sr_step_host(w.widths, torch.from_numpy(theta2).pin_memory(), torch.from_numpy(spins).pin_memory(),
+                    torch.from_numpy(ij), torch.from_numpy(jj), w.lam, dh, eh, ws)
+    assert torch.equal(dh, d.cpu()) and torch.equal(eh, en.cpu())
+    assert not torch.equal(dh, torch.from_numpy(ref))
+
+
+def test_device_trace(sr):
+    """sr_trace_buffer: one record per CTA of the traced kernels, inside a CUDA-graph replay."""
+    n, ns = 300, 200
+    g = torch.Generator(device=dev()).manual_seed(3)
+    A = torch.randn(ns, n, dtype=C128, device=dev(), generator=g) / ns ** 0.5
+    offs = [0, n]
+    S = torch.empty(n * n, dtype=C128, device=dev())
+    F = torch.randn(n, dtype=C128, device=dev(), generator=g)
+    d = torch.empty_like(F)
+    sr.sr_block_qgt_i8(A, offs, S)
+    sr.sr_block_solve(offs, S, F, 1e-3, d)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        sr.sr_block_qgt_i8(A, offs, S)
+        sr.sr_block_solve(offs, S, F, 1e-3, d)
+    buf = torch.zeros(40 * 100000, dtype=torch.uint8, device=dev())
+    sr.sr_trace_buffer(buf)
+    try:
+        graph.replay()
+        torch.cuda.synchronize()
+    finally:
+        sr.sr_trace_buffer(None)
+    recs = sr.sr_trace_records(buf)
+    kinds = {r[1] for r in recs}
+    assert {"gram", "split", "colmax", "diag", "trsm", "back", "output"} <= kinds
+    assert all(r[5] >= r[4] > 0 for r in recs)
+    assert sum(1 for r in recs if r[1] == "diag") == (n + 63) // 64   # one CTA per panel
+    # tracing off: nothing more is appended
+    graph.replay()
+    torch.cuda.synchronize()
+    assert len(sr.sr_trace_records(buf)) == len(recs)
 
 
 @pytest.mark.parametrize("cfg", [1, 2, 3])

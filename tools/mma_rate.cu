@@ -3,6 +3,7 @@
 // K-major), one CTA per SM, 512 TMEM columns.  Prints MACs/clk/SM and chip TOPS.
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, int sw) {
@@ -13,12 +14,13 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, int sw) {
 }
 
 template <int KIND>  // 0 = i8, 1 = f16 (bf16)
-__global__ void __launch_bounds__(128, 1) bench(int N, int iters, int sw, int nacc, long long* out) {
+__global__ void __launch_bounds__(128, 1) bench(int N, int iters, int sw, int nacc, long long* out, int rnd = 0) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x)   // zeros, or random bytes (power runs)
+    reinterpret_cast<uint32_t*>(sm)[i] = rnd ? (uint32_t)(i * 2654435761u) ^ (uint32_t)(blockIdx.x * 40503u) : 0u;
   uint32_t baddr = (uint32_t)__cvta_generic_to_shared(&bar);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(baddr));
@@ -65,7 +67,36 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int iters, int sw, int na
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
-int main() {
+// Power mode: mma_rate power N seconds -- int8 MMAs of M=128 x N x 32 with random operands
+// launched back to back for the given time (sample nvidia-smi alongside); prints the
+// sustained rate.
+int power_mode(int N, double seconds) {
+  long long* d;
+  cudaMalloc(&d, 148 * 8);
+  cudaFuncSetAttribute(bench<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int iters = 200000;
+  bench<0><<<148, 128, 65536>>>(N, iters, 4, 512 / N, d, 1);
+  cudaDeviceSynchronize();
+  float ms = 0.f;
+  long long launches = 0;
+  cudaEventRecord(a);
+  while (ms < seconds * 1e3) {
+    for (int r = 0; r < 10; r++) bench<0><<<148, 128, 65536>>>(N, iters, 4, 512 / N, d, 1);
+    launches += 10;
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+  }
+  const double ops = 2.0 * 128.0 * N * 32 * iters * 148 * launches;
+  printf("i8 N=%d random operands: %.0f T(ops)/s sustained over %.1f s\n", N, ops / (ms * 1e-3) / 1e12, ms / 1e3);
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 3 && argv[1][0] == 'p') return power_mode(atoi(argv[2]), atof(argv[3]));
   long long* d;
   cudaMalloc(&d, 148 * 8);
   long long h[148];
