@@ -48,7 +48,13 @@ constexpr int kChunkK = 16384;            // K' per exact int32 accumulation
 #endif
 constexpr bool kATmem = SR_OZ_A_TMEM;     // operand A staged into TMEM by tcgen05.cp
 constexpr uint32_t kACol = kSlices * BN;  // TMEM columns [448, 504): the A digits of one K step
-constexpr int kBand = 8;                  // row panels per rasterisation band
+#ifndef SR_OZ_EXP
+#define SR_OZ_EXP 0   // energy experiments (tools only): 1 no S stores, 2 no epilogue, 3 L2-resident operands
+#endif
+#ifndef SR_OZ_BAND
+#define SR_OZ_BAND 8
+#endif
+constexpr int kBand = SR_OZ_BAND;         // row panels per rasterisation band
 constexpr int kNonFinite = 1 << 20;       // column exponent marking a column with Inf / NaN
 constexpr int kMaxBlk = 24;
 constexpr int kEpiWarps = 8;              // two per TMEM lane quarter, 32 columns each
@@ -253,8 +259,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (long long t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
         int b, I, J, pass;
         decode(P, t, b, I, J, pass);
-        const int rowA = (int)(P.b[b].col0 + (long long)I * BM);
-        const int rowB = (int)(P.b[b].col0 + (long long)J * BN);
+        const int rowA = SR_OZ_EXP == 3 ? (int)P.b[b].col0 : (int)(P.b[b].col0 + (long long)I * BM);
+        const int rowB = SR_OZ_EXP == 3 ? (int)P.b[b].col0 : (int)(P.b[b].col0 + (long long)J * BN);
         const int kB = pass ? (int)P.Kp : 0;
         for (int kk = 0; kk < P.kstages; kk++) {
           mbar_wait(empty0 + 8 * s, ph ^ 1);
@@ -345,6 +351,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int ch = 0; ch < nchunks; ch++, c++) {
         mbar_wait(tfull, c & 1);
         tc_fence_after();
+        if (SR_OZ_EXP == 2) {   // energy experiment: no epilogue work at all
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty);
+          continue;
+        }
         // Phase 1: TMEM -> registers, the seven digit-diagonal sums combined by Horner
         // (exact int32 -> FP64), then TMEM is released so the next tile's MMAs overlap
         // phase 2 (scaling and the global writes).
@@ -367,6 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty);
+        if (SR_OZ_EXP == 1 && vals[0] != 12345.0) continue;   // energy experiment: no stores
         // Phase 2 (column exponents fetched once per lane, broadcast by shuffles)
         const int jl = J * BN + c0 + lane;
         const int ej_lane = jl < n ? P.expo[B.col0 + jl] : 0;
