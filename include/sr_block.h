@@ -174,7 +174,8 @@ SR_API sr_status sr_center_force_global(int64_t n_local, int64_t n_total, int64_
  *   block_offsets (host) int64 [n_blocks+1], column ranges of the blocks in A
  *   S        complex, blocks packed back to back: block b is n_b x n_b row-major at
  *            element offset sum_{c<b} n_c^2; both triangles written (Hermitian),
- *            diagonal imaginary parts exactly 0. */
+ *            diagonal imaginary parts exactly 0.
+ *   n_samples = 0 writes S = 0 (A may then be NULL; sr_block_qgt_i8 needs no workspace). */
 SR_API size_t sr_block_qgt_workspace_bytes(int n_blocks, const int64_t* block_offsets /*host*/);
 SR_API sr_status sr_block_qgt(int64_t n_samples, int n_blocks,
                               const int64_t* block_offsets /*host*/, const double* A, int64_t lda,

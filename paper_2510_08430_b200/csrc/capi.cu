@@ -454,7 +454,7 @@ SR_API sr_status sr_block_qgt(int64_t n_samples, int n_blocks, const int64_t* bl
   SR_CHECK_ARG(n_samples >= 0 && lda >= block_offsets[n_blocks], "lda < n_p");
   for (int b = 0; b < n_blocks; b++)
     SR_CHECK_ARG(block_offsets[b + 1] - block_offsets[b] < (1LL << 31), "block too large");
-  SR_CHECK_ARG(A && S, "null pointer");
+  SR_CHECK_ARG(S && (A || n_samples == 0), "null pointer");
   return block_qgt_impl(n_samples, n_blocks, block_offsets, reinterpret_cast<const double2*>(A), lda,
                         reinterpret_cast<double2*>(S), (cudaStream_t)stream);
 }
@@ -470,7 +470,7 @@ SR_API sr_status sr_block_qgt_i8(int64_t n_samples, int n_blocks, const int64_t*
   SR_CHECK_ARG(n_samples >= 0 && lda >= block_offsets[n_blocks], "lda < n_p");
   SR_CHECK_ARG(block_offsets[n_blocks] < (1LL << 31) / oz::kSlices, "n_p too large for the slice tensor map");
   SR_CHECK_ARG(n_samples <= (1LL << 31) / 8, "n_samples too large");
-  SR_CHECK_ARG(A && S, "null pointer");
+  SR_CHECK_ARG(S && (A || n_samples == 0), "null pointer");
   return oz::block_qgt_i8(n_samples, n_blocks, block_offsets, reinterpret_cast<const double2*>(A), lda,
                           reinterpret_cast<double2*>(S), workspace, workspace_bytes, (cudaStream_t)stream);
 }

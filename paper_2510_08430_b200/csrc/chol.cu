@@ -401,7 +401,8 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
         SR_CUDA(cudaEventRecord(Q.es, st));
         SR_TRY(oz::trail_apply_i8(m, K, trailing, B.npad, B.tws, 0, kStrip, trail_ctas(cs.count), st));
         SR_CUDA(cudaStreamWaitEvent(Q.s4, Q.es, 0));
-        SR_TRY(oz::trail_apply_i8(m, K, trailing, B.npad, B.tws, look, 0, -trail_b_tpc(), Q.s4));
+        static const int b_ctas = env_int("SR_TRAIL_B_CTAS", 0);   // > 0: persistent (b) on that many CTAs
+        SR_TRY(oz::trail_apply_i8(m, K, trailing, B.npad, B.tws, look, 0, b_ctas > 0 ? b_ctas : -trail_b_tpc(), Q.s4));
         SR_CUDA(cudaEventRecord(Q.et, Q.s4));
         pending_b = true;
       } else if (i8) {   // int8 digit-slice tcgen05 engine (ozaki.cu), lower triangle

@@ -983,15 +983,15 @@ long long gram_ctas() {
 
 sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double2* A, long long lda, double2* S,
                        void* ws, size_t ws_bytes, cudaStream_t st) {
+  long long s_total = 0;
+  for (int b = 0; b < nblk; b++) s_total += (offs[b + 1] - offs[b]) * (offs[b + 1] - offs[b]);
+  if (ns == 0) {   // empty batch: S = 0, nothing read
+    SR_CUDA(cudaMemsetAsync(S, 0, (size_t)s_total * sizeof(double2), st));
+    return SR_OK;
+  }
   if (ws_bytes < workspace_bytes(ns, nblk, offs) || !ws) {
     set_error("sr_block_qgt_i8: workspace too small");
     return SR_ERR_WORKSPACE;
-  }
-  long long s_total = 0;
-  for (int b = 0; b < nblk; b++) s_total += (offs[b + 1] - offs[b]) * (offs[b + 1] - offs[b]);
-  if (ns == 0) {
-    SR_CUDA(cudaMemsetAsync(S, 0, (size_t)s_total * sizeof(double2), st));
-    return SR_OK;
   }
   const long long Kp = pad_k(ns);
   size_t mb = 0;

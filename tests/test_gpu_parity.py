@@ -382,3 +382,27 @@ def test_full_size_config(sr, cfg):
         r = blocks[i] @ d1[lo:hi] + w.lam * d1[lo:hi] + b.F[lo:hi]
         assert (torch.linalg.vector_norm(r) / torch.linalg.vector_norm(b.F[lo:hi])).item() < 1e-9
     assert abs(en.item() - el.mean()) < 1e-12 * abs(el.mean())
+
+
+def test_empty_batch(sr):
+    """N_s = 0 (include/sr_block.h): the Jacobian is a no-op, both Gram engines write S = 0,
+    and the shifted solve of S = 0 is -F / lambda exactly."""
+    w = SMALL_NETS[0][1]
+    _, params = workloads.make_inputs(w)
+    theta = T(sr.model.pack(params))
+    n0, n_p = w.widths[0], w.n_params
+    spins = torch.zeros(1, n0, dtype=torch.int8, device=dev())[:0]
+    lp = torch.zeros(1, dtype=C128, device=dev())[:0]
+    O = torch.zeros(1, n_p, dtype=C128, device=dev())[:0]
+    sr.sr_jacobian(w.widths, theta, spins, lp, O)
+    offs = sr.block_offsets(w.widths)
+    n_s = sum((offs[b + 1] - offs[b]) ** 2 for b in range(len(offs) - 1))
+    for fn in (sr.sr_block_qgt, sr.sr_block_qgt_i8):
+        S = torch.full((n_s,), complex(3.0, 1.0), dtype=C128, device=dev())
+        fn(O, offs, S)
+        assert torch.count_nonzero(S).item() == 0
+    F = torch.randn(n_p, dtype=C128, device=dev())
+    d = torch.empty_like(F)
+    lam = 0.25
+    sr.sr_block_solve(offs, S, F, lam, d)
+    assert torch.allclose(d, -F / lam, rtol=1e-15, atol=0)
