@@ -499,6 +499,7 @@ sr_status local_energy_impl(const NetDesc& net, const double* theta_d, long long
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, sm) != cudaSuccess || per_sm < 1)
       per_sm = 1;
+    if (const char* e = getenv("SR_ENERGY_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
     return (unsigned)std::max<long long>(1, std::min<long long>(max_tiles, (long long)per_sm * kNumSMs));
   };
   if (rb == 32) {
