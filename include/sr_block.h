@@ -20,9 +20,14 @@
  * - Every pointer is a DEVICE pointer unless the argument says (host).  Device
  *   buffers are owned by the caller; the library never allocates or frees device
  *   memory, and keeps no state between calls apart from the process-wide Gram engine
- *   choice (sr_set_gram_engine) and the optional kernel timer (sr_kernel_timer).  Scratch comes in through a
- *   `workspace` pointer whose size the matching *_workspace_bytes() query returns
- *   (256-byte aligned base required).
+ *   choice (sr_set_gram_engine), the optional kernel timer (sr_kernel_timer) and device
+ *   trace (sr_trace_buffer), the CUDA-graph cache of sr_step_host, and a pool of side
+ *   streams/events created on first use (the blocked solves run independent blocks and
+ *   off-chain updates on them, forked from and joined back into `stream`).  Scratch
+ *   comes in through a `workspace` pointer whose size the matching *_workspace_bytes()
+ *   query returns (256-byte aligned base required).
+ * - Threads: calls may come from any host thread, but not concurrently -- the side-stream
+ *   pool, the graph cache and the timer are shared, unsynchronised process state.
  * - `stream` is a cudaStream_t (NULL = legacy default stream).  All device work is
  *   enqueued on it; calls return without synchronising, except sr_step_host.
  * - Network: complex MLP with widths[0..n_layers] (widths[0] = N sites),
