@@ -173,6 +173,12 @@ def run_gpu(args):
         # keep stdout to the one JSON line: the NCCL communicator set-up prints a version banner
         # on fd 1, so it runs with fd 1 pointed at /dev/null
         def _init():
+            if "RANK" not in os.environ:   # --sharded without torchrun: a one-rank group
+                import socket
+                with socket.socket() as so:
+                    so.bind(("127.0.0.1", 0))
+                    port = so.getsockname()[1]
+                os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
             dist.init_process_group("nccl", device_id=dev)
             dist.barrier()
         _quiet_fd1(_init)

@@ -207,22 +207,32 @@ def sr_center_force_global(O, e_loc, n_total, moments, e_tilde, F_partial, energ
 
 
 # ------------------------------------------------------------------ stage (4)
+def _cols(A, name):
+    """A CUDA complex128 matrix whose rows are contiguous (a column slice of a wider matrix
+    is allowed): returns its leading dimension."""
+    if not A.is_cuda or A.dtype != torch.complex128 or A.dim() != 2 or (A.shape[1] > 1 and A.stride(1) != 1):
+        raise SRError(f"{name} must be a CUDA complex128 matrix with unit column stride")
+    return A.stride(0) if A.shape[0] > 1 else A.shape[1]
+
+
 def sr_block_qgt(A, offsets, S):
+    """Stage (4) on the FP64 DMMA engine.  A may be a column slice (leading dimension = A.stride(0))."""
     lib = load()
-    _dev(A, torch.complex128, "A")
+    lda = _cols(A, "A")
     _dev(S, torch.complex128, "S")
     nblk = len(offsets) - 1
     need = sum((offsets[b + 1] - offsets[b]) ** 2 for b in range(nblk))
     if S.numel() < need:
         raise SRError("S too small for the packed blocks")
-    _check(lib.sr_block_qgt(A.shape[0], nblk, _offsets(offsets), _ptr(A), A.shape[1], _ptr(S), None, 0,
+    _check(lib.sr_block_qgt(A.shape[0], nblk, _offsets(offsets), _ptr(A), lda, _ptr(S), None, 0,
                             _stream(A.device)), "sr_block_qgt")
 
 
 def sr_block_qgt_i8(A, offsets, S, workspace=None):
-    """Stage (4) on the int8 tcgen05 tensor cores (digit slices; include/sr_block.h)."""
+    """Stage (4) on the int8 tcgen05 tensor cores (digit slices; include/sr_block.h).  A may be
+    a column slice (leading dimension = A.stride(0))."""
     lib = load()
-    _dev(A, torch.complex128, "A")
+    lda = _cols(A, "A")
     _dev(S, torch.complex128, "S")
     nblk = len(offsets) - 1
     need = sum((offsets[b + 1] - offsets[b]) ** 2 for b in range(nblk))
@@ -230,7 +240,7 @@ def sr_block_qgt_i8(A, offsets, S, workspace=None):
         raise SRError("S too small for the packed blocks")
     off = _offsets(offsets)
     ws = _workspace(lib.sr_block_qgt_i8_workspace_bytes(A.shape[0], nblk, off), A.device, workspace)
-    _check(lib.sr_block_qgt_i8(A.shape[0], nblk, off, _ptr(A), A.shape[1], _ptr(S), *_ws_args(ws),
+    _check(lib.sr_block_qgt_i8(A.shape[0], nblk, off, _ptr(A), lda, _ptr(S), *_ws_args(ws),
                                _stream(A.device)), "sr_block_qgt_i8")
 
 

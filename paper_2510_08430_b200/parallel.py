@@ -197,9 +197,12 @@ class ShardedStep:
     STAGES = STAGES
 
     def __init__(self, widths, spins_all, bij, bj, lam, rank, world, device, ops=None, group=None,
-                 gram_engine="int8"):
+                 gram_engine="int8", per_block_gram=None):
         self.lam = lam
         self.rank, self.world = rank, world
+        # per-block Gram launches, each followed by its asynchronous reduce (default when
+        # partial S_b travel, world > 1); one grouped launch otherwise
+        self.per_block_gram = world > 1 if per_block_gram is None else per_block_gram
         self.group = group
         self.n_total = spins_all.shape[0]
         lo, hi = shard_range(self.n_total, rank, world)
@@ -227,11 +230,25 @@ class ShardedStep:
         o.column_moments(b.O, b.e_loc, self.n_total, self.moments)
         dist.all_gather(list(self.moments_all.unbind(0)), self.moments, group=g)
         o.center_force_global(b.O, b.e_loc, self.n_total, self.moments_all, b.energy, b.e_tilde, b.F)
-        dist.all_reduce(b.F, group=g)
+        # the force all-reduce and each block's reduce to its owner run asynchronously: block
+        # b's partial S travels while the Gram of block b+1 is computed
+        f_work = dist.all_reduce(b.F, group=g, async_op=True)
         _rec(events, 3, st)
-        o.block_qgt(b.O, b.offs, b.S)
-        for blk in range(len(b.offs) - 1):
-            dist.reduce(b.s_block(blk), dst=block_owner(blk, self.world, self.sizes), group=g)
+        nblk = len(b.offs) - 1
+        if not self.per_block_gram:   # one grouped Gram launch, then the reduces
+            o.block_qgt(b.O, b.offs, b.S)
+            works = [dist.reduce(b.s_block(blk), dst=block_owner(blk, self.world, self.sizes), group=g,
+                                 async_op=True) for blk in range(nblk)]
+        else:
+            works = []
+            for blk in range(nblk):
+                lo, hi = b.offs[blk], b.offs[blk + 1]
+                o.block_qgt(b.O[:, lo:hi], [0, hi - lo], b.s_block(blk))
+                works.append(dist.reduce(b.s_block(blk), dst=block_owner(blk, self.world, self.sizes), group=g,
+                                         async_op=True))
+        for wk in works:
+            wk.wait()
+        f_work.wait()
         _rec(events, 4, st)
         b.dtheta.zero_()
         if self.owned:   # this rank's contiguous blocks in one call (concurrent streams)

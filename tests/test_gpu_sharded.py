@@ -35,8 +35,8 @@ def nccl_group():
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cfg", [0, 1])
-def test_sharded_step_matches_local_and_oracle(nccl_group, cfg):
+@pytest.mark.parametrize("cfg,per_block", [(0, False), (1, False), (0, True), (1, True)])
+def test_sharded_step_matches_local_and_oracle(nccl_group, cfg, per_block):
     import paper_2510_08430_b200 as sr
     from paper_2510_08430_b200 import parallel
     w = workloads.CONFIGS[cfg]
@@ -46,7 +46,7 @@ def test_sharded_step_matches_local_and_oracle(nccl_group, cfg):
     theta = torch.from_numpy(sr.model.pack(params)).to(dev)
     local = parallel.LocalStep(w.widths, spins, ij, jj, w.lam, dev)
     d_local, e_local = (x.clone() for x in local.run(theta))
-    shard = parallel.ShardedStep(w.widths, spins, ij, jj, w.lam, 0, 1, dev)
+    shard = parallel.ShardedStep(w.widths, spins, ij, jj, w.lam, 0, 1, dev, per_block_gram=per_block)
     d_shard, e_shard = shard.run(theta)
     torch.cuda.synchronize()
     rel = (torch.linalg.vector_norm(d_shard - d_local) / torch.linalg.vector_norm(d_local)).item()

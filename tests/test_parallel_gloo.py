@@ -81,7 +81,8 @@ def _worker(rank, world, port, result_path):
     spins, params = workloads.make_inputs(w)
     import paper_2510_08430_b200 as sr
     ij, jj = sr.lattice.for_workload(w)
-    step = ShardedStep(w.widths, spins, ij, jj, w.lam, rank, world, "cpu", ops=OracleOps())
+    step = ShardedStep(w.widths, spins, ij, jj, w.lam, rank, world, "cpu", ops=OracleOps(),
+                       per_block_gram=world != 2)   # world 2 also covers the grouped launch
     d, e = step.run(torch.from_numpy(sr.model.pack(params)))
     if rank == 0:
         np.save(result_path, np.concatenate([d.numpy(), e.numpy()]))
