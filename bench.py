@@ -221,9 +221,15 @@ def run_gpu(args):
     stage_ms = {name: float(np.mean([evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(n_stage_runs)]))
                 for i, name in enumerate(step.STAGES)}
 
-    use_graph = not sharded and not args.no_graph
+    use_graph = not args.no_graph
     if use_graph:
-        step.capture(theta)                  # the whole step as one CUDA graph
+        try:
+            step.capture(theta)              # the whole step (collectives included) as one CUDA graph
+        except Exception as exc:             # capture unsupported here: time the eager step instead
+            print(f"bench: CUDA-graph capture failed ({exc}); timing eager launches", file=sys.stderr)
+            use_graph = False
+            torch.cuda.synchronize(dev)
+    if use_graph:
         for _ in range(args.warmup):
             step.replay()
     torch.cuda.synchronize(dev)
@@ -255,7 +261,7 @@ def run_gpu(args):
 
     # e2e: the same step through sr_step_host (host buffers in and out, every step)
     if sharded:
-        e2e = run_e2e_sharded(torch, dist, step, theta_h, dev, args)
+        e2e = run_e2e_sharded(torch, dist, step, theta_h, dev, args, theta if use_graph else None)
     else:
         del step                      # the e2e run allocates its own sr_step workspace
         torch.cuda.empty_cache()
@@ -356,18 +362,20 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
-def run_e2e_sharded(torch, dist, step, theta_h, dev, args):
+def run_e2e_sharded(torch, dist, step, theta_h, dev, args, theta_graph=None):
     """e2e of the sharded step through the public Python API: every step copies theta from
-    pinned host memory, runs parallel.ShardedStep (C ABI + NCCL) and reads dtheta back;
-    host clock between barriers, max over ranks.  (The spins shard stays resident: the
-    samples are the rank's data, not a per-step input.)"""
+    pinned host memory, runs parallel.ShardedStep (C ABI + NCCL; the captured CUDA graph when
+    theta_graph, the buffer it was captured on, is given) and reads dtheta back; host clock
+    between barriers, max over ranks.  (The spins shard stays resident: the samples are the
+    rank's data, not a per-step input.)"""
     th = torch.from_numpy(theta_h).pin_memory()
     dth = torch.empty(theta_h.shape[0], dtype=torch.complex128).pin_memory()
-    theta = torch.empty(theta_h.shape[0], dtype=torch.complex128, device=dev)
+    theta = theta_graph if theta_graph is not None else torch.empty(theta_h.shape[0], dtype=torch.complex128,
+                                                                     device=dev)
 
     def one():
         theta.copy_(th, non_blocking=True)
-        d, _ = step.run(theta)
+        d, _ = step.replay() if theta_graph is not None else step.run(theta)
         dth.copy_(d, non_blocking=True)
         torch.cuda.synchronize(dev)
 
@@ -381,7 +389,8 @@ def run_e2e_sharded(torch, dist, step, theta_h, dev, args):
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     return {"value": args.steps / float(dt.item()), "unit": "steps/s", "h2d_bytes_per_step": int(th.numel() * 16),
             "d2h_bytes_per_step": int(dth.numel() * 16),
-            "api": "parallel.ShardedStep.run (C ABI + NCCL), pinned theta in, dtheta out, host-clock timed"}
+            "api": ("parallel.ShardedStep " + ("graph replay" if theta_graph is not None else "run") +
+                    " (C ABI + NCCL), pinned theta in, dtheta out, host-clock timed")}
 
 
 def run_e2e(sr, torch, w, theta_h, spins, ij, jj, dev, args):

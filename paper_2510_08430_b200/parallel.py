@@ -260,3 +260,17 @@ class ShardedStep:
         dist.all_reduce(b.dtheta, group=g)
         _rec(events, 5, st)
         return b.dtheta, b.energy
+
+    # --- CUDA graph of the whole sharded step, NCCL collectives included (they are captured
+    # as graph nodes; every rank captures the same sequence) ---
+    def capture(self, theta):
+        self.run(theta)
+        torch.cuda.synchronize(self.device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.run(theta)
+        return self.graph
+
+    def replay(self):
+        self.graph.replay()
+        return self.buf.dtheta, self.buf.energy

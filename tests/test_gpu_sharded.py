@@ -59,3 +59,29 @@ def test_sharded_step_matches_local_and_oracle(nccl_group, cfg, per_block):
         ref = solvers.block_solve(estimators.qgt_blocks(O, off), estimators.force(O, e), off, w.lam)
         got = d_shard.cpu().numpy()
         assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-9
+
+
+def test_sharded_step_graph_replay(nccl_group):
+    """The sharded step captured as one CUDA graph (NCCL collectives as graph nodes, as bench.py
+    times it) replays to the eager result, and follows a new theta."""
+    import paper_2510_08430_b200 as sr
+    from paper_2510_08430_b200 import parallel
+    w = workloads.CONFIGS[0]
+    spins, params = workloads.make_inputs(w)
+    ij, jj = sr.lattice.for_workload(w)
+    dev = torch.device("cuda:0")
+    theta = torch.from_numpy(sr.model.pack(params)).to(dev)
+    for per_block in (False, True):
+        shard = parallel.ShardedStep(w.widths, spins, ij, jj, w.lam, 0, 1, dev, per_block_gram=per_block)
+        d_eager = shard.run(theta)[0].clone()
+        shard.capture(theta)
+        d_graph = shard.replay()[0].clone()
+        torch.cuda.synchronize()
+        assert torch.equal(d_graph, d_eager)
+        theta.mul_(1.01)
+        d_new = shard.replay()[0].clone()
+        d_ref = parallel.ShardedStep(w.widths, spins, ij, jj, w.lam, 0, 1, dev,
+                                     per_block_gram=per_block).run(theta)[0]
+        torch.cuda.synchronize()
+        assert torch.equal(d_new, d_ref)
+        theta.div_(1.01)
