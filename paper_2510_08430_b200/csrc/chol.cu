@@ -262,9 +262,13 @@ int side_tm() {
 
 // Trailing-update lookahead (see solve_block); SR_LOOKAHEAD=0 turns it off, SR_TRAIL_B_TPC
 // sets the tiles per CTA of the off-chain part.
-bool lookahead() {
-  static const int v = env_int("SR_LOOKAHEAD", 0);   // measured 35.3 vs 34.6 ms at configs[1] (the GPU is full during the solve)
-  return v != 0;
+// Default: on for a single block (an owner's solve in the sharded step, the full-QGT and
+// NTK solves), where the chain leaves SMs idle (6480 block: graph 10.56 -> 10.07 ms with (b)
+// on 120 persistent CTAs; 16240: 94.4 -> 92.9 ms); off for several concurrent blocks, which
+// fill the GPU already (configs[1] step 35.3 vs 34.6 ms).
+bool lookahead(int nblocks) {
+  static const int v = env_int("SR_LOOKAHEAD", -1);
+  return v < 0 ? nblocks == 1 : v != 0;
 }
 int trail_b_tpc() {
   static const int v = std::max(1, env_int("SR_TRAIL_B_TPC", 2));
@@ -390,7 +394,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
       double2* trailing = B.Fm + (long long)pend * NB * B.npad + (long long)pend * NB;
       const long long K = (long long)(pend - p0) * NB;
       const long long look = (long long)kStrip * NB;   // the next strip's columns
-      if (i8 && lookahead() && m > look) {
+      if (i8 && lookahead(cs.count) && m > look) {
         // Lookahead: the chain needs only the next strip's columns (a), so the rest of the
         // trailing matrix (b) is updated on s4 (lowest priority, non-persistent grid) while
         // the next strip factors.  (b) reads the digit slices and writes columns beyond the
@@ -401,7 +405,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
         SR_CUDA(cudaEventRecord(Q.es, st));
         SR_TRY(oz::trail_apply_i8(m, K, trailing, B.npad, B.tws, 0, kStrip, trail_ctas(cs.count), st));
         SR_CUDA(cudaStreamWaitEvent(Q.s4, Q.es, 0));
-        static const int b_ctas = env_int("SR_TRAIL_B_CTAS", 0);   // > 0: persistent (b) on that many CTAs
+        static const int b_ctas = env_int("SR_TRAIL_B_CTAS", 120);   // > 0: persistent (b) on that many CTAs
         SR_TRY(oz::trail_apply_i8(m, K, trailing, B.npad, B.tws, look, 0, b_ctas > 0 ? b_ctas : -trail_b_tpc(), Q.s4));
         SR_CUDA(cudaEventRecord(Q.et, Q.s4));
         pending_b = true;
