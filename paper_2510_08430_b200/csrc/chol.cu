@@ -297,7 +297,7 @@ bool pdl_chain() {
 // waits on s2 -- s2's job(p-1) has two panel steps to finish before s3's job(p+1) needs it.
 struct BlockStreams {
   cudaStream_t s2, s3, s4;
-  cudaEvent_t ea, eb, ec, es, et;
+  cudaEvent_t ea, eb, ec, ed, es, et;
 };
 // Stagger of equal-size blocks (SR_STAGGER=k, k >= 1): block b starts once the previous
 // block of the same size has factored k panels, so their strip-end trailing updates (full-
@@ -361,8 +361,13 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
       timer_begin("chol_inner", st);
       if (side) SR_TRY((gram::launch_skinny<gram::SUB>(next_tile, st, pdl_chain())));
       timer_end(st);
+      // The off-chain jobs start after the next-tile update, so the next chol_diag is already
+      // pending (at the chain's higher priority) when their CTAs flood the SMs.
+      static const bool after_next = env_int("SR_SIDE_AFTER_NEXT", 1) != 0;
+      const cudaEvent_t side_go = after_next ? Q.ed : Q.ea;
+      if (side && after_next) SR_CUDA(cudaEventRecord(Q.ed, st));
       if (side && next_rows.count) {
-        SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.ea, 0));
+        SR_CUDA(cudaStreamWaitEvent(Q.s3, side_go, 0));
         if (p > p0) SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.eb, 0));
         timer_begin("chol_next_rows", Q.s3);
         if (inner_tiles()) SR_TRY((gram::launch<gram::NH, gram::SUB>(next_rows, Q.s3)));
@@ -372,7 +377,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
         SR_CUDA(cudaEventRecord(Q.ec, Q.s3));
       }
       if (inner_rest.count) {
-        SR_CUDA(cudaStreamWaitEvent(Q.s2, Q.ea, 0));
+        SR_CUDA(cudaStreamWaitEvent(Q.s2, side_go, 0));
         timer_begin("chol_inner_rest", Q.s2);
         if (inner_tiles()) SR_TRY((gram::launch<gram::NH, gram::SUB>(inner_rest, Q.s2)));
         else if (side_tm() == 32) SR_TRY((gram::launch_skinny<gram::SUB, 32>(inner_rest, Q.s2)));
@@ -465,6 +470,7 @@ sr_status side_pool(SidePool*& out) {
       SR_CUDA(cudaStreamCreateWithPriority(&q.s3, cudaStreamNonBlocking, side_prio ? std::min(lo, hi + 1) : hi));
       SR_CUDA(cudaStreamCreateWithPriority(&q.s4, cudaStreamNonBlocking, lo));
       SR_CUDA(cudaEventCreateWithFlags(&q.es, cudaEventDisableTiming));
+      SR_CUDA(cudaEventCreateWithFlags(&q.ed, cudaEventDisableTiming));
       SR_CUDA(cudaEventCreateWithFlags(&q.et, cudaEventDisableTiming));
       SR_CUDA(cudaEventCreateWithFlags(&pool.join[i], cudaEventDisableTiming));
       SR_CUDA(cudaEventCreateWithFlags(&pool.stag[i], cudaEventDisableTiming));

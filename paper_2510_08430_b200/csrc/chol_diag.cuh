@@ -25,11 +25,12 @@ constexpr int NB = 64;
 // Phase timings: tools/diag_probe.cu (66.9k cycles for the first scalar-FP64 version,
 // 50.1k with the DMMA SYRK and inverse levels).
 constexpr int LDT = NB + 1;   // 1040-byte rows
-constexpr size_t kDiagSmem = ((size_t)2 * NB * LDT + 32 * 33) * sizeof(double2);   // T, X, W
+// T and X (the inverse's scratch W lives in T's unused strict upper triangle): 130 KB, so
+// a diagonal tile fits on an SM beside one 87 KB skinny CTA of the off-chain updates
+constexpr size_t kDiagSmem = (size_t)2 * NB * LDT * sizeof(double2);
 
 // 8x8 complex tile on DMMA: C += sum_{k in [k0, k1)} A[r][k] B[k][c] for r, c < 8, with A and
 // B row-major in shared memory (k0, k1 multiples of 4).  Lane l holds C[l/4][2(l%4) + {0,1}].
-constexpr int LDW = 33;
 __device__ __forceinline__ void dmma_t(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
@@ -240,15 +241,15 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
   SR_DIAG_PROBE(2);
   if (t == 0 && bad && info) atomicCAS(info, 0, (int)(B.row_base + (long long)p * NB + bad));
   {   // 8 -> 16: X21 = -X22 (L21 X11) inside each 16-block (warps 0-3, one block each)
-    double2* W = dsm + 2 * NB * LDT;
+    double2* W = T + 32;   // scratch in T's unused strict upper triangle (rows 0-31, cols 32-63)
     if (warp < 4) {
       const int o = 16 * warp;
       double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
       tile_mma(T + (o + 8) * LDT + o, LDT, X + o * LDT + o, LDT, 0, 8, lane, cr, ci);
-      tile_put(W + 8 * warp * LDW, LDW, lane, cr, ci, 1.0);
+      tile_put(W + 8 * warp * LDT, LDT, lane, cr, ci, 1.0);
       __syncwarp();
       cr[0] = cr[1] = ci[0] = ci[1] = 0.0;
-      tile_mma(X + (o + 8) * LDT + o + 8, LDT, W + 8 * warp * LDW, LDW, 0, 8, lane, cr, ci);
+      tile_mma(X + (o + 8) * LDT + o + 8, LDT, W + 8 * warp * LDT, LDT, 0, 8, lane, cr, ci);
       tile_put(X + (o + 8) * LDT + o, LDT, lane, cr, ci, -1.0);
     }
     __syncthreads();
@@ -261,15 +262,15 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
   // the 16-blocks (the level above), so a tile's K range starts at its column (L X) or ends
   // at its row (X W).
   {
-    double2* W = dsm + 2 * NB * LDT;   // [32][LDW] scratch product
+    double2* W = T + 32;   // [32][LDT] scratch product in T's unused strict upper triangle
     {   // 16 -> 32: W' = L21' X11' (rows 32b+16.., cols 32b..), X21' = -X22' W'
       const int bb = warp >> 2, ti = (warp >> 1) & 1, tj = warp & 1, o = 32 * bb;
       double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
       tile_mma(T + (o + 16 + 8 * ti) * LDT + o, LDT, X + o * LDT + o + 8 * tj, LDT, 8 * tj, 16, lane, cr, ci);
-      tile_put(W + (16 * bb + 8 * ti) * LDW + 8 * tj, LDW, lane, cr, ci, 1.0);
+      tile_put(W + (16 * bb + 8 * ti) * LDT + 8 * tj, LDT, lane, cr, ci, 1.0);
       __syncthreads();
       cr[0] = cr[1] = ci[0] = ci[1] = 0.0;
-      tile_mma(X + (o + 16 + 8 * ti) * LDT + o + 16, LDT, W + 16 * bb * LDW + 8 * tj, LDW, 0, 8 * ti + 8, lane, cr, ci);
+      tile_mma(X + (o + 16 + 8 * ti) * LDT + o + 16, LDT, W + 16 * bb * LDT + 8 * tj, LDT, 0, 8 * ti + 8, lane, cr, ci);
       tile_put(X + (o + 16 + 8 * ti) * LDT + o + 8 * tj, LDT, lane, cr, ci, -1.0);
       __syncthreads();
     }
@@ -280,14 +281,14 @@ __global__ void __launch_bounds__(256) chol_diag(const CholBlock B, int* info, i
         const int tj = 2 * (warp & 1) + h;
         double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
         tile_mma(T + (32 + 8 * ti) * LDT, LDT, X + 8 * tj, LDT, 8 * tj, 32, lane, cr, ci);
-        tile_put(W + 8 * ti * LDW + 8 * tj, LDW, lane, cr, ci, 1.0);
+        tile_put(W + 8 * ti * LDT + 8 * tj, LDT, lane, cr, ci, 1.0);
       }
       __syncthreads();
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const int tj = 2 * (warp & 1) + h;
         double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
-        tile_mma(X + (32 + 8 * ti) * LDT + 32, LDT, W + 8 * tj, LDW, 0, 8 * ti + 8, lane, cr, ci);
+        tile_mma(X + (32 + 8 * ti) * LDT + 32, LDT, W + 8 * tj, LDT, 0, 8 * ti + 8, lane, cr, ci);
         tile_put(X + (32 + 8 * ti) * LDT + 8 * tj, LDT, lane, cr, ci, -1.0);
       }
       __syncthreads();

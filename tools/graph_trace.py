@@ -13,13 +13,44 @@ import paper_2510_08430_b200 as sr  # noqa: E402
 from paper_2510_08430_b200 import parallel  # noqa: E402
 import workloads  # noqa: E402
 
-w = workloads.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 1]
+arg = sys.argv[1] if len(sys.argv) > 1 else "1"
 out = sys.argv[2] if len(sys.argv) > 2 else None
 dev = torch.device("cuda:0")
-spins, params = workloads.make_inputs(w)
-ij, jj = sr.lattice.for_workload(w)
-step = parallel.LocalStep(w.widths, spins, ij, jj, w.lam, dev)
-theta = torch.from_numpy(sr.model.pack(params)).to(dev)
+if arg.startswith("solve"):   # solve-only graph of one block of the given size, e.g. solve6480
+    import numpy as np
+
+    class _SolveOnly:
+        def __init__(self, n):
+            g = torch.Generator(device=dev).manual_seed(0)
+            A = torch.randn(4096, n, dtype=torch.complex128, device=dev, generator=g) / 64.0
+            self.S = torch.empty(n * n, dtype=torch.complex128, device=dev)
+            sr.sr_block_qgt_i8(A, [0, n], self.S)
+            self.F = torch.randn(n, dtype=torch.complex128, device=dev, generator=g)
+            self.d = torch.empty_like(self.F)
+            self.n = n
+
+        def run(self):
+            sr.sr_block_solve([0, self.n], self.S, self.F, 1e-3, self.d)
+
+        def capture(self, _theta):
+            self.run()
+            torch.cuda.synchronize()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                self.run()
+
+        def replay(self):
+            self.graph.replay()
+
+    w = workloads.CONFIGS[1]
+    step = _SolveOnly(int(arg[5:]))
+    theta = None
+else:
+    w = workloads.CONFIGS[int(arg)]
+    spins, params = workloads.make_inputs(w)
+    ij, jj = sr.lattice.for_workload(w)
+    step = parallel.LocalStep(w.widths, spins, ij, jj, w.lam, dev)
+    theta = torch.from_numpy(sr.model.pack(params)).to(dev)
 step.capture(theta)
 for _ in range(3):
     step.replay()
