@@ -263,6 +263,7 @@ def run_gpu(args):
     if sharded:
         e2e = run_e2e_sharded(torch, dist, step, theta_h, dev, args, theta if use_graph else None)
     else:
+        comparison = None if args.no_compare else compare_solves(sr, torch, step, w, dev)
         del step                      # the e2e run allocates its own sr_step workspace
         torch.cuda.empty_cache()
         e2e = run_e2e(sr, torch, w, theta_h, spins_all, ij, jj, dev, args)
@@ -355,11 +356,55 @@ def run_gpu(args):
         "clocks": clk,
         "e2e": e2e,
     }
+    if not sharded and comparison is not None:
+        rec["comparison_solves"] = comparison
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rec["cpu_baseline"] = cpu_baseline(w)
     print(json.dumps(rec), flush=True)
     if sharded:
         dist.destroy_process_group()
+
+
+def compare_solves(sr, torch, step, w, dev, max_gb=40.0):
+    """The comparison paths of north_star on the step's own centred Jacobian A, force F and
+    residuals e: block QGT + block solve (the method), the full-QGT solve and the
+    sample-space NTK solve (§1-2), each timed once eagerly with CUDA events after a
+    warm call; reports how far the block update is from the full one, and the push-through
+    identity (full == NTK) on real data.  Skipped when the full QGT would not fit."""
+    b = step.buf
+    lib = sr.load()
+    need = lib.sr_full_qgt_solve_workspace_bytes(b.O.shape[0], b.n_p) / 1e9
+    if need > max_gb:
+        return {"skipped": f"full-QGT workspace {need:.0f} GB > {max_gb:.0f} GB"}
+    d_full = torch.empty_like(b.dtheta)
+    d_ntk = torch.empty_like(b.dtheta)
+    ws_full = torch.empty(lib.sr_full_qgt_solve_workspace_bytes(b.O.shape[0], b.n_p), dtype=torch.uint8, device=dev)
+    ws_ntk = torch.empty(lib.sr_ntk_solve_workspace_bytes(b.O.shape[0], b.n_p), dtype=torch.uint8, device=dev)
+    calls = {
+        "block_qgt+block_solve": lambda: (step.ops.block_qgt(b.O, b.offs, b.S),
+                                          step.ops.block_solve(b.offs, b.S, b.F, w.lam, b.dtheta)),
+        "full_qgt_solve": lambda: sr.sr_full_qgt_solve(b.O, b.F, w.lam, d_full, workspace=ws_full),
+        "ntk_solve": lambda: sr.sr_ntk_solve(b.O, b.e_tilde, w.lam, d_ntk, workspace=ws_ntk),
+    }
+    ms = {}
+    for name, fn in calls.items():
+        fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms[name] = e0.elapsed_time(e1)
+    nrm = lambda x: float(torch.linalg.vector_norm(x).item())   # noqa: E731
+    out = {"ms": ms,
+           "rel_l2_full_vs_ntk": nrm(d_full - d_ntk) / nrm(d_full),
+           "rel_l2_block_vs_full": nrm(b.dtheta - d_full) / nrm(d_full),
+           "sizes": {"full_qgt": b.n_p, "ntk": int(b.O.shape[0]), "blocks": [int(x) for x in block_sizes(w)]},
+           "note": "eager, one timed call each after a warm call; A, F, e from the step above"}
+    del ws_full, ws_ntk
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_e2e_sharded(torch, dist, step, theta_h, dev, args, theta_graph=None):
@@ -507,6 +552,7 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=list(workloads.BY_NAME))
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-compare", action="store_true", help="skip the full-QGT / NTK comparison solves")
     ap.add_argument("--no-graph", action="store_true", help="launch stage by stage instead of one CUDA graph")
     ap.add_argument("--sharded", action="store_true",
                     help="run the sample-sharded NCCL step even on one rank (tests the multi-GPU path)")
