@@ -560,14 +560,21 @@ SR_API sr_status sr_block_solve(int n_blocks, const int64_t* block_offsets, cons
                           workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
+// The comparison solves' Grams run on the selected engine (sr_set_gram_engine); the int8
+// engine's digit slices follow the Cholesky workspace.
+size_t full_i8_ws(long long ns, long long n_p) {
+  if (ns < 1) return 0;
+  const int64_t o[2] = {0, n_p};
+  return oz::workspace_bytes(ns, 1, o);
+}
+
 SR_API size_t sr_full_qgt_solve_workspace_bytes(int64_t n_samples, int64_t n_p) {
-  (void)n_samples;
-  if (n_p < 1) return 0;
+  if (n_p < 1 || n_samples < 0) return 0;
   long long sz = n_p;
   Arena a(nullptr, 0);
   CholSet cs{};
   carve_chol(a, cs, &sz, 1);
-  return a.used;
+  return round256(a.used) + full_i8_ws(n_samples, n_p);
 }
 
 SR_API sr_status sr_full_qgt_solve(int64_t n_samples, int64_t n_p, const double* A, int64_t lda, const double* F,
@@ -589,9 +596,16 @@ SR_API sr_status sr_full_qgt_solve(int64_t n_samples, int64_t n_p, const double*
   }
   CholBlock& B = cs.b[0];
   const double2* Ad = reinterpret_cast<const double2*>(A);
-  gram::ProbSet ps{};
-  gram::add_prob(ps, Ad, lda, Ad, lda, B.Fm, B.npad, (int)n_p, (int)n_p, n_samples, true);
-  SR_TRY((gram::launch<gram::TN, gram::HERM_STORE>(ps, st)));
+  if (g_gram_engine == SR_GRAM_INT8 && n_samples > 0) {   // S straight into the padded factor matrix
+    const size_t used = round256(a.used);
+    const int64_t o[2] = {0, n_p};
+    SR_TRY(oz::block_qgt_i8(n_samples, 1, o, Ad, lda, B.Fm, static_cast<char*>(workspace) + used,
+                            workspace_bytes > used ? workspace_bytes - used : 0, st, B.npad));
+  } else {
+    gram::ProbSet ps{};
+    gram::add_prob(ps, Ad, lda, Ad, lda, B.Fm, B.npad, (int)n_p, (int)n_p, n_samples, true);
+    SR_TRY((gram::launch<gram::TN, gram::HERM_STORE>(ps, st)));
+  }
   if (S_out) SR_TRY(copy_matrix(B.Fm, B.npad, reinterpret_cast<double2*>(S_out), n_p, n_p, n_p, st));
   B.F = reinterpret_cast<const double2*>(F);
   B.out = reinterpret_cast<double2*>(dtheta);
@@ -605,7 +619,7 @@ SR_API size_t sr_ntk_solve_workspace_bytes(int64_t n_samples, int64_t n_p) {
   CholSet cs{};
   carve_chol(a, cs, &sz, 1);
   a.take<double2>(n_samples);
-  return a.used + aHv_ws(n_samples, n_p);
+  return a.used + std::max(aHv_ws(n_samples, n_p), round256(oz::rows_workspace_bytes(n_samples, n_p)));
 }
 
 SR_API sr_status sr_ntk_solve(int64_t n_samples, int64_t n_p, const double* A, int64_t lda, const double* e_tilde,
@@ -629,9 +643,13 @@ SR_API sr_status sr_ntk_solve(int64_t n_samples, int64_t n_p, const double* A, i
   }
   CholBlock& B = cs.b[0];
   const double2* Ad = reinterpret_cast<const double2*>(A);
-  gram::ProbSet ps{};
-  gram::add_prob(ps, Ad, lda, Ad, lda, B.Fm, B.npad, (int)n_samples, (int)n_samples, n_p, true);
-  SR_TRY((gram::launch<gram::NH, gram::HERM_STORE>(ps, st)));
+  if (g_gram_engine == SR_GRAM_INT8) {   // T = A A^H on the int8 engine (rows split), scratch after y
+    SR_TRY(oz::gram_rows_i8(Ad, lda, n_samples, n_p, B.Fm, B.npad, a.base + a.used, rest, st));
+  } else {
+    gram::ProbSet ps{};
+    gram::add_prob(ps, Ad, lda, Ad, lda, B.Fm, B.npad, (int)n_samples, (int)n_samples, n_p, true);
+    SR_TRY((gram::launch<gram::NH, gram::HERM_STORE>(ps, st)));
+  }
   if (T_out)
     SR_TRY(copy_matrix(B.Fm, B.npad, reinterpret_cast<double2*>(T_out), n_samples, n_samples, n_samples, st));
   B.F = reinterpret_cast<const double2*>(e_tilde);

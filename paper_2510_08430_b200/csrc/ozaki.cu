@@ -982,7 +982,7 @@ long long gram_ctas() {
 }
 
 sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double2* A, long long lda, double2* S,
-                       void* ws, size_t ws_bytes, cudaStream_t st) {
+                       void* ws, size_t ws_bytes, cudaStream_t st, long long ldc) {
   long long s_total = 0;
   for (int b = 0; b < nblk; b++) s_total += (offs[b + 1] - offs[b]) * (offs[b + 1] - offs[b]);
   if (ns == 0) {   // empty batch: S = 0, nothing read
@@ -1034,7 +1034,7 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
       B.n = (int)(offs[b + 1] - offs[b]);
       B.col0 = offs[b] - c0;
       B.C = S + soff;
-      B.ldc = B.n;
+      B.ldc = ldc > 0 ? ldc : B.n;   // ldc > 0: one block written with that leading dimension
       soff += (long long)B.n * B.n;
       B.RT = (B.n + R * BN - 1) / (R * BN);
       B.CT = (B.n + BN - 1) / BN;
@@ -1132,6 +1132,54 @@ sr_status trail_update_i8(const double2* L, long long ldl, long long m, long lon
   if (m <= 0 || K <= 0) return SR_OK;
   SR_TRY(trail_split_i8(L, ldl, m, K, ws, ws_bytes, st));
   return trail_apply_i8(m, K, C, ldc, ws, 0, 0, max_ctas, st);
+}
+
+size_t rows_workspace_bytes(long long m, long long K) { return trail_workspace_bytes(m, K); }
+
+sr_status gram_rows_i8(const double2* L, long long ldl, long long m, long long K, double2* C, long long ldc, void* ws,
+                       size_t ws_bytes, cudaStream_t st) {
+  if (m <= 0) return SR_OK;
+  if (K <= 0 || m >= (1LL << 31) / kSlices) {
+    set_error("gram_rows_i8: bad sizes");
+    return SR_ERR_INVALID;
+  }
+  if (ws_bytes < rows_workspace_bytes(m, K) || !ws) {
+    set_error("gram_rows_i8: workspace too small");
+    return SR_ERR_WORKSPACE;
+  }
+  SR_TRY(set_attrs());
+  const long long Kp = pad_k(K);
+  Arena a(ws, ws_bytes);
+  int8_t* E = a.take<int8_t>((size_t)kSlices * 3 * Kp * m);
+  int* expo = a.take<int>(m);
+  // rows scaled and split with the imaginary part negated (as for the trailing updates), so
+  // the column-Gram of the split is sum_k L[i][k] conj(L[j][k])
+  oz_split_rows<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(L, ldl, (int)m, (int)K, (int)Kp, E, expo);
+  SR_LAUNCHED();
+  Params P{};
+  P.nblk = 1;
+  P.Kp = Kp;
+  P.kstages = (int)(2 * Kp / BKB);
+  P.spc = kChunkK / BKB;
+  P.expo = expo;
+  Blk& B = P.b[0];
+  B.col0 = 0;
+  B.C = C;
+  B.ldc = ldc;
+  B.n = (int)m;
+  B.RT = (B.n + BM - 1) / BM;
+  B.CT = (B.n + BN - 1) / BN;
+  B.tile_begin = 0;
+  P.total_tiles = 2 * lower_tiles(B.n);
+  CUtensorMap ma, mb;
+  SR_TRY(make_map(ma, E, Kp, m, BM));
+  SR_TRY(make_map(mb, E, Kp, m, BN));
+  const unsigned grid = (unsigned)std::min<long long>(P.total_tiles, kNumSMs);
+  timer_begin("gram_i8", st);
+  gram_i8<MODE_HERM><<<grid, kThreads, kSmem, st>>>(ma, mb, P);
+  timer_end(st);
+  SR_LAUNCHED();
+  return SR_OK;
 }
 
 }  // namespace oz

@@ -14,7 +14,16 @@ size_t workspace_bytes(long long ns, int nblk, const int64_t* offs);
 // digit slices of the column-scaled A with tcgen05 kind::i8 MMAs accumulated exactly in
 // TMEM (int32) and recombined in FP64.
 sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double2* A, long long lda, double2* S,
-                       void* ws, size_t ws_bytes, cudaStream_t st);
+                       void* ws, size_t ws_bytes, cudaStream_t st, long long ldc = 0);
+// (ldc > 0, one block: the result is written with that leading dimension, e.g. straight into
+// a padded Cholesky matrix -- the full-QGT solve.)
+
+// T = L L^H (both triangles, real diagonal) for the m rows of L (m x K, row-major, ld ldl),
+// written with leading dimension ldc: the NTK Gram A A^H of the sample-space solve.  Rows are
+// scaled and split like the trailing updates' L; any K (chunked exact accumulation).
+size_t rows_workspace_bytes(long long m, long long K);
+sr_status gram_rows_i8(const double2* L, long long ldl, long long m, long long K, double2* C, long long ldc, void* ws,
+                       size_t ws_bytes, cudaStream_t st);
 
 // Cholesky trailing update C[i][j] -= sum_k L[i][k] conj(L[j][k]) for i >= j < m (lower
 // triangle only; C row-major with leading dimension ldc, L row-major along k with ldl),
