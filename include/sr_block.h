@@ -203,9 +203,10 @@ SR_API sr_status sr_block_qgt_i8(int64_t n_samples, int n_blocks,
                                  const int64_t* block_offsets /*host*/, const double* A, int64_t lda,
                                  double* S, void* workspace, size_t workspace_bytes, void* stream);
 
-/* sr_set_gram_engine — engine of the dense contractions: sr_step's stage (4) and the
- * deferred trailing updates (A_22 -= L_21 L_21^H, K = 512) of every Cholesky
- * factorisation (sr_block_solve, sr_full_qgt_solve, sr_ntk_solve, sr_step).
+/* sr_set_gram_engine — engine of the dense contractions: sr_step's stage (4), the Grams of
+ * the comparison solves (the full QGT A^H A of sr_full_qgt_solve, the NTK A A^H of
+ * sr_ntk_solve) and the deferred trailing updates (A_22 -= L_21 L_21^H, K = 512) of every
+ * Cholesky factorisation (sr_block_solve, sr_full_qgt_solve, sr_ntk_solve, sr_step).
  * SR_GRAM_FP64 = FP64 DMMA tensor cores (sr_block_qgt), SR_GRAM_INT8 = int8 tcgen05 digit
  * slices (sr_block_qgt_i8; for the trailing updates the rows of each L_21 strip are
  * scaled and split the same way).  Process-wide; returns the previous setting, or -1 for
