@@ -119,7 +119,7 @@ def block_owner(b, world, sizes=None):
 
 
 class _Buffers:
-    def __init__(self, widths, spins, bij, bj, device):
+    def __init__(self, widths, spins, bij, bj, device, full_s=True):
         c = torch.complex128
         self.widths = list(widths)
         self.n_p = sr.n_params(widths)
@@ -135,7 +135,7 @@ class _Buffers:
         self.e_tilde = torch.empty(ns, dtype=c, device=device)
         self.F = torch.empty(self.n_p, dtype=c, device=device)
         n_s = sum((self.offs[b + 1] - self.offs[b]) ** 2 for b in range(len(self.offs) - 1))
-        self.S = torch.empty(n_s, dtype=c, device=device)
+        self.S = torch.empty(n_s, dtype=c, device=device) if full_s else None
         self.dtheta = torch.empty(self.n_p, dtype=c, device=device)
 
     def s_block(self, b):
@@ -207,12 +207,20 @@ class ShardedStep:
         self.n_total = spins_all.shape[0]
         lo, hi = shard_range(self.n_total, rank, world)
         self.device = torch.device(device)
-        self.buf = _Buffers(widths, spins_all[lo:hi], bij, bj, self.device)
+        # per-block launches keep only the owned blocks of S plus one or two staging buffers
+        # for the partials that travel (configs[4] at 8 ranks: 32 GB instead of 79 GB of S)
+        self.buf = _Buffers(widths, spins_all[lo:hi], bij, bj, self.device, full_s=not self.per_block_gram)
         offs = sr.block_offsets(widths)
         self.sizes = [offs[b + 1] - offs[b] for b in range(len(offs) - 1)]
         self.ranges = block_ranges(self.sizes, world)
         olo, ohi = self.ranges[rank]
         self.own_offs = [offs[b] - offs[olo] for b in range(olo, ohi + 1)] if ohi > olo else None
+        if self.per_block_gram:
+            c = torch.complex128
+            self.S_own = torch.empty(max(1, sum(n * n for n in self.sizes[olo:ohi])), dtype=c, device=self.device)
+            others = [n * n for b, n in enumerate(self.sizes) if not olo <= b < ohi]
+            self.staging = [torch.empty(max(others), dtype=c, device=self.device)
+                            for _ in range(min(2, len(others)))] if others else []
         self.ops = ops or CudaOps(widths, hi - lo, len(bj), self.device, gram_engine, solve_offsets=self.own_offs)
         self.moments = torch.empty(2 * self.buf.n_p + 2, dtype=torch.complex128, device=self.device)
         self.moments_all = torch.empty(world, 2 * self.buf.n_p + 2, dtype=torch.complex128, device=self.device)
@@ -240,12 +248,26 @@ class ShardedStep:
             works = [dist.reduce(b.s_block(blk), dst=block_owner(blk, self.world, self.sizes), group=g,
                                  async_op=True) for blk in range(nblk)]
         else:
-            works = []
+            works, pending, k = [], [None, None], 0
+            olo = self.ranges[self.rank][0]
             for blk in range(nblk):
                 lo, hi = b.offs[blk], b.offs[blk + 1]
-                o.block_qgt(b.O[:, lo:hi], [0, hi - lo], b.s_block(blk))
-                works.append(dist.reduce(b.s_block(blk), dst=block_owner(blk, self.world, self.sizes), group=g,
-                                         async_op=True))
+                n = hi - lo
+                owner = block_owner(blk, self.world, self.sizes)
+                if owner == self.rank:   # the reduce lands in place in the owned slot
+                    pos = sum(m * m for m in self.sizes[olo:blk])
+                    target = self.S_own[pos:pos + n * n]
+                else:                    # a staging buffer whose previous reduce has completed
+                    j = k % len(self.staging)
+                    k += 1
+                    if pending[j] is not None:
+                        pending[j].wait()
+                    target = self.staging[j][:n * n]
+                o.block_qgt(b.O[:, lo:hi], [0, n], target)
+                wk = dist.reduce(target, dst=owner, group=g, async_op=True)
+                if owner != self.rank:
+                    pending[j] = wk
+                works.append(wk)
         for wk in works:
             wk.wait()
         f_work.wait()
@@ -254,9 +276,13 @@ class ShardedStep:
         if self.owned:   # this rank's contiguous blocks in one call (concurrent streams)
             olo, ohi = self.owned[0], self.owned[-1] + 1
             lo, hi = b.offs[olo], b.offs[ohi]
-            spos = sum(n * n for n in self.sizes[:olo])
             slen = sum(n * n for n in self.sizes[olo:ohi])
-            o.block_solve(self.own_offs, b.S[spos:spos + slen], b.F[lo:hi], self.lam, b.dtheta[lo:hi])
+            if self.per_block_gram:
+                s_own = self.S_own[:slen]
+            else:
+                spos = sum(n * n for n in self.sizes[:olo])
+                s_own = b.S[spos:spos + slen]
+            o.block_solve(self.own_offs, s_own, b.F[lo:hi], self.lam, b.dtheta[lo:hi])
         dist.all_reduce(b.dtheta, group=g)
         _rec(events, 5, st)
         return b.dtheta, b.energy
