@@ -247,17 +247,10 @@ int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-// Off-chain in-strip updates (s2 / s3 jobs) on 64x64-tile CTAs (the FP64 engine's
-// tile_kernel, weights of B amortised over 64 rows) instead of the 16-row skinny kernel;
-// SR_INNER_TILES=0/1.
-bool inner_tiles() {
-  static const int v = env_int("SR_INNER_TILES", 0);
+// Split TRSM (see solve_block); SR_TRSM_SPLIT=0 restores the whole TRSM on the chain.
+bool trsm_split() {
+  static const int v = env_int("SR_TRSM_SPLIT", 1);
   return v != 0;
-}
-
-int side_tm() {
-  static const int v = env_int("SR_SIDE_TM", 16);
-  return v;
 }
 
 // Trailing-update lookahead (see solve_block); SR_LOOKAHEAD=0 turns it off, SR_TRAIL_B_TPC
@@ -297,7 +290,7 @@ bool pdl_chain() {
 // waits on s2 -- s2's job(p-1) has two panel steps to finish before s3's job(p+1) needs it.
 struct BlockStreams {
   cudaStream_t s2, s3, s4;
-  cudaEvent_t ea, eb, ec, ed, es, et;
+  cudaEvent_t ea, eb, ec, ed, er, es, et;
 };
 // Stagger of equal-size blocks (SR_STAGGER=k, k >= 1): block b starts once the previous
 // block of the same size has factored k panels, so their strip-end trailing updates (full-
@@ -334,9 +327,19 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
       if (p > p0) SR_CUDA(cudaStreamWaitEvent(st, Q.ec, 0));
       const long long m = B.npad - (long long)(p + 1) * NB;
       if (m <= 0) continue;
-      gram::ProbSet trsm{}, next_tile{}, next_rows{}, inner_rest{};
+      gram::ProbSet trsm{}, trsm_rest{}, next_tile{}, next_rows{}, inner_rest{};
       double2* panel = B.Fm + (long long)(p + 1) * NB * B.npad + (long long)p * NB;
-      gram::add_prob(trsm, panel, B.npad, B.linv + (long long)p * NB * NB, NB, panel, B.npad, (int)m, NB, NB, false);
+      const double2* linv_p = B.linv + (long long)p * NB * NB;
+      // Split TRSM: the chain solves only the next panel's row block (all that the next-tile
+      // update and chol_diag(p+1) read); the rows below go to s3 ahead of its update job.
+      const bool split = trsm_split() && p + 1 < pend && m > NB;
+      if (split) {
+        gram::add_prob(trsm, panel, B.npad, linv_p, NB, panel, B.npad, NB, NB, NB, false);
+        gram::add_prob(trsm_rest, panel + (long long)NB * B.npad, B.npad, linv_p, NB, panel + (long long)NB * B.npad,
+                       B.npad, (int)(m - NB), NB, NB, false);
+      } else {
+        gram::add_prob(trsm, panel, B.npad, linv_p, NB, panel, B.npad, (int)m, NB, NB, false);
+      }
       for (int jj = p + 1; jj < pend; jj++) {   // later columns of the strip, rows i >= jj
         const double2* lrows = B.Fm + (long long)jj * NB * B.npad + (long long)p * NB;
         double2* cblk = B.Fm + (long long)jj * NB * B.npad + (long long)jj * NB;
@@ -369,19 +372,22 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
       if (side && next_rows.count) {
         SR_CUDA(cudaStreamWaitEvent(Q.s3, side_go, 0));
         if (p > p0) SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.eb, 0));
+        if (split) {
+          timer_begin("chol_trsm_rest", Q.s3);
+          SR_TRY((gram::launch_skinny<gram::STORE>(trsm_rest, Q.s3)));
+          timer_end(Q.s3);
+          SR_CUDA(cudaEventRecord(Q.er, Q.s3));   // all of L column p: the s2 job may start
+        }
         timer_begin("chol_next_rows", Q.s3);
-        if (inner_tiles()) SR_TRY((gram::launch<gram::NH, gram::SUB>(next_rows, Q.s3)));
-        else if (side_tm() == 32) SR_TRY((gram::launch_skinny<gram::SUB, 32>(next_rows, Q.s3)));
-        else SR_TRY((gram::launch_skinny<gram::SUB>(next_rows, Q.s3)));
+        SR_TRY((gram::launch_skinny<gram::SUB>(next_rows, Q.s3)));
         timer_end(Q.s3);
         SR_CUDA(cudaEventRecord(Q.ec, Q.s3));
       }
       if (inner_rest.count) {
         SR_CUDA(cudaStreamWaitEvent(Q.s2, side_go, 0));
+        if (split) SR_CUDA(cudaStreamWaitEvent(Q.s2, Q.er, 0));
         timer_begin("chol_inner_rest", Q.s2);
-        if (inner_tiles()) SR_TRY((gram::launch<gram::NH, gram::SUB>(inner_rest, Q.s2)));
-        else if (side_tm() == 32) SR_TRY((gram::launch_skinny<gram::SUB, 32>(inner_rest, Q.s2)));
-        else SR_TRY((gram::launch_skinny<gram::SUB>(inner_rest, Q.s2)));
+        SR_TRY((gram::launch_skinny<gram::SUB>(inner_rest, Q.s2)));
         timer_end(Q.s2);
         SR_CUDA(cudaEventRecord(Q.eb, Q.s2));
       }
@@ -471,6 +477,7 @@ sr_status side_pool(SidePool*& out) {
       SR_CUDA(cudaStreamCreateWithPriority(&q.s4, cudaStreamNonBlocking, lo));
       SR_CUDA(cudaEventCreateWithFlags(&q.es, cudaEventDisableTiming));
       SR_CUDA(cudaEventCreateWithFlags(&q.ed, cudaEventDisableTiming));
+      SR_CUDA(cudaEventCreateWithFlags(&q.er, cudaEventDisableTiming));
       SR_CUDA(cudaEventCreateWithFlags(&q.et, cudaEventDisableTiming));
       SR_CUDA(cudaEventCreateWithFlags(&pool.join[i], cudaEventDisableTiming));
       SR_CUDA(cudaEventCreateWithFlags(&pool.stag[i], cudaEventDisableTiming));
