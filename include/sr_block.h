@@ -106,6 +106,21 @@ SR_API size_t sr_kernel_timeline(char* buf, size_t bytes);
  * must outlive every launch made while it is installed. */
 SR_API sr_status sr_trace_buffer(void* records, int64_t capacity);
 
+/* sr_graph_capture_begin / sr_graph_capture_end / sr_graph_launch / sr_graph_destroy —
+ * CUDA-graph capture of any sequence of the calls above, instantiated with per-node
+ * priorities (cudaGraphInstantiateFlagUseNodePriority) so that the blocked solves' panel
+ * chain keeps its higher stream priority over the off-chain updates inside the graph (a
+ * graph instantiated without the flag runs every node at the priority of the stream it is
+ * launched into).  begin: `stream` must be a non-default stream; the calls that follow on
+ * it (and on the side streams they fork) are recorded, not run.  end: *graph_exec receives
+ * an opaque executable graph owned by the caller (sr_graph_destroy frees it).  launch: runs
+ * it on `stream`; the buffers and the workspace captured must still be valid.  Errors as
+ * above (capture failures surface as SR_ERR_CUDA from end). */
+SR_API sr_status sr_graph_capture_begin(void* stream);
+SR_API sr_status sr_graph_capture_end(void* stream, void** graph_exec);
+SR_API sr_status sr_graph_launch(void* graph_exec, void* stream);
+SR_API sr_status sr_graph_destroy(void* graph_exec);
+
 /* ---------------------------------------------------------------- stage (1) ---
  * sr_jacobian — PAPER.md §2 Eq. 2 "O_i(x) = d_{theta_i} log psi_theta(x)".
  *   theta    complex [n_p]                       network parameters (layout above)

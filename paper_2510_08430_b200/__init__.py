@@ -12,5 +12,6 @@ from ._lib import (  # noqa: F401
     sr_block_solve, sr_full_qgt_solve, sr_ntk_solve,
     sr_step, sr_step_host, sr_step_workspace_bytes, sr_step_s_offset, sr_step_host_extra_bytes,
     sr_launch_count, sr_reset_launch_count, sr_kernel_timer, sr_kernel_time_ms, sr_kernel_timeline, sr_trace_buffer, sr_trace_records,
+    Graph,
 )
 from . import lattice, model  # noqa: F401

@@ -33,6 +33,10 @@ SIGNATURES = {
     "sr_kernel_time_ms": (_dbl, [C.c_char_p, _I64P]),
     "sr_kernel_timeline": (C.c_size_t, [C.c_char_p, C.c_size_t]),
     "sr_trace_buffer": (_i32, [C.c_void_p, _i64]),
+    "sr_graph_capture_begin": (_i32, [C.c_void_p]),
+    "sr_graph_capture_end": (_i32, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "sr_graph_launch": (_i32, [C.c_void_p, C.c_void_p]),
+    "sr_graph_destroy": (_i32, [C.c_void_p]),
     "sr_jacobian_workspace_bytes": (_sz, [_i32, _I32P, _i64]),
     "sr_jacobian": (_i32, [_i32, _I32P, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _sz, _vp]),
     "sr_local_energy_workspace_bytes": (_sz, [_i32, _I32P, _i64, _i64]),
@@ -332,6 +336,47 @@ def sr_reset_launch_count():
 
 def sr_kernel_timer(enable):
     load().sr_kernel_timer(1 if enable else 0)
+
+
+class Graph:
+    """A CUDA graph captured through the library (sr_graph_capture_begin/end): per-node
+    priorities are kept at instantiation, unlike torch.cuda.CUDAGraph.  Usage:
+        g = Graph(device); with g.capture(): <library calls on torch's current stream>
+        g.replay()"""
+
+    def __init__(self, device):
+        self.device = torch.device(device)
+        self.stream = torch.cuda.Stream(self.device)
+        self.exec = None
+
+    def capture(self):
+        import contextlib
+
+        @contextlib.contextmanager
+        def _cap():
+            lib = load()
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(self.stream):
+                _check(lib.sr_graph_capture_begin(C.c_void_p(self.stream.cuda_stream)), "sr_graph_capture_begin")
+                try:
+                    yield self
+                finally:
+                    h = C.c_void_p()
+                    _check(lib.sr_graph_capture_end(C.c_void_p(self.stream.cuda_stream), C.byref(h)),
+                           "sr_graph_capture_end")
+                    self.exec = h
+            torch.cuda.current_stream(self.device).wait_stream(self.stream)
+        return _cap()
+
+    def replay(self):
+        _check(load().sr_graph_launch(self.exec, _stream(self.device)), "sr_graph_launch")
+
+    def __del__(self):
+        try:
+            if self.exec is not None and _lib is not None:
+                _lib.sr_graph_destroy(self.exec)
+        except Exception:
+            pass
 
 
 TRACE_KINDS = {1: "diag", 2: "trsm", 3: "skinny_sub", 4: "gram", 5: "trail", 6: "rhs", 7: "back", 8: "back_rest",

@@ -332,7 +332,8 @@ sr_status step_graphed(const StepLayout& L, const StepGraphKey& key, const doubl
   cudaGraph_t graph = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(cap, &graph);
   cudaGraphExec_t exec = nullptr;
-  if (r != SR_OK || ec != cudaSuccess || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+  if (r != SR_OK || ec != cudaSuccess ||
+      cudaGraphInstantiateWithFlags(&exec, graph, cudaGraphInstantiateFlagUseNodePriority) != cudaSuccess) {
     if (graph) cudaGraphDestroy(graph);
     cudaGetLastError();
     if (r != SR_OK) return r;
@@ -476,6 +477,35 @@ SR_API sr_status sr_block_qgt_i8(int64_t n_samples, int n_blocks, const int64_t*
 }
 
 SR_API void sr_kernel_timer(int enable) { g_timer = enable != 0; }
+
+SR_API sr_status sr_graph_capture_begin(void* stream) {
+  SR_CHECK_ARG(stream != nullptr, "capture needs a non-default stream");
+  SR_CUDA(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal));
+  return SR_OK;
+}
+
+SR_API sr_status sr_graph_capture_end(void* stream, void** graph_exec) {
+  SR_CHECK_ARG(stream != nullptr && graph_exec != nullptr, "null pointer");
+  cudaGraph_t g = nullptr;
+  SR_CUDA(cudaStreamEndCapture((cudaStream_t)stream, &g));
+  cudaGraphExec_t e = nullptr;
+  const cudaError_t r = cudaGraphInstantiateWithFlags(&e, g, cudaGraphInstantiateFlagUseNodePriority);
+  cudaGraphDestroy(g);
+  SR_CUDA(r);
+  *graph_exec = e;
+  return SR_OK;
+}
+
+SR_API sr_status sr_graph_launch(void* graph_exec, void* stream) {
+  SR_CHECK_ARG(graph_exec != nullptr, "null graph");
+  SR_CUDA(cudaGraphLaunch((cudaGraphExec_t)graph_exec, (cudaStream_t)stream));
+  return SR_OK;
+}
+
+SR_API sr_status sr_graph_destroy(void* graph_exec) {
+  if (graph_exec) SR_CUDA(cudaGraphExecDestroy((cudaGraphExec_t)graph_exec));
+  return SR_OK;
+}
 
 SR_API sr_status sr_trace_buffer(void* records, int64_t capacity) {
   SR_CHECK_ARG(records == nullptr || capacity >= 2, "capacity must be >= 2 records");

@@ -247,6 +247,14 @@ int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
+// In-strip updates of the columns beyond the two-column lookahead: left-looking (one K =
+// 64 (p - p0 + 1) update of column p+3 per step on s2, SR_INSTRIP_LEFT=1) or right-looking
+// (every panel updating all later columns, SR_INSTRIP_LEFT=0).
+bool instrip_left() {
+  static const int v = env_int("SR_INSTRIP_LEFT", 1);
+  return v != 0;
+}
+
 // Split TRSM (see solve_block); SR_TRSM_SPLIT=0 restores the whole TRSM on the chain.
 bool trsm_split() {
   static const int v = env_int("SR_TRSM_SPLIT", 1);
@@ -327,7 +335,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
       if (p > p0) SR_CUDA(cudaStreamWaitEvent(st, Q.ec, 0));
       const long long m = B.npad - (long long)(p + 1) * NB;
       if (m <= 0) continue;
-      gram::ProbSet trsm{}, trsm_rest{}, next_tile{}, next_rows{}, inner_rest{};
+      gram::ProbSet trsm{}, trsm_rest{}, next_tile{}, next_rows{}, next_rows2{}, inner_rest{};
       double2* panel = B.Fm + (long long)(p + 1) * NB * B.npad + (long long)p * NB;
       const double2* linv_p = B.linv + (long long)p * NB * NB;
       // Split TRSM: the chain solves only the next panel's row block (all that the next-tile
@@ -340,6 +348,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
       } else {
         gram::add_prob(trsm, panel, B.npad, linv_p, NB, panel, B.npad, (int)m, NB, NB, false);
       }
+      const bool left = instrip_left();
       for (int jj = p + 1; jj < pend; jj++) {   // later columns of the strip, rows i >= jj
         const double2* lrows = B.Fm + (long long)jj * NB * B.npad + (long long)p * NB;
         double2* cblk = B.Fm + (long long)jj * NB * B.npad + (long long)jj * NB;
@@ -349,8 +358,16 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
           if (rows > NB)
             gram::add_prob(next_rows, lrows + (long long)NB * B.npad, B.npad, lrows, B.npad,
                            cblk + (long long)NB * B.npad, B.npad, rows - NB, NB, NB, false);
-        } else if (jj == p + 2) {   // two-column lookahead on s3 (see the ordering note above)
-          gram::add_prob(next_rows, lrows, B.npad, lrows, B.npad, cblk, B.npad, rows, NB, NB, false);
+        } else if (jj == p + 2) {   // two-column lookahead on s3 (see the ordering note above);
+          // left-looking after the first step: its own launch, behind the s2 job it waits for
+          gram::add_prob(left && p > p0 ? next_rows2 : next_rows, lrows, B.npad, lrows, B.npad, cblk, B.npad, rows,
+                         NB, NB, false);
+        } else if (left) {
+          if (jj == p + 3) {   // left-looking: column p+3 by all of the strip's panels p0..p at once
+            const double2* lk = B.Fm + (long long)jj * NB * B.npad + (long long)p0 * NB;
+            gram::add_prob(inner_rest, lk, B.npad, lk, B.npad, cblk, B.npad, rows, NB, (long long)(p - p0 + 1) * NB,
+                           false);
+          }
         } else {
           gram::add_prob(inner_rest, lrows, B.npad, lrows, B.npad, cblk, B.npad, rows, NB, NB, false);
         }
@@ -369,9 +386,9 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
       static const bool after_next = env_int("SR_SIDE_AFTER_NEXT", 1) != 0;
       const cudaEvent_t side_go = after_next ? Q.ed : Q.ea;
       if (side && after_next) SR_CUDA(cudaEventRecord(Q.ed, st));
-      if (side && next_rows.count) {
+      if (side && (next_rows.count || next_rows2.count)) {
         SR_CUDA(cudaStreamWaitEvent(Q.s3, side_go, 0));
-        if (p > p0) SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.eb, 0));
+        if (p > p0 && !left) SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.eb, 0));
         if (split) {
           timer_begin("chol_trsm_rest", Q.s3);
           SR_TRY((gram::launch_skinny<gram::STORE>(trsm_rest, Q.s3)));
@@ -379,13 +396,18 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
           SR_CUDA(cudaEventRecord(Q.er, Q.s3));   // all of L column p: the s2 job may start
         }
         timer_begin("chol_next_rows", Q.s3);
-        SR_TRY((gram::launch_skinny<gram::SUB>(next_rows, Q.s3)));
+        if (next_rows.count) SR_TRY((gram::launch_skinny<gram::SUB>(next_rows, Q.s3)));
+        // left-looking: column p+2 first takes the s2 job of the previous step (panels
+        // p0..p-1), which began right after that step's TRSM
+        if (next_rows2.count) SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.eb, 0));
+        if (next_rows2.count) SR_TRY((gram::launch_skinny<gram::SUB>(next_rows2, Q.s3)));
         timer_end(Q.s3);
         SR_CUDA(cudaEventRecord(Q.ec, Q.s3));
       }
       if (inner_rest.count) {
-        SR_CUDA(cudaStreamWaitEvent(Q.s2, side_go, 0));
-        if (split) SR_CUDA(cudaStreamWaitEvent(Q.s2, Q.er, 0));
+        if (left) SR_CUDA(cudaStreamWaitEvent(Q.s2, split ? Q.er : Q.ea, 0));
+        else SR_CUDA(cudaStreamWaitEvent(Q.s2, side_go, 0));
+        if (split && !left) SR_CUDA(cudaStreamWaitEvent(Q.s2, Q.er, 0));
         timer_begin("chol_inner_rest", Q.s2);
         SR_TRY((gram::launch_skinny<gram::SUB>(inner_rest, Q.s2)));
         timer_end(Q.s2);

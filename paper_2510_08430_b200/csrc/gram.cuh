@@ -304,7 +304,7 @@ constexpr int SK_THREADS = 128;
 template <int TM>
 constexpr size_t skinny_smem() { return (size_t)(TM + 64) * SK_LD * sizeof(double2); }   // 87 / 104 KB
 
-template <int EP, int SK_TM = 16>
+template <int EP, int SK_TM = 16, bool KLOOP = false>
 __global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_constant__ ProbSet ps) {
   constexpr int MI = SK_TM / 8;
   TraceScope trace_(EP == STORE ? TR_TRSM : TR_SKINNY_SUB, (int)ps.p[0].M);
@@ -318,24 +318,6 @@ __global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_cons
   const int m0 = (int)((long long)blockIdx.x - P.tile_begin) * SK_TM;
   const long long K = P.K;
   pdl_wait();
-#pragma unroll
-  for (int h = 0; h < 2; h++) {   // two commit groups: k in [32h, 32h + 32)
-#pragma unroll
-    for (int it = 0; it < (SK_TM * 32) / SK_THREADS; it++) {
-      const int e = threadIdx.x + it * SK_THREADS;
-      const int r = e >> 5, k = 32 * h + (e & 31);
-      const bool v = (m0 + r < P.M) && (k < K);
-      cp_async16(sa + r * SK_LD + k, v ? P.A + (long long)(m0 + r) * P.lda + k : P.A, v);
-    }
-#pragma unroll
-    for (int it = 0; it < (64 * 32) / SK_THREADS; it++) {
-      const int e = threadIdx.x + it * SK_THREADS;
-      const int r = e >> 5, k = 32 * h + (e & 31);
-      const bool v = (r < P.N) && (k < K);
-      cp_async16(sb + r * SK_LD + k, v ? P.B + (long long)r * P.ldb + k : P.B, v);
-    }
-    cp_commit();
-  }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lr = lane >> 2, lk = lane & 3;
   double acc_r[MI][2][2], acc_i[MI][2][2];
@@ -346,35 +328,60 @@ __global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_cons
       acc_r[a][b][0] = acc_r[a][b][1] = 0.0;
       acc_i[a][b][0] = acc_i[a][b][1] = 0.0;
     }
+  // K in chunks of 64: one chunk (straight-line, KLOOP = false) for the chain's K = 64
+  // products; the left-looking column updates of a strip have K up to 64 (kStrip - 2)
+  const long long kend = KLOOP ? K : 1;
+#pragma unroll 1
+  for (long long kc = 0; kc < kend; kc += 64) {
+    if (kc > 0) __syncthreads();   // the previous chunk has been consumed
 #pragma unroll
-  for (int h = 0; h < 2; h++) {
-    if (h == 0) cp_wait<1>(); else cp_wait<0>();
-    __syncthreads();
+    for (int h = 0; h < 2; h++) {   // two commit groups: k in [32h, 32h + 32)
 #pragma unroll
-    for (int k4 = 32 * h; k4 < 32 * h + 32; k4 += 4) {
-      double ar[MI], ai[MI], nai[MI], br[2], bi[2];
-#pragma unroll
-      for (int mi = 0; mi < MI; mi++) {
-        const double2 v = sa[(mi * 8 + lr) * SK_LD + k4 + lk];
-        ar[mi] = v.x;
-        ai[mi] = v.y;
-        nai[mi] = -v.y;
+      for (int it = 0; it < (SK_TM * 32) / SK_THREADS; it++) {
+        const int e = threadIdx.x + it * SK_THREADS;
+        const int r = e >> 5, k = 32 * h + (e & 31);
+        const bool v = (m0 + r < P.M) && (kc + k < K);
+        cp_async16(sa + r * SK_LD + k, v ? P.A + (long long)(m0 + r) * P.lda + kc + k : P.A, v);
       }
 #pragma unroll
-      for (int ni = 0; ni < 2; ni++) {
-        const double2 v = sb[(w * 16 + ni * 8 + lr) * SK_LD + k4 + lk];
-        br[ni] = v.x;
-        bi[ni] = -v.y;   // b(k,n) = conj(B[n][k])
+      for (int it = 0; it < (64 * 32) / SK_THREADS; it++) {
+        const int e = threadIdx.x + it * SK_THREADS;
+        const int r = e >> 5, k = 32 * h + (e & 31);
+        const bool v = (r < P.N) && (kc + k < K);
+        cp_async16(sb + r * SK_LD + k, v ? P.B + (long long)r * P.ldb + kc + k : P.B, v);
       }
+      cp_commit();
+    }
 #pragma unroll
-      for (int mi = 0; mi < MI; mi++)
+    for (int h = 0; h < 2; h++) {
+      if (h == 0) cp_wait<1>(); else cp_wait<0>();
+      __syncthreads();
+#pragma unroll
+      for (int k4 = 32 * h; k4 < 32 * h + 32; k4 += 4) {
+        double ar[MI], ai[MI], nai[MI], br[2], bi[2];
+#pragma unroll
+        for (int mi = 0; mi < MI; mi++) {
+          const double2 v = sa[(mi * 8 + lr) * SK_LD + k4 + lk];
+          ar[mi] = v.x;
+          ai[mi] = v.y;
+          nai[mi] = -v.y;
+        }
 #pragma unroll
         for (int ni = 0; ni < 2; ni++) {
-          dmma(acc_r[mi][ni][0], acc_r[mi][ni][1], ar[mi], br[ni]);
-          dmma(acc_i[mi][ni][0], acc_i[mi][ni][1], ar[mi], bi[ni]);
-          dmma(acc_r[mi][ni][0], acc_r[mi][ni][1], nai[mi], bi[ni]);
-          dmma(acc_i[mi][ni][0], acc_i[mi][ni][1], ai[mi], br[ni]);
+          const double2 v = sb[(w * 16 + ni * 8 + lr) * SK_LD + k4 + lk];
+          br[ni] = v.x;
+          bi[ni] = -v.y;   // b(k,n) = conj(B[n][k])
         }
+#pragma unroll
+        for (int mi = 0; mi < MI; mi++)
+#pragma unroll
+          for (int ni = 0; ni < 2; ni++) {
+            dmma(acc_r[mi][ni][0], acc_r[mi][ni][1], ar[mi], br[ni]);
+            dmma(acc_i[mi][ni][0], acc_i[mi][ni][1], ar[mi], bi[ni]);
+            dmma(acc_r[mi][ni][0], acc_r[mi][ni][1], nai[mi], bi[ni]);
+            dmma(acc_i[mi][ni][0], acc_i[mi][ni][1], ai[mi], br[ni]);
+          }
+      }
     }
   }
 #pragma unroll
@@ -395,27 +402,36 @@ __global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_cons
 }
 
 // Launch a set of NH problems with N <= 64 and K <= 64 (not lower) on the skinny kernel.
-template <int EP, int SK_TM = 16>
-inline sr_status launch_skinny(ProbSet ps, cudaStream_t st, bool pdl = false) {
+template <int EP, int SK_TM, bool KLOOP>
+inline sr_status launch_skinny_k(const ProbSet& ps, long long total, cudaStream_t st, bool pdl) {
   constexpr size_t kSkinnySmem = skinny_smem<SK_TM>();
-  static_assert(EP == SUB || EP == STORE, "skinny epilogues: SUB or STORE");
-  long long total = 0;
-  for (int i = 0; i < ps.count; i++) {
-    if (ps.p[i].N > 64 || ps.p[i].K > 64 || ps.p[i].lower) return SR_ERR_INVALID;
-    ps.p[i].tile_begin = total;
-    total += (ps.p[i].M + SK_TM - 1) / SK_TM;
-  }
-  if (total == 0) return SR_OK;
   static bool attr_set = false;
   if (!attr_set) {
-    SR_CUDA(cudaFuncSetAttribute(skinny_kernel<EP, SK_TM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SR_CUDA(cudaFuncSetAttribute(skinny_kernel<EP, SK_TM, KLOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kSkinnySmem));
     attr_set = true;
   }
-  if (pdl) SR_CUDA(launch_pdl(skinny_kernel<EP, SK_TM>, dim3((unsigned)total), dim3(SK_THREADS), kSkinnySmem, st, ps));
-  else skinny_kernel<EP, SK_TM><<<(unsigned)total, SK_THREADS, kSkinnySmem, st>>>(ps);
+  if (pdl)
+    SR_CUDA(launch_pdl(skinny_kernel<EP, SK_TM, KLOOP>, dim3((unsigned)total), dim3(SK_THREADS), kSkinnySmem, st, ps));
+  else
+    skinny_kernel<EP, SK_TM, KLOOP><<<(unsigned)total, SK_THREADS, kSkinnySmem, st>>>(ps);
   SR_LAUNCHED();
   return SR_OK;
+}
+
+template <int EP, int SK_TM = 16>
+inline sr_status launch_skinny(ProbSet ps, cudaStream_t st, bool pdl = false) {
+  static_assert(EP == SUB || EP == STORE, "skinny epilogues: SUB or STORE");
+  long long total = 0, kmax = 0;
+  for (int i = 0; i < ps.count; i++) {
+    if (ps.p[i].N > 64 || ps.p[i].lower || (EP == STORE && ps.p[i].K > 64)) return SR_ERR_INVALID;
+    ps.p[i].tile_begin = total;
+    total += (ps.p[i].M + SK_TM - 1) / SK_TM;
+    kmax = std::max(kmax, (long long)ps.p[i].K);
+  }
+  if (total == 0) return SR_OK;
+  if (kmax > 64) return launch_skinny_k<EP, SK_TM, true>(ps, total, st, pdl);
+  return launch_skinny_k<EP, SK_TM, false>(ps, total, st, pdl);
 }
 
 }  // namespace gram

@@ -16,6 +16,8 @@ the collective pattern can be exercised on CPU with gloo (tests/test_parallel_gl
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -177,13 +179,22 @@ class LocalStep:
         return b.dtheta, b.energy
 
     # --- CUDA graph of the whole step (the ~1000 launches of a step replayed as one) ---
-    def capture(self, theta):
-        """Capture run(theta) into a CUDA graph; theta's buffer is read at replay time."""
+    def capture(self, theta, lib_graph=None):
+        """Capture run(theta) into a CUDA graph; theta's buffer is read at replay time.  With
+        lib_graph (default: environment SR_LIB_GRAPH, else on) the graph is captured and
+        instantiated by the library (sr.Graph) so the solves' stream priorities survive."""
+        if lib_graph is None:
+            lib_graph = os.environ.get("SR_LIB_GRAPH", "1") != "0"
         self.run(theta)                      # warm: lazy attributes, side streams
         torch.cuda.synchronize(self.device)
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            self.run(theta)
+        if lib_graph:
+            self.graph = sr.Graph(self.device)
+            with self.graph.capture():
+                self.run(theta)
+        else:
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                self.run(theta)
         return self.graph
 
     def replay(self):

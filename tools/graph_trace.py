@@ -35,9 +35,14 @@ if arg.startswith("solve"):   # solve-only graph of one block of the given size,
         def capture(self, _theta):
             self.run()
             torch.cuda.synchronize()
-            self.graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(self.graph):
-                self.run()
+            if os.environ.get("SR_LIB_GRAPH", "1") != "0":   # library-instantiated: node priorities kept
+                self.graph = sr.Graph(dev)
+                with self.graph.capture():
+                    self.run()
+            else:
+                self.graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(self.graph):
+                    self.run()
 
         def replay(self):
             self.graph.replay()
