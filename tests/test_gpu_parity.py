@@ -406,3 +406,43 @@ def test_empty_batch(sr):
     lam = 0.25
     sr.sr_block_solve(offs, S, F, lam, d)
     assert torch.allclose(d, -F / lam, rtol=1e-15, atol=0)
+
+
+def test_library_graph_capture(sr):
+    """sr.Graph (sr_graph_capture_begin/end, sr_graph_launch): a captured block QGT + solve
+    replays to the eager result and reads its inputs at replay time; LocalStep's graph
+    (the bench's timed step) equals its eager step."""
+    from paper_2510_08430_b200 import parallel
+    n, ns = 300, 256
+    g = torch.Generator(device=dev()).manual_seed(5)
+    A = torch.randn(ns, n, dtype=C128, device=dev(), generator=g) / ns ** 0.5
+    offs = [0, 120, n]
+    S = torch.empty(120 * 120 + 180 * 180, dtype=C128, device=dev())
+    F = torch.randn(n, dtype=C128, device=dev(), generator=g)
+    d = torch.empty_like(F)
+    sr.sr_block_qgt_i8(A, offs, S)
+    sr.sr_block_solve(offs, S, F, 1e-3, d)
+    torch.cuda.synchronize()
+    ref = d.clone()
+    graph = sr.Graph(dev())
+    with graph.capture():
+        sr.sr_block_qgt_i8(A, offs, S)
+        sr.sr_block_solve(offs, S, F, 1e-3, d)
+    d.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(d, ref)
+    F.mul_(2.0)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.allclose(d, 2.0 * ref, rtol=1e-13, atol=0)
+    w = workloads.CONFIGS[0]
+    spins, params = workloads.make_inputs(w)
+    ij, jj = sr.lattice.for_workload(w)
+    theta = T(sr.model.pack(params))
+    step = parallel.LocalStep(w.widths, spins, ij, jj, w.lam, dev())
+    d_eager = step.run(theta)[0].clone()
+    step.capture(theta)
+    d_graph = step.replay()[0]
+    torch.cuda.synchronize()
+    assert torch.equal(d_graph, d_eager)
