@@ -264,6 +264,21 @@ SR_API sr_status sr_ntk_solve(int64_t n_samples, int64_t n_p, const double* A, i
                               double* T_out, int32_t* info, void* workspace,
                               size_t workspace_bytes, void* stream);
 
+/* sr_gram_nh — C = A B^H (complex; C[i][j] = sum_k A[i][k] conj(B[j][k])) for row-major
+ * A (m x k, lda), B (n x k, ldb), C (m x n, ldc), on the FP64 DMMA tile engine: the
+ * block-row T_r,s = A_r A_s^H of the sample-space (NTK) matrix when samples are sharded
+ * over ranks (parallel.ShardedStep.ntk_solve).  m, n or k = 0 is allowed (C is left
+ * untouched for m or n = 0, zeroed for k = 0). */
+SR_API sr_status sr_gram_nh(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                            int64_t ldb, double* C, int64_t ldc, void* stream);
+
+/* sr_aHv — out = alpha A^H v (complex) for A (n_rows x n_p, lda), v [n_rows], out [n_p]:
+ * the final product dtheta = -A^H y of the NTK solve, per rank on its own rows (summed over
+ * ranks by the caller).  Deterministic (fixed-order chunk reduction). */
+SR_API size_t sr_aHv_workspace_bytes(int64_t n_rows, int64_t n_p);
+SR_API sr_status sr_aHv(int64_t n_rows, int64_t n_p, const double* A, int64_t lda, const double* v, double alpha,
+                        double* out, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---------------------------------------------------------------- full step ---
  * sr_step — stages (1)-(5) back to back on device buffers (uniform weights):
  *   theta complex [n_p], spins int8 [n_samples][N], bonds as in stage (2);

@@ -33,6 +33,9 @@ SIGNATURES = {
     "sr_kernel_time_ms": (_dbl, [C.c_char_p, _I64P]),
     "sr_kernel_timeline": (C.c_size_t, [C.c_char_p, C.c_size_t]),
     "sr_trace_buffer": (_i32, [C.c_void_p, _i64]),
+    "sr_gram_nh": (_i32, [_i64, _i64, _i64, C.c_void_p, _i64, C.c_void_p, _i64, C.c_void_p, _i64, C.c_void_p]),
+    "sr_aHv_workspace_bytes": (_sz, [_i64, _i64]),
+    "sr_aHv": (_i32, [_i64, _i64, C.c_void_p, _i64, C.c_void_p, _dbl, C.c_void_p, C.c_void_p, _sz, C.c_void_p]),
     "sr_graph_capture_begin": (_i32, [C.c_void_p]),
     "sr_graph_capture_end": (_i32, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "sr_graph_launch": (_i32, [C.c_void_p, C.c_void_p]),
@@ -288,6 +291,27 @@ def sr_ntk_solve(A, e_tilde, lam, dtheta, T_out=None, info=None, workspace=None)
     ws = _workspace(lib.sr_ntk_solve_workspace_bytes(ns, npar), A.device, workspace)
     _check(lib.sr_ntk_solve(ns, npar, _ptr(A), A.shape[1], _ptr(e_tilde), float(lam), _ptr(dtheta),
                             _ptr(T_out), _ptr(info), *_ws_args(ws), _stream(A.device)), "sr_ntk_solve")
+
+
+def sr_gram_nh(A, B, C_out):
+    """C_out = A B^H (rows of A against rows of B; A, B may be row slices / column slices)."""
+    lda, ldb = _cols(A, "A"), _cols(B, "B")
+    ldc = _cols(C_out, "C")
+    if A.shape[1] != B.shape[1] or C_out.shape[0] != A.shape[0] or C_out.shape[1] != B.shape[0]:
+        raise SRError("sr_gram_nh: shape mismatch")
+    _check(load().sr_gram_nh(A.shape[0], B.shape[0], A.shape[1], _ptr(A), lda, _ptr(B), ldb, _ptr(C_out), ldc,
+                             _stream(A.device)), "sr_gram_nh")
+
+
+def sr_aHv(A, v, alpha, out, workspace=None):
+    """out = alpha A^H v."""
+    lib = load()
+    lda = _cols(A, "A")
+    _dev(v, torch.complex128, "v")
+    _dev(out, torch.complex128, "out")
+    ws = _workspace(lib.sr_aHv_workspace_bytes(A.shape[0], A.shape[1]), A.device, workspace)
+    _check(lib.sr_aHv(A.shape[0], A.shape[1], _ptr(A), lda, _ptr(v), float(alpha), _ptr(out), *_ws_args(ws),
+                      _stream(A.device)), "sr_aHv")
 
 
 # ------------------------------------------------------------------ full step

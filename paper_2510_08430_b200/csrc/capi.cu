@@ -478,6 +478,31 @@ SR_API sr_status sr_block_qgt_i8(int64_t n_samples, int n_blocks, const int64_t*
 
 SR_API void sr_kernel_timer(int enable) { g_timer = enable != 0; }
 
+SR_API sr_status sr_gram_nh(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                            int64_t ldb, double* C, int64_t ldc, void* stream) {
+  SR_CHECK_ARG(m >= 0 && n >= 0 && k >= 0 && m < (1LL << 31) && n < (1LL << 31), "bad sizes");
+  SR_CHECK_ARG(lda >= k && ldb >= k && ldc >= n, "leading dimension too small");
+  if (m == 0 || n == 0) return SR_OK;
+  SR_CHECK_ARG(C && ((A && B) || k == 0), "null pointer");
+  gram::ProbSet ps{};
+  gram::add_prob(ps, reinterpret_cast<const double2*>(A), lda, reinterpret_cast<const double2*>(B), ldb,
+                 reinterpret_cast<double2*>(C), ldc, (int)m, (int)n, k, false);
+  return gram::launch<gram::NH, gram::STORE>(ps, (cudaStream_t)stream);
+}
+
+SR_API size_t sr_aHv_workspace_bytes(int64_t n_rows, int64_t n_p) {
+  if (n_rows < 1 || n_p < 1) return 0;
+  return aHv_ws(n_rows, n_p);
+}
+
+SR_API sr_status sr_aHv(int64_t n_rows, int64_t n_p, const double* A, int64_t lda, const double* v, double alpha,
+                        double* out, void* workspace, size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(n_rows >= 1 && n_p >= 1 && lda >= n_p, "bad sizes");
+  SR_CHECK_ARG(A && v && out && workspace, "null pointer");
+  return aHv_impl(n_rows, n_p, reinterpret_cast<const double2*>(A), lda, reinterpret_cast<const double2*>(v), alpha,
+                  reinterpret_cast<double2*>(out), workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
 SR_API sr_status sr_graph_capture_begin(void* stream) {
   SR_CHECK_ARG(stream != nullptr, "capture needs a non-default stream");
   SR_CUDA(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal));

@@ -65,14 +65,26 @@ class CudaOps:
         sr.sr_center_force_global(O, e_loc, n_total, moments_all, e_tilde, F_partial, energy=energy,
                                   workspace=self.ws)
 
+    def _ws(self, need):
+        # the shared workspace when it is large enough, else a temporary (comparison solves)
+        return self.ws if need <= self.ws.numel() else None
+
     def block_qgt(self, A, offs, S):
         if self.gram_engine == "int8":
-            sr.sr_block_qgt_i8(A, offs, S, workspace=self.ws)
+            need = sr.load().sr_block_qgt_i8_workspace_bytes(A.shape[0], len(offs) - 1, sr._offsets(offs))
+            sr.sr_block_qgt_i8(A, offs, S, workspace=self._ws(need))
         else:
             sr.sr_block_qgt(A, offs, S)
 
     def block_solve(self, offs, S, F, lam, dtheta, info=None):
-        sr.sr_block_solve(offs, S, F, lam, dtheta, info=info, workspace=self.ws)
+        need = sr.load().sr_block_solve_workspace_bytes(len(offs) - 1, sr._offsets(offs))
+        sr.sr_block_solve(offs, S, F, lam, dtheta, info=info, workspace=self._ws(need))
+
+    def gram_nh(self, A, B, C):
+        sr.sr_gram_nh(A, B, C)
+
+    def aHv(self, A, v, alpha, out):
+        sr.sr_aHv(A, v, alpha, out)
 
 
 def shard_range(n, rank, world):
@@ -297,6 +309,61 @@ class ShardedStep:
         dist.all_reduce(b.dtheta, group=g)
         _rec(events, 5, st)
         return b.dtheta, b.energy
+
+    # --- comparison paths, sharded the same way (north_star); call after run() ---
+    def full_qgt_solve(self):
+        """Full-QGT solve with samples sharded: each rank's partial S = A_r^H A_r over all n_p
+        columns, NCCL reduce to rank 0, which solves (S + lambda I) dtheta = -F (one blocked
+        Cholesky); dtheta broadcast.  Returns dtheta (every rank)."""
+        import torch.distributed as dist
+        b, o, g = self.buf, self.ops, self.group
+        n = b.n_p
+        S = torch.empty(n * n, dtype=torch.complex128, device=self.device)
+        o.block_qgt(b.O, [0, n], S)
+        dist.reduce(S, dst=0, group=g)
+        d = torch.zeros(n, dtype=torch.complex128, device=self.device)
+        if self.rank == 0:
+            o.block_solve([0, n], S, b.F, self.lam, d)
+        dist.broadcast(d, src=0, group=g)
+        return d
+
+    def ntk_solve(self):
+        """Sample-space (NTK / MinSR) solve with samples sharded: T = A A^H assembled by
+        block rows -- rank r computes T_r,s = A_r A_s^H as each rank's A_s is broadcast in
+        turn -- gathered to rank 0 with the residuals e, which solves (T + lambda I) y = e;
+        y is broadcast and each rank forms -A_r^H y_r, summed by an all-reduce.  Returns
+        dtheta (every rank)."""
+        import torch.distributed as dist
+        b, o, g = self.buf, self.ops, self.group
+        c = torch.complex128
+        N, G, r = self.n_total, self.world, self.rank
+        rows = [shard_range(N, q, G) for q in range(G)]
+        lo, hi = rows[r]
+        T_r = torch.empty(hi - lo, N, dtype=c, device=self.device)
+        for q, (qlo, qhi) in enumerate(rows):
+            A_q = b.O if q == r else torch.empty(qhi - qlo, b.n_p, dtype=c, device=self.device)
+            dist.broadcast(A_q, src=q, group=g)
+            if qhi > qlo and hi > lo:
+                o.gram_nh(b.O, A_q, T_r[:, qlo:qhi])
+        mx = max(qhi - qlo for qlo, qhi in rows)
+        T_pad = torch.zeros(mx, N, dtype=c, device=self.device)
+        T_pad[:hi - lo] = T_r
+        e_pad = torch.zeros(mx, dtype=c, device=self.device)
+        e_pad[:hi - lo] = b.e_tilde
+        T_all = [torch.empty_like(T_pad) for _ in range(G)]
+        e_all = [torch.empty_like(e_pad) for _ in range(G)]
+        dist.all_gather(T_all, T_pad, group=g)
+        dist.all_gather(e_all, e_pad, group=g)
+        z = torch.empty(N, dtype=c, device=self.device)
+        if r == 0:
+            T = torch.cat([T_all[q][:qhi - qlo] for q, (qlo, qhi) in enumerate(rows)]).reshape(-1)
+            e = torch.cat([e_all[q][:qhi - qlo] for q, (qlo, qhi) in enumerate(rows)])
+            o.block_solve([0, N], T, e, self.lam, z)   # z = -(T + lambda I)^{-1} e
+        dist.broadcast(z, src=0, group=g)
+        d = torch.empty(b.n_p, dtype=c, device=self.device)
+        o.aHv(b.O, z[lo:hi].contiguous(), 1.0, d)     # -A_r^H y_r = A_r^H z_r
+        dist.all_reduce(d, group=g)
+        return d
 
     # --- CUDA graph of the whole sharded step, NCCL collectives included (they are captured
     # as graph nodes; every rank captures the same sequence) ---

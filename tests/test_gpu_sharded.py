@@ -85,3 +85,35 @@ def test_sharded_step_graph_replay(nccl_group):
         torch.cuda.synchronize()
         assert torch.equal(d_new, d_ref)
         theta.div_(1.01)
+
+
+def test_sharded_comparison_solves(nccl_group):
+    """The full-QGT and NTK comparison paths sharded the same way (ShardedStep.full_qgt_solve /
+    ntk_solve: partial-S reduce to rank 0; NTK block rows A_r A_s^H by broadcasts, gathered,
+    y broadcast, A_r^H y_r all-reduced) agree with the single-GPU sr_full_qgt_solve /
+    sr_ntk_solve on the same centred Jacobian, and with each other (push-through)."""
+    import paper_2510_08430_b200 as sr
+    from paper_2510_08430_b200 import parallel
+    w = workloads.CONFIGS[0]
+    spins, params = workloads.make_inputs(w)
+    ij, jj = sr.lattice.for_workload(w)
+    dev = torch.device("cuda:0")
+    theta = torch.from_numpy(sr.model.pack(params)).to(dev)
+    shard = parallel.ShardedStep(w.widths, spins, ij, jj, w.lam, 0, 1, dev, per_block_gram=True)
+    shard.run(theta)
+    d_full = shard.full_qgt_solve().clone()
+    d_ntk = shard.ntk_solve().clone()
+    b = shard.buf
+    ref_full = torch.empty_like(d_full)
+    ref_ntk = torch.empty_like(d_ntk)
+    sr.sr_full_qgt_solve(b.O, b.F, w.lam, ref_full)
+    sr.sr_ntk_solve(b.O, b.e_tilde, w.lam, ref_ntk)
+    torch.cuda.synchronize()
+    rel = lambda a, c: (torch.linalg.vector_norm(a - c) / torch.linalg.vector_norm(c)).item()  # noqa: E731
+    assert rel(d_full, ref_full) < 1e-12
+    assert rel(d_ntk, ref_ntk) < 1e-10
+    assert rel(d_ntk, d_full) < 1e-10
+    O = network.jacobian(params, spins)
+    e = hamiltonian.local_energies(params, spins, hamiltonian.bonds_for(w))
+    full = solvers.full_solve(estimators.qgt_full(O), estimators.force(O, e), w.lam)
+    assert np.linalg.norm(d_full.cpu().numpy() - full) / np.linalg.norm(full) < 1e-9

@@ -62,6 +62,12 @@ class OracleOps:
             S[pos:pos + n * n].copy_((a.conj().T @ a).reshape(-1))
             pos += n * n
 
+    def gram_nh(self, A, B, C):
+        C.copy_(A @ B.conj().T)
+
+    def aHv(self, A, v, alpha, out):
+        out.copy_(alpha * (A.conj().T @ v))
+
     def block_solve(self, offs, S, F, lam, dtheta, info=None):
         pos = 0
         for b in range(len(offs) - 1):
@@ -84,8 +90,10 @@ def _worker(rank, world, port, result_path):
     step = ShardedStep(w.widths, spins, ij, jj, w.lam, rank, world, "cpu", ops=OracleOps(),
                        per_block_gram=world != 2)   # world 2 also covers the grouped launch
     d, e = step.run(torch.from_numpy(sr.model.pack(params)))
+    d_full = step.full_qgt_solve()   # comparison paths, sharded the same way
+    d_ntk = step.ntk_solve()
     if rank == 0:
-        np.save(result_path, np.concatenate([d.numpy(), e.numpy()]))
+        np.save(result_path, np.concatenate([d.numpy(), e.numpy(), d_full.numpy(), d_ntk.numpy()]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -103,8 +111,10 @@ def test_sharded_step_equals_unsharded_oracle(tmp_path, world):
     """world 1: one owner of both blocks; 2: one block each; 3: a rank without a block."""
     out = str(tmp_path / "d.npy")
     mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
-    got = np.load(out)
+    res = np.load(out)
     w = workloads.CONFIGS[0].with_samples(64)
+    n_p = w.n_params
+    got, got_full, got_ntk = res[:n_p + 1], res[n_p + 1:2 * n_p + 1], res[2 * n_p + 1:]
     spins, params = workloads.make_inputs(w)
     O = network.jacobian(params, spins)
     e = hamiltonian.local_energies(params, spins, hamiltonian.bonds_for(w))
@@ -112,3 +122,7 @@ def test_sharded_step_equals_unsharded_oracle(tmp_path, world):
     ref = solvers.block_solve(estimators.qgt_blocks(O, off), estimators.force(O, e), off, w.lam)
     assert np.linalg.norm(got[:-1] - ref) / np.linalg.norm(ref) < 1e-10
     assert abs(got[-1] - estimators.energy(e)) < 1e-12
+    # full-QGT and NTK comparison solves (sharded) against the oracle's full solve
+    full = solvers.full_solve(estimators.qgt_full(O), estimators.force(O, e), w.lam)
+    assert np.linalg.norm(got_full - full) / np.linalg.norm(full) < 1e-10
+    assert np.linalg.norm(got_ntk - full) / np.linalg.norm(full) < 1e-10
