@@ -321,6 +321,9 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
   // intensity of a per-panel update, 4x fewer passes over the trailing matrix).
   const bool i8 = gram_engine() == SR_GRAM_INT8;
   bool pending_b = false;   // a lookahead (b) update on s4 not yet joined into st
+  // ec / eb are waited on only once recorded by this call (inside a CUDA-graph capture, a
+  // wait on an event last recorded outside it is an error, not a no-op)
+  bool ec_rec = false, eb_rec = false;
   for (int p0 = 0; p0 < B.P; p0 += kStrip) {
     const int pend = std::min(p0 + kStrip, B.P);
     for (int p = p0; p < pend; p++) {
@@ -332,7 +335,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
       if (stagger_rec && p + 1 == stagger_panels()) SR_CUDA(cudaEventRecord(stagger_rec, st));
       // the previous panel's update of this column below the diagonal tile (s3) must be
       // complete before TRSM(p) (and joined into st in any case)
-      if (p > p0) SR_CUDA(cudaStreamWaitEvent(st, Q.ec, 0));
+      if (p > p0 && ec_rec) SR_CUDA(cudaStreamWaitEvent(st, Q.ec, 0));
       const long long m = B.npad - (long long)(p + 1) * NB;
       if (m <= 0) continue;
       gram::ProbSet trsm{}, trsm_rest{}, next_tile{}, next_rows{}, next_rows2{}, inner_rest{};
@@ -388,7 +391,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
       if (side && after_next) SR_CUDA(cudaEventRecord(Q.ed, st));
       if (side && (next_rows.count || next_rows2.count)) {
         SR_CUDA(cudaStreamWaitEvent(Q.s3, side_go, 0));
-        if (p > p0 && !left) SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.eb, 0));
+        if (p > p0 && !left && eb_rec) SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.eb, 0));
         if (split) {
           timer_begin("chol_trsm_rest", Q.s3);
           SR_TRY((gram::launch_skinny<gram::STORE>(trsm_rest, Q.s3)));
@@ -399,10 +402,11 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
         if (next_rows.count) SR_TRY((gram::launch_skinny<gram::SUB>(next_rows, Q.s3)));
         // left-looking: column p+2 first takes the s2 job of the previous step (panels
         // p0..p-1), which began right after that step's TRSM
-        if (next_rows2.count) SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.eb, 0));
+        if (next_rows2.count && eb_rec) SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.eb, 0));
         if (next_rows2.count) SR_TRY((gram::launch_skinny<gram::SUB>(next_rows2, Q.s3)));
         timer_end(Q.s3);
         SR_CUDA(cudaEventRecord(Q.ec, Q.s3));
+        ec_rec = true;
       }
       if (inner_rest.count) {
         if (left) SR_CUDA(cudaStreamWaitEvent(Q.s2, split ? Q.er : Q.ea, 0));
@@ -412,6 +416,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
         SR_TRY((gram::launch_skinny<gram::SUB>(inner_rest, Q.s2)));
         timer_end(Q.s2);
         SR_CUDA(cudaEventRecord(Q.eb, Q.s2));
+        eb_rec = true;
       }
     }
     const long long m = B.npad - (long long)pend * NB;
