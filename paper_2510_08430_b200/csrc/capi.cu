@@ -162,15 +162,16 @@ std::vector<int64_t> largest_block(const std::vector<int64_t>& offs) {
   return {0, mx};
 }
 
-// Pipelined step (int8 engine): the Grams of the blocks run one after another on the step
-// stream, largest first, and block b's Cholesky starts on its side stream as soon as S_b
-// is complete, so the latency-bound panel chains overlap the remaining Grams.
-// SR_PIPE=0 restores Gram-all-then-solve-all.
+// Pipelined step (int8 engine, SR_PIPE=1): the Grams of the blocks run one after another on
+// the step stream, largest first, and block b's Cholesky starts on its side stream as soon
+// as S_b is complete, so the panel chains overlap the remaining Grams.  Off by default: the
+// step is power-bound, and the per-block Gram launches cost more than the overlap gains
+// (configs[1] graph 36.2-36.3 vs 35.8-35.9 ms).
 bool pipe_step() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SR_PIPE");
-    v = e ? atoi(e) != 0 : 1;
+    v = e ? atoi(e) != 0 : 0;
   }
   return v != 0;
 }
