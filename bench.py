@@ -365,45 +365,52 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
-def compare_solves(sr, torch, step, w, dev, max_gb=40.0):
+def compare_solves(sr, torch, step, w, dev):
     """The comparison paths of north_star on the step's own centred Jacobian A, force F and
     residuals e: block QGT + block solve (the method), the full-QGT solve and the
     sample-space NTK solve (§1-2), each timed once eagerly with CUDA events after a
     warm call; reports how far the block update is from the full one, and the push-through
-    identity (full == NTK) on real data.  Skipped when the full QGT would not fit."""
+    identity (full == NTK) on real data.  A path whose workspace does not fit in the free
+    device memory (with the step's buffers still resident) is skipped."""
     b = step.buf
     lib = sr.load()
-    need = lib.sr_full_qgt_solve_workspace_bytes(b.O.shape[0], b.n_p) / 1e9
-    if need > max_gb:
-        return {"skipped": f"full-QGT workspace {need:.0f} GB > {max_gb:.0f} GB"}
-    d_full = torch.empty_like(b.dtheta)
-    d_ntk = torch.empty_like(b.dtheta)
-    ws_full = torch.empty(lib.sr_full_qgt_solve_workspace_bytes(b.O.shape[0], b.n_p), dtype=torch.uint8, device=dev)
-    ws_ntk = torch.empty(lib.sr_ntk_solve_workspace_bytes(b.O.shape[0], b.n_p), dtype=torch.uint8, device=dev)
-    calls = {
-        "block_qgt+block_solve": lambda: (step.ops.block_qgt(b.O, b.offs, b.S),
-                                          step.ops.block_solve(b.offs, b.S, b.F, w.lam, b.dtheta)),
-        "full_qgt_solve": lambda: sr.sr_full_qgt_solve(b.O, b.F, w.lam, d_full, workspace=ws_full),
-        "ntk_solve": lambda: sr.sr_ntk_solve(b.O, b.e_tilde, w.lam, d_ntk, workspace=ws_ntk),
-    }
-    ms = {}
+    ns = b.O.shape[0]
+    free = torch.cuda.mem_get_info(dev)[0] - (2 << 30)
+    need = {"full_qgt_solve": lib.sr_full_qgt_solve_workspace_bytes(ns, b.n_p) + 16 * b.n_p,
+            "ntk_solve": lib.sr_ntk_solve_workspace_bytes(ns, b.n_p) + 16 * b.n_p}
+    out_d = {"full_qgt_solve": torch.empty_like(b.dtheta), "ntk_solve": torch.empty_like(b.dtheta)}
+    calls = {"block_qgt+block_solve": lambda ws: (step.ops.block_qgt(b.O, b.offs, b.S),
+                                                  step.ops.block_solve(b.offs, b.S, b.F, w.lam, b.dtheta)),
+             "full_qgt_solve": lambda ws: sr.sr_full_qgt_solve(b.O, b.F, w.lam, out_d["full_qgt_solve"], workspace=ws),
+             "ntk_solve": lambda ws: sr.sr_ntk_solve(b.O, b.e_tilde, w.lam, out_d["ntk_solve"], workspace=ws)}
+    ms, skipped = {}, {}
     for name, fn in calls.items():
-        fn()
+        ws = None
+        if name in need:
+            if need[name] > free:
+                skipped[name] = f"workspace {need[name] / 1e9:.0f} GB > {free / 1e9:.0f} GB free"
+                continue
+            ws = torch.empty(int(need[name]), dtype=torch.uint8, device=dev)
+        fn(ws)
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        fn()
+        fn(ws)
         e1.record()
         torch.cuda.synchronize(dev)
         ms[name] = e0.elapsed_time(e1)
+        del ws
+        torch.cuda.empty_cache()
     nrm = lambda x: float(torch.linalg.vector_norm(x).item())   # noqa: E731
-    out = {"ms": ms,
-           "rel_l2_full_vs_ntk": nrm(d_full - d_ntk) / nrm(d_full),
-           "rel_l2_block_vs_full": nrm(b.dtheta - d_full) / nrm(d_full),
-           "sizes": {"full_qgt": b.n_p, "ntk": int(b.O.shape[0]), "blocks": [int(x) for x in block_sizes(w)]},
+    out = {"ms": ms, "sizes": {"full_qgt": b.n_p, "ntk": int(ns), "blocks": [int(x) for x in block_sizes(w)]},
            "note": "eager, one timed call each after a warm call; A, F, e from the step above"}
-    del ws_full, ws_ntk
-    torch.cuda.empty_cache()
+    ref = "full_qgt_solve" if "full_qgt_solve" in ms else ("ntk_solve" if "ntk_solve" in ms else None)
+    if "full_qgt_solve" in ms and "ntk_solve" in ms:
+        out["rel_l2_full_vs_ntk"] = nrm(out_d["full_qgt_solve"] - out_d["ntk_solve"]) / nrm(out_d["full_qgt_solve"])
+    if ref:
+        out[f"rel_l2_block_vs_{ref.split('_')[0]}"] = nrm(b.dtheta - out_d[ref]) / nrm(out_d[ref])
+    if skipped:
+        out["skipped"] = skipped
     return out
 
 
