@@ -221,7 +221,11 @@ def run_gpu(args):
     stage_ms = {name: float(np.mean([evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(n_stage_runs)]))
                 for i, name in enumerate(step.STAGES)}
 
-    use_graph = not args.no_graph
+    # One GPU (also --sharded as a 1-rank NCCL group): the step is replayed as one CUDA graph.
+    # More than one rank: eager launches unless SR_BENCH_GRAPH_SHARDED=1 -- graph capture of
+    # the NCCL collectives is tested here only on a 1-rank group, and a capture failing on
+    # some ranks could leave the others waiting inside a collective.
+    use_graph = not args.no_graph and (world == 1 or os.environ.get("SR_BENCH_GRAPH_SHARDED") == "1")
     if use_graph:
         try:
             step.capture(theta)              # the whole step (collectives included) as one CUDA graph
