@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kThreads) energy_eval(NetDesc net, const doubl
     __syncthreads();
     for (int l = 1; l < net.L; l++) {
       const int fout = net.w[l + 1];
-      dense_z<RB, (RB / 8 < kEnergyMG ? RB / 8 : kEnergyMG)>(wt + net.toff[l], net.w[l], fout, cur, ld, nxt, ld);
+      dense_z<RB, (RB / 8 < kEnergyMG ? RB / 8 : kEnergyMG), true>(wt + net.toff[l], net.w[l], fout, cur, ld, nxt, ld);
       __syncthreads();
       const double2* bl = theta + net.boff[l];
       for (int e = threadIdx.x; e < RB * fout; e += kThreads) {
