@@ -49,6 +49,9 @@ __device__ __forceinline__ void net_dmma(double& c0, double& c1, double a, doubl
 // BATCH: the B fragments of 8 k steps are loaded together ahead of their MMAs (8 L2 loads
 // in flight; measured: local energy 0.722 -> 0.695 ms at configs[1], 35.5 -> 31.8 ms at
 // configs[2]; the Jacobian kernels are faster without it, 0.258 vs 0.299 ms).
+#ifndef SR_DENSE_BQ
+#define SR_DENSE_BQ 8
+#endif
 template <int RB, int MG = 1, bool BATCH = false>
 __device__ __forceinline__ void dense_z(const double2* __restrict__ M, int n_in, int n_out, const double2* hin,
                                         int ldin, double2* zout, int ldz) {
@@ -82,13 +85,14 @@ __device__ __forceinline__ void dense_z(const double2* __restrict__ M, int n_in,
       }
     };
     if (BATCH) {
-    const int k32 = k_full & ~31;
-    for (int k0 = 0; k0 < k32; k0 += 32) {
-      double2 bb[8];
+    constexpr int BQ = SR_DENSE_BQ;
+    const int k32 = k_full - k_full % (4 * BQ);
+    for (int k0 = 0; k0 < k32; k0 += 4 * BQ) {
+      double2 bb[BQ];
 #pragma unroll
-      for (int q = 0; q < 8; q++) bb[q] = n_ok ? __ldg(mcol + (long long)(k0 + 4 * q + gc) * n_out) : make_double2(0.0, 0.0);
+      for (int q = 0; q < BQ; q++) bb[q] = n_ok ? __ldg(mcol + (long long)(k0 + 4 * q + gc) * n_out) : make_double2(0.0, 0.0);
 #pragma unroll
-      for (int q = 0; q < 8; q++) {
+      for (int q = 0; q < BQ; q++) {
 #pragma unroll
         for (int g = 0; g < MG; g++) {
           const double2 a = arow[g * 8 * ldin + k0 + 4 * q];
