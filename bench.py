@@ -123,8 +123,9 @@ class ClockSampler:
         mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
+        pw = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(rows)}
+                "power_w": float(np.median(pw)) if pw else None, "samples": len(rows)}
 
 
 # ----------------------------------------------------------------------------- dist
