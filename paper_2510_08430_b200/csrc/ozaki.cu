@@ -36,8 +36,15 @@ namespace {
 
 constexpr int BM = 128;                   // tile rows (i, A-operand rows, TMEM lanes)
 constexpr int BN = 64;                    // tile cols (j, B-operand rows, TMEM columns per accumulator)
-constexpr int BKB = 64;                   // K bytes per pipeline stage (one 64-byte swizzle row)
-constexpr int kStages = 2;
+#ifndef SR_OZ_BKB
+#define SR_OZ_BKB 64
+#endif
+// K bytes per pipeline stage = one swizzle row: 64 (64-byte swizzle, 2 stages of 86 KB) or
+// 32 (32-byte swizzle, one MMA K step per stage, 5 stages of 43 KB)
+constexpr int BKB = SR_OZ_BKB;
+constexpr int kStages = BKB == 64 ? 2 : 5;
+constexpr uint32_t kSwzLayout = BKB == 64 ? 4u : 6u;    // UMMA descriptor layout type: SWIZZLE_64B / _32B
+constexpr uint32_t kSwzSBO = 8u * BKB;                 // bytes between 8-row core-matrix groups
 constexpr int kASlice = BM * BKB;         // 8 KB
 constexpr int kBSlice = BN * BKB;         // 4 KB
 constexpr int kAStage = kSlices * kASlice;
@@ -146,10 +153,10 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
 // K-major operand, 64-byte swizzle: 8-row core groups 512 bytes apart (SBO), LBO unused (1),
-// descriptor version 1 (sm_100), layout type 4 = SWIZZLE_64B.
+// descriptor version 1 (sm_100), layout type 4 = SWIZZLE_64B (6 = SWIZZLE_32B).
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(kSwzSBO >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)kSwzLayout << 61);
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
@@ -893,7 +900,8 @@ sr_status make_map(CUtensorMap& m, void* base, long long Kp, long long ncols, in
   const cuuint32_t box[3] = {(cuuint32_t)BKB, (cuuint32_t)rows, (cuuint32_t)box_slices};
   const cuuint32_t es[3] = {1, 1, 1};
   const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, BKB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
