@@ -446,3 +446,25 @@ def test_library_graph_capture(sr):
     d_graph = step.replay()[0]
     torch.cuda.synchronize()
     assert torch.equal(d_graph, d_eager)
+
+
+@pytest.mark.parametrize("env", [
+    {"SR_PIPE": "1"},
+    {"SR_INSTRIP_LEFT": "0", "SR_TRSM_SPLIT": "0"},
+    {"SR_LOOKAHEAD": "1", "SR_SIDE_AFTER_NEXT": "0"},
+    {"SR_LOOKAHEAD": "0", "SR_PDL": "0"},
+], ids=["pipe", "right_looking_whole_trsm", "lookahead_all", "no_lookahead_no_pdl"])
+def test_switches_keep_parity(env):
+    """The measurement switches change scheduling only: the step, the block
+    solve and the full/NTK solves stay within tolerance under each non-default setting (run
+    in a child process, since the switches are read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_parity.py"),
+                        "-k", "block_solve_parity or step_and_step_host or full_and_ntk or graph_capture"],
+                       cwd=root, env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
