@@ -468,3 +468,22 @@ def test_switches_keep_parity(env):
                        cwd=root, env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.parametrize("m,n,k", [(70, 33, 129), (1, 64, 5), (130, 1, 64), (64, 64, 0)])
+def test_gram_nh_and_aHv(sr, m, n, k):
+    """sr_gram_nh (C = A B^H, FP64 DMMA) on ragged shapes and K = 0, and sr_aHv (alpha A^H v),
+    against numpy in complex128; A and B also as column slices of wider matrices."""
+    rng = np.random.default_rng(m * 1000 + n + k)
+    Aw = rng.standard_normal((m, k + 3)) + 1j * rng.standard_normal((m, k + 3))
+    Bw = rng.standard_normal((n, k + 5)) + 1j * rng.standard_normal((n, k + 5))
+    A, B = T(Aw)[:, 1:1 + k], T(Bw)[:, 2:2 + k]
+    C = torch.full((m, n), complex(7.0, 7.0), dtype=C128, device=dev())
+    sr.sr_gram_nh(A, B, C)
+    ref = Aw[:, 1:1 + k] @ Bw[:, 2:2 + k].conj().T if k else np.zeros((m, n))
+    assert rel(C.cpu().numpy(), ref) < 1e-14 if k else np.count_nonzero(C.cpu().numpy()) == 0
+    if k:
+        v = rng.standard_normal(m) + 1j * rng.standard_normal(m)
+        out = torch.empty(k, dtype=C128, device=dev())
+        sr.sr_aHv(A, T(v), -0.5, out)
+        assert rel(out.cpu().numpy(), -0.5 * (Aw[:, 1:1 + k].conj().T @ v)) < 1e-14
