@@ -57,3 +57,25 @@ def test_workload_inputs_are_seeded_and_in_sector():
     p = workloads.draw_params((100, 128), 0)
     sd = 0.1 / np.sqrt(100)
     assert abs(p[0][0].real.std() / sd - 1) < 0.05 and abs(p[0][0].imag.std() / sd - 1) < 0.05
+
+
+def test_bench_reference_arm_json_contract():
+    """bench.py --impl reference (the CPU-oracle arm of this tier) prints one JSON line with
+    the keys the driver reads, on the same config as the native arm."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0"], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "impl", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["workload"] == "heis_chain_N40"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
