@@ -487,3 +487,29 @@ def test_gram_nh_and_aHv(sr, m, n, k):
         out = torch.empty(k, dtype=C128, device=dev())
         sr.sr_aHv(A, T(v), -0.5, out)
         assert rel(out.cpu().numpy(), -0.5 * (Aw[:, 1:1 + k].conj().T @ v)) < 1e-14
+
+
+def test_bench_native_json_contract():
+    """bench.py (native arm, short run) prints one JSON line with the keys the driver and the
+    tier rules require: roofline {bound, achieved, peak, unit, frac, traffic}, e2e with the
+    per-step copy bytes, gpu_launches, clocks."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "2", "--warmup", "3",
+                        "--no-cpu-baseline", "--no-compare"], cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    rf = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in rf, k
+    assert 0.0 < rf["frac"] < 1.5 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["config"]["workload"] == "heis_chain_N40" and d["n_gpus"] == 1
