@@ -112,6 +112,16 @@ size_t block_solve_ws(int nblk, const int64_t* offs) {
   return a.used;
 }
 
+// FP64 engine's QGT Grams with TMA-staged K-slabs (SR_FP64_TMA=0: the cp.async kernel).
+bool fp64_tma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SR_FP64_TMA");
+    v = e ? atoi(e) != 0 : 1;
+  }
+  return v != 0;
+}
+
 sr_status block_qgt_impl(long long ns, int nblk, const int64_t* offs, const double2* A, long long lda,
                          double2* S, cudaStream_t st) {
   gram::ProbSet ps{};
@@ -122,7 +132,10 @@ sr_status block_qgt_impl(long long ns, int nblk, const int64_t* offs, const doub
     soff += n * n;
   }
   timer_begin("gram_tn", st);
-  const sr_status r = gram::launch<gram::TN, gram::HERM_STORE>(ps, st);
+  // every block is a column range of A: K-slabs staged by TMA (gram::tn_tma_kernel)
+  const sr_status r = fp64_tma() && ns > 0
+                          ? gram::launch_tn_tma<gram::HERM_STORE>(ps, A, lda, offs[nblk], ns, st)
+                          : gram::launch<gram::TN, gram::HERM_STORE>(ps, st);
   timer_end(st);
   return r;
 }
@@ -660,7 +673,8 @@ SR_API sr_status sr_full_qgt_solve(int64_t n_samples, int64_t n_p, const double*
   } else {
     gram::ProbSet ps{};
     gram::add_prob(ps, Ad, lda, Ad, lda, B.Fm, B.npad, (int)n_p, (int)n_p, n_samples, true);
-    SR_TRY((gram::launch<gram::TN, gram::HERM_STORE>(ps, st)));
+    if (fp64_tma() && n_samples > 0) SR_TRY((gram::launch_tn_tma<gram::HERM_STORE>(ps, Ad, lda, n_p, n_samples, st)));
+    else SR_TRY((gram::launch<gram::TN, gram::HERM_STORE>(ps, st)));
   }
   if (S_out) SR_TRY(copy_matrix(B.Fm, B.npad, reinterpret_cast<double2*>(S_out), n_p, n_p, n_p, st));
   B.F = reinterpret_cast<const double2*>(F);

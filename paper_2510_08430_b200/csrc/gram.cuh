@@ -11,6 +11,10 @@
 // a 3-stage cp.async pipeline (16-byte copies, zero-fill outside the matrix) into padded
 // shared-memory tiles whose strides make every fragment load bank-conflict free.
 #pragma once
+#include <cuda.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace sr {
@@ -255,6 +259,148 @@ __global__ void __launch_bounds__(kThreads, min_blocks<FL>()) tile_kernel(const 
     }
 }
 
+// ---------------------------------------------------------------- TN with TMA staging
+// The TN flavour (the QGT Grams: every problem a column range of ONE row-major matrix X)
+// with its K-slabs staged by TMA instead of cp.async: per stage and 64-column panel, eight
+// 2-D boxes of 16 rows x 8 complex (128 bytes, 128-byte swizzle), completing on an
+// mbarrier; one thread issues the copies.  Element (k, m) of a panel lives at
+//   (m / 8) * 2048 + k * 128 + ((m % 8) ^ (k % 8)) * 16
+// so the DMMA fragment loads (8 columns x 4 k per quarter-warp) stay bank-conflict free
+// without padding.  Rows past K and columns past the matrix read as zero (TMA OOB fill);
+// columns past a problem's range belong to its neighbour and only reach masked outputs.
+constexpr int TMA_PANEL = BK * BM * 16;            // 16 KB per 64-column panel
+constexpr int TMA_STAGES = 3;
+constexpr size_t kTmaSmem = (size_t)TMA_STAGES * 2 * TMA_PANEL + 1024 + 64;
+
+__device__ __forceinline__ double2 frag_sw(const uint8_t* panel, int m, int k) {
+  return *reinterpret_cast<const double2*>(panel + (m >> 3) * 2048 + k * 128 + (((m & 7) ^ (k & 7)) << 4));
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+      ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done)
+                 : "r"(bar), "r"(parity)
+                 : "memory");
+}
+
+template <int EP>
+__global__ void __launch_bounds__(kThreads, 2) tn_tma_kernel(const __grid_constant__ ProbSet ps,
+                                                             const __grid_constant__ CUtensorMap map,
+                                                             const double2* __restrict__ base) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + TMA_STAGES * 2 * TMA_PANEL);
+  int pi, I, J;
+  tile_of(ps, blockIdx.x, pi, I, J);
+  const Prob& P = ps.p[pi];
+  const int m0 = I * BM, n0 = J * BN;
+  const long long K = P.K;
+  const int KT = (int)((K + BK - 1) / BK);
+  // column coordinates (in doubles) of the two panels inside the matrix
+  const int ca = (int)(2 * ((P.A - base) + m0)), cb = (int)(2 * ((P.B - base) + n0));
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int lr = lane >> 2, lk = lane & 3;
+  auto issue = [&](int kt) {   // thread 0: slab kt into stage kt % TMA_STAGES
+    const int st = kt % TMA_STAGES;
+    const uint32_t bar = bar0 + 8 * st;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(2 * TMA_PANEL) : "memory");
+    const uint32_t da = sbase + st * 2 * TMA_PANEL, db = da + TMA_PANEL;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      tma2d(da + q * 2048, &map, ca + 16 * q, kt * BK, bar);
+      tma2d(db + q * 2048, &map, cb + 16 * q, kt * BK, bar);
+    }
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TMA_STAGES; s++)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0 + 8 * s));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&map) : "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int s = 0; s < TMA_STAGES - 1 && s < KT; s++) issue(s);
+
+  double acc_r[4][2][2], acc_i[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int b = 0; b < 2; b++) {
+      acc_r[a][b][0] = acc_r[a][b][1] = 0.0;
+      acc_i[a][b][0] = acc_i[a][b][1] = 0.0;
+    }
+#pragma unroll 1
+  for (int kt = 0; kt < KT; kt++) {
+    __syncthreads();   // every warp is done with slab kt-1, whose stage the next issue refills
+    if (threadIdx.x == 0 && kt + TMA_STAGES - 1 < KT) issue(kt + TMA_STAGES - 1);
+    const int st = kt % TMA_STAGES;
+    mbar_wait_parity(bar0 + 8 * st, (uint32_t)((kt / TMA_STAGES) & 1));
+    const uint8_t* a_s = sm + st * 2 * TMA_PANEL;
+    const uint8_t* b_s = a_s + TMA_PANEL;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double ar[4], ai[4], nai[4], br[2], bi[2];
+#pragma unroll
+      for (int mi = 0; mi < 4; mi++) {
+        const double2 v = frag_sw(a_s, wm * 32 + mi * 8 + lr, k4 + lk);
+        ar[mi] = v.x;
+        ai[mi] = -v.y;   // a(m,k) = conj(A[k][m])
+        nai[mi] = v.y;
+      }
+#pragma unroll
+      for (int ni = 0; ni < 2; ni++) {
+        const double2 v = frag_sw(b_s, wn * 16 + ni * 8 + lr, k4 + lk);
+        br[ni] = v.x;
+        bi[ni] = v.y;
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+        for (int ni = 0; ni < 2; ni++) {
+          dmma(acc_r[mi][ni][0], acc_r[mi][ni][1], ar[mi], br[ni]);
+          dmma(acc_i[mi][ni][0], acc_i[mi][ni][1], ar[mi], bi[ni]);
+          dmma(acc_r[mi][ni][0], acc_r[mi][ni][1], nai[mi], bi[ni]);
+          dmma(acc_i[mi][ni][0], acc_i[mi][ni][1], ai[mi], br[ni]);
+        }
+    }
+  }
+#pragma unroll
+  for (int mi = 0; mi < 4; mi++)
+#pragma unroll
+    for (int ni = 0; ni < 2; ni++) {
+      const int m = m0 + wm * 32 + mi * 8 + lr;
+      const int nb = n0 + wn * 16 + ni * 8 + 2 * lk;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int n = nb + h;
+        if (m >= P.M || n >= P.N) continue;
+        double2 v = make_double2(acc_r[mi][ni][h], acc_i[mi][ni][h]);
+        double2* c = P.C + (long long)m * P.ldc + n;
+        if (EP == HERM_STORE) {
+          if (I == J && m < n) continue;
+          if (m == n) v.y = 0.0;
+          *c = v;
+          if (m != n) P.C[(long long)n * P.ldc + m] = cconj(v);
+        } else if (EP == SUB) {
+          *c = csub(*c, v);
+        } else {
+          *c = v;
+        }
+      }
+    }
+}
+
 // Host helpers -----------------------------------------------------------------
 inline int tiles(long long n, int b) { return (int)((n + b - 1) / b); }
 
@@ -432,6 +578,49 @@ inline sr_status launch_skinny(ProbSet ps, cudaStream_t st, bool pdl = false) {
   if (total == 0) return SR_OK;
   if (kmax > 64) return launch_skinny_k<EP, SK_TM, true>(ps, total, st, pdl);
   return launch_skinny_k<EP, SK_TM, false>(ps, total, st, pdl);
+}
+
+using TmaEncode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// TN problems that are all column ranges of one row-major matrix X (ncols columns, K rows,
+// leading dimension ld complex) on the TMA-staged kernel.
+template <int EP>
+inline sr_status launch_tn_tma(const ProbSet& ps, const double2* X, long long ld, long long ncols, long long K,
+                               cudaStream_t st) {
+  if (ps.total_tiles == 0) return SR_OK;
+  static TmaEncode enc = nullptr;
+  if (!enc) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SR_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) {
+      set_error("cuTensorMapEncodeTiled unavailable");
+      return SR_ERR_CUDA;
+    }
+    enc = reinterpret_cast<TmaEncode>(p);
+  }
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)(2 * ncols), (cuuint64_t)std::max(1LL, K)};
+  const cuuint64_t strides[1] = {(cuuint64_t)(16 * ld)};
+  const cuuint32_t box[2] = {16, (cuuint32_t)BK};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double2*>(X), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (FP64 Gram): " + std::to_string((int)r));
+    return SR_ERR_CUDA;
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    SR_CUDA(cudaFuncSetAttribute(tn_tma_kernel<EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+    attr_set = true;
+  }
+  tn_tma_kernel<EP><<<(unsigned)ps.total_tiles, kThreads, kTmaSmem, st>>>(ps, map, X);
+  SR_LAUNCHED();
+  return SR_OK;
 }
 
 }  // namespace gram
