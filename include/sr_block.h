@@ -243,6 +243,39 @@ SR_API sr_status sr_block_solve(int n_blocks, const int64_t* block_offsets /*hos
                                 int32_t* info, void* workspace, size_t workspace_bytes,
                                 void* stream);
 
+/* sr_block_qgt_solve — stages (4) and (5) fused per block (the per-block schedule):
+ * for b = 0, 1, ...: S_b = A_b^H A_b (Eq. 3) is formed straight into block b's
+ * padded Cholesky matrix on the selected Gram engine and (S_b + lambda I) dtheta_b = -F_b is
+ * solved (§2, "Each block S_l is inverted independently") before block b+1's Gram.
+ * Same result as sr_block_qgt followed by sr_block_solve (same kernels, same order of every
+ * sum), but the workspace holds ONE block -- the largest -- instead of every S_b and its
+ * factor copy: configs[4]'s eight blocks need 10.6 GB + digit slices instead of 157 GB.
+ * Blocks run one after another (no S_b is kept; nothing to inspect).
+ *   A        complex [n_samples][lda], the centred, weighted Jacobian (stage 3 output)
+ *   F        complex [n_p];  dtheta complex [n_p] (out);  info int32 [1] (out) or NULL:
+ *            0, or the global row + 1 of the first non-positive pivot of the first
+ *            failing block.
+ * Workspace: sr_block_qgt_solve_workspace_bytes(n_samples, ...).  Errors as sr_block_solve. */
+SR_API size_t sr_block_qgt_solve_workspace_bytes(int64_t n_samples, int n_blocks,
+                                                 const int64_t* block_offsets /*host*/);
+SR_API sr_status sr_block_qgt_solve(int64_t n_samples, int n_blocks, const int64_t* block_offsets /*host*/,
+                                    const double* A, int64_t lda, const double* F, double lambda,
+                                    double* dtheta, int32_t* info, void* workspace,
+                                    size_t workspace_bytes, void* stream);
+
+/* sr_set_step_schedule — how sr_step / sr_step_host run stages (4)-(5):
+ * SR_SCHED_BATCHED (default): every S_b is formed (one grouped Gram launch), then all blocks
+ *   are factorised together on concurrent streams; sr_step_s_offset() locates the S blocks.
+ * SR_SCHED_PER_BLOCK: sr_block_qgt_solve (one block at a time, O(max n_b^2) memory); the
+ *   step workspace drops sum_b n_b^2 complex of S and all but one factor (configs[4] at
+ *   8192 samples: 42 GB instead of 189 GB); sr_step_s_offset() returns SIZE_MAX.
+ * Process-wide, read by the workspace queries too: query and call under the same setting.
+ * Returns the previous setting, or -1 for an unknown schedule (unchanged). */
+#define SR_SCHED_BATCHED 0
+#define SR_SCHED_PER_BLOCK 1
+SR_API int sr_set_step_schedule(int schedule);
+SR_API int sr_get_step_schedule(void);
+
 /* ------------------------------------------------------- comparison paths ---
  * sr_full_qgt_solve — PAPER.md §2 "S . delta theta = -F" with the full n_p x n_p QGT:
  *   S = A^H A formed in the workspace, (S + lambda I) dtheta = -F by Cholesky.
@@ -284,7 +317,8 @@ SR_API sr_status sr_aHv(int64_t n_rows, int64_t n_p, const double* A, int64_t ld
  *   theta complex [n_p], spins int8 [n_samples][N], bonds as in stage (2);
  *   dtheta complex [n_p] (out), energy complex [1] (out).
  * The workspace holds O/A, E_loc, S blocks and the factor storage; the S blocks sit
- * at offset sr_step_s_offset() of the workspace (for inspection). */
+ * at offset sr_step_s_offset() of the workspace (for inspection; SIZE_MAX under the
+ * per-block schedule, sr_set_step_schedule, which keeps no S). */
 SR_API size_t sr_step_workspace_bytes(int n_layers, const int32_t* widths /*host*/,
                                       int64_t n_samples, int64_t n_bonds);
 SR_API size_t sr_step_s_offset(int n_layers, const int32_t* widths /*host*/, int64_t n_samples,

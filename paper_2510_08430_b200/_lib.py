@@ -58,6 +58,10 @@ SIGNATURES = {
     "sr_get_gram_engine": (_i32, []),
     "sr_block_solve_workspace_bytes": (_sz, [_i32, _I64P]),
     "sr_block_solve": (_i32, [_i32, _I64P, _vp, _vp, _dbl, _vp, _vp, _vp, _sz, _vp]),
+    "sr_block_qgt_solve_workspace_bytes": (_sz, [_i64, _i32, _I64P]),
+    "sr_block_qgt_solve": (_i32, [_i64, _i32, _I64P, _vp, _i64, _vp, _dbl, _vp, _vp, _vp, _sz, _vp]),
+    "sr_set_step_schedule": (_i32, [_i32]),
+    "sr_get_step_schedule": (_i32, []),
     "sr_full_qgt_solve_workspace_bytes": (_sz, [_i64, _i64]),
     "sr_full_qgt_solve": (_i32, [_i64, _i64, _vp, _i64, _vp, _dbl, _vp, _vp, _vp, _vp, _sz, _vp]),
     "sr_ntk_solve_workspace_bytes": (_sz, [_i64, _i64]),
@@ -276,11 +280,42 @@ def sr_block_solve(offsets, S, F, lam, dtheta, info=None, workspace=None):
                               *_ws_args(ws), _stream(S.device)), "sr_block_solve")
 
 
+def sr_block_qgt_solve(A, offsets, F, lam, dtheta, info=None, workspace=None):
+    """Stages (4)+(5) one block at a time (include/sr_block.h): A may be a column slice."""
+    lib = load()
+    lda = _cols(A, "A")
+    nblk = len(offsets) - 1
+    off = _offsets(offsets)
+    for t, n in ((F, "F"), (dtheta, "dtheta")):
+        _dev(t, torch.complex128, n)
+        if t.numel() < offsets[-1]:
+            raise SRError(f"{n} shorter than n_p")
+    ws = _workspace(lib.sr_block_qgt_solve_workspace_bytes(A.shape[0], nblk, off), A.device, workspace)
+    _check(lib.sr_block_qgt_solve(A.shape[0], nblk, off, _ptr(A), lda, _ptr(F), float(lam), _ptr(dtheta), _ptr(info),
+                                  *_ws_args(ws), _stream(A.device)), "sr_block_qgt_solve")
+
+
+SCHED_BATCHED, SCHED_PER_BLOCK = 0, 1
+
+
+def sr_set_step_schedule(schedule):
+    """Schedule of sr_step's stages (4)-(5): SCHED_BATCHED or SCHED_PER_BLOCK."""
+    prev = int(load().sr_set_step_schedule(int(schedule)))
+    if prev < 0:
+        raise SRError(f"unknown step schedule {schedule}")
+    return prev
+
+
+def sr_get_step_schedule():
+    return int(load().sr_get_step_schedule())
+
+
 def sr_full_qgt_solve(A, F, lam, dtheta, S_out=None, info=None, workspace=None):
     lib = load()
     ns, npar = A.shape[0], F.shape[0]
+    lda = _cols(A, "A")
     ws = _workspace(lib.sr_full_qgt_solve_workspace_bytes(ns, npar), A.device, workspace)
-    _check(lib.sr_full_qgt_solve(ns, npar, _ptr(A), A.shape[1], _ptr(F), float(lam), _ptr(dtheta),
+    _check(lib.sr_full_qgt_solve(ns, npar, _ptr(A), lda, _ptr(F), float(lam), _ptr(dtheta),
                                  _ptr(S_out), _ptr(info), *_ws_args(ws), _stream(A.device)),
            "sr_full_qgt_solve")
 

@@ -32,19 +32,38 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit to an object file in parallel (one nvcc each), then
+    link the shared library (static cudart)."""
     if not force and up_to_date():
         return LIB
-    cmd = [NVCC, *FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+    jobs = []
+    for s in SOURCES:
+        obj = os.path.join(objdir, s.replace(".cu", ".o"))
+        cmd = [NVCC, *cflags, "-c", os.path.join(CSRC, s), "-o", obj]
+        jobs.append((cmd, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    log_txt, failed = "", False
+    for cmd, obj, p in jobs:
+        out, err = p.communicate()
+        log_txt += " ".join(cmd) + "\n" + out + err
+        failed |= p.returncode != 0
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+            *[o for _, o, _ in jobs], "-o", LIB + ".tmp"]
+    if not failed:
+        r = subprocess.run(link, capture_output=True, text=True)
+        log_txt += " ".join(link) + "\n" + r.stdout + r.stderr
+        failed = r.returncode != 0
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if r.returncode != 0:
-        sys.stderr.write(r.stderr)
+        f.write(log_txt)
+    if failed:
+        sys.stderr.write(log_txt[-6000:])
         raise RuntimeError(f"nvcc failed (see {log})")
     os.replace(LIB + ".tmp", LIB)
     if verbose:
-        sys.stderr.write(r.stderr)
+        sys.stderr.write(log_txt)
     return LIB
 
 

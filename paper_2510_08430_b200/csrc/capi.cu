@@ -162,10 +162,93 @@ sr_status block_solve_impl(int nblk, const int64_t* offs, const double2* S, cons
   return chol_solve(cs, lam, false, -1.0, st);
 }
 
+// The comparison solves' Grams run on the selected engine (sr_set_gram_engine); the int8
+// engine's digit slices follow the Cholesky workspace.
+size_t full_i8_ws(long long ns, long long n_p) {
+  if (ns < 1) return 0;
+  const int64_t o[2] = {0, n_p};
+  return oz::workspace_bytes(ns, 1, o);
+}
+
+size_t full_qgt_ws(long long ns, long long n_p) {
+  long long sz = n_p;
+  Arena a(nullptr, 0);
+  CholSet cs{};
+  carve_chol(a, cs, &sz, 1);
+  return round256(a.used) + full_i8_ws(ns, n_p);
+}
+
+// S = A^H A (n x n, the n columns of A at lda) formed straight into the padded Cholesky
+// matrix on the selected Gram engine, then (S + lambda I) out = -F.  keep_info: *info is
+// not reset (blocks solved one call at a time report the first failure); row_base: the
+// global row of column 0 in the reported pivot.
+sr_status gram_solve_one(long long ns, long long n, const double2* A, long long lda, const double2* F, double lam,
+                         double2* out, double2* S_out, int* info, bool keep_info, long long row_base, void* ws,
+                         size_t bytes, cudaStream_t st) {
+  long long sz = n;
+  Arena a(ws, bytes);
+  CholSet cs{};
+  cs.info = info;
+  cs.keep_info = keep_info;
+  carve_chol(a, cs, &sz, 1);
+  if (!a.ok()) {
+    set_error("gram + solve: workspace too small");
+    return SR_ERR_WORKSPACE;
+  }
+  CholBlock& B = cs.b[0];
+  B.row_base = row_base;
+  if (g_gram_engine == SR_GRAM_INT8 && ns > 0) {   // S straight into the padded factor matrix
+    const size_t used = round256(a.used);
+    const int64_t o[2] = {0, n};
+    SR_TRY(oz::block_qgt_i8(ns, 1, o, A, lda, B.Fm, static_cast<char*>(ws) + used, bytes > used ? bytes - used : 0,
+                            st, B.npad));
+  } else {
+    gram::ProbSet ps{};
+    gram::add_prob(ps, A, lda, A, lda, B.Fm, B.npad, (int)n, (int)n, ns, true);
+    timer_begin("gram_tn", st);
+    const sr_status r = fp64_tma() && ns > 0 ? gram::launch_tn_tma<gram::HERM_STORE>(ps, A, lda, n, ns, st)
+                                             : gram::launch<gram::TN, gram::HERM_STORE>(ps, st);
+    timer_end(st);
+    SR_TRY(r);
+  }
+  if (S_out) SR_TRY(copy_matrix(B.Fm, B.npad, S_out, n, n, n, st));
+  B.F = F;
+  B.out = out;
+  return chol_solve(cs, lam, true, -1.0, st);
+}
+
+// Stages (4)+(5) per block: block b's S_b is formed in its padded factor matrix and solved
+// before block b+1's Gram, so the workspace holds one block (the largest) instead of every
+// S_b plus its factor copy (sr_block_qgt_solve, the SR_SCHED_PER_BLOCK step schedule).
+size_t qgt_solve_ws(long long ns, int nblk, const int64_t* offs) {
+  size_t mx = 0;
+  for (int b = 0; b < nblk; b++) mx = std::max(mx, full_qgt_ws(ns, offs[b + 1] - offs[b]));
+  return round256(sizeof(int)) + mx;
+}
+
+sr_status qgt_solve_impl(long long ns, int nblk, const int64_t* offs, const double2* A, long long lda,
+                         const double2* F, double lam, double2* dtheta, int* info, void* ws, size_t bytes,
+                         cudaStream_t st) {
+  if (bytes < qgt_solve_ws(ns, nblk, offs)) {
+    set_error("sr_block_qgt_solve: workspace too small");
+    return SR_ERR_WORKSPACE;
+  }
+  if (info) SR_CUDA(cudaMemsetAsync(info, 0, sizeof(int), st));
+  char* rest = static_cast<char*>(ws) + round256(sizeof(int));
+  const size_t rbytes = bytes - round256(sizeof(int));
+  for (int b = 0; b < nblk; b++)
+    SR_TRY(gram_solve_one(ns, offs[b + 1] - offs[b], A + offs[b], lda, F + offs[b], lam, dtheta + offs[b], nullptr,
+                          info, true, offs[b], rest, rbytes, st));
+  return SR_OK;
+}
+
+int g_step_schedule = SR_SCHED_BATCHED;
+
 struct StepLayout {
   NetDesc net;
   std::vector<int64_t> offs;
   size_t log_psi, O, e_loc, energy, e_tilde, F, S, scratch, scratch_bytes, total, chol_off;
+  bool per_block;
   size_t h_theta, h_spins, h_bij, h_bj, h_dtheta, h_energy, host_total;
 };
 
@@ -249,16 +332,23 @@ sr_status step_layout(int n_layers, const int32_t* widths, long long ns, long lo
   L->energy = take(c16);
   L->e_tilde = take(ns * c16);
   L->F = take(net.n_p * c16);
-  L->S = take((size_t)s_elems * c16);
+  const bool per_block = g_step_schedule == SR_SCHED_PER_BLOCK;
+  L->per_block = per_block;
+  L->S = take(per_block ? 0 : (size_t)s_elems * c16);
   size_t scr = jacobian_ws(net, ns);
   scr = std::max(scr, local_energy_ws(net, ns, nb));
   scr = std::max(scr, center_force_ws(ns, net.n_p));
-  scr = std::max(scr, block_solve_ws(n_layers, L->offs.data()));
-  scr = std::max(scr, oz::workspace_bytes(ns, n_layers, L->offs.data()));
-  // pipelined int8 step: the digit slices of one block and the Cholesky workspace of all
-  // blocks are live at once
-  L->chol_off = round256(oz::workspace_bytes(ns, 1, largest_block(L->offs).data()));
-  scr = std::max(scr, L->chol_off + block_solve_ws(n_layers, L->offs.data()));
+  if (per_block) {
+    L->chol_off = 0;
+    scr = std::max(scr, qgt_solve_ws(ns, n_layers, L->offs.data()));
+  } else {
+    scr = std::max(scr, block_solve_ws(n_layers, L->offs.data()));
+    scr = std::max(scr, oz::workspace_bytes(ns, n_layers, L->offs.data()));
+    // pipelined int8 step: the digit slices of one block and the Cholesky workspace of all
+    // blocks are live at once
+    L->chol_off = round256(oz::workspace_bytes(ns, 1, largest_block(L->offs).data()));
+    scr = std::max(scr, L->chol_off + block_solve_ws(n_layers, L->offs.data()));
+  }
   L->scratch_bytes = round256(scr);
   L->scratch = take(L->scratch_bytes);
   L->total = off;
@@ -286,6 +376,10 @@ sr_status step_impl(const StepLayout& L, const double* theta, const int8_t* spin
   SR_TRY(jacobian_impl(net, theta, spins, ns, log_psi, O, net.n_p, scr, L.scratch_bytes, st));
   SR_TRY(local_energy_impl(net, theta, nb, bij, bj, spins, ns, log_psi, e_loc, scr, L.scratch_bytes, st));
   SR_TRY(center_force_impl(ns, net.n_p, O, net.n_p, nullptr, e_loc, energy, e_tilde, F, scr, L.scratch_bytes, st));
+  if (L.per_block)
+    return qgt_solve_impl(ns, net.L, L.offs.data(), reinterpret_cast<const double2*>(O), net.n_p,
+                          reinterpret_cast<const double2*>(F), lam, reinterpret_cast<double2*>(dtheta), nullptr, scr,
+                          L.scratch_bytes, st);
   if (g_gram_engine == SR_GRAM_INT8 && pipe_step())
     return pipelined_qgt_solve(net.L, L.offs.data(), ns, reinterpret_cast<const double2*>(O), net.n_p, S,
                                reinterpret_cast<const double2*>(F), lam, reinterpret_cast<double2*>(dtheta),
@@ -310,9 +404,10 @@ struct StepGraphKey {
   std::vector<int32_t> widths;
   long long ns, nb;
   double lam;
-  int engine;
+  int engine, schedule;
   bool operator==(const StepGraphKey& o) const {
-    return ws == o.ws && widths == o.widths && ns == o.ns && nb == o.nb && lam == o.lam && engine == o.engine;
+    return ws == o.ws && widths == o.widths && ns == o.ns && nb == o.nb && lam == o.lam && engine == o.engine &&
+           schedule == o.schedule;
   }
 };
 struct StepGraph {
@@ -629,21 +724,9 @@ SR_API sr_status sr_block_solve(int n_blocks, const int64_t* block_offsets, cons
                           workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
-// The comparison solves' Grams run on the selected engine (sr_set_gram_engine); the int8
-// engine's digit slices follow the Cholesky workspace.
-size_t full_i8_ws(long long ns, long long n_p) {
-  if (ns < 1) return 0;
-  const int64_t o[2] = {0, n_p};
-  return oz::workspace_bytes(ns, 1, o);
-}
-
 SR_API size_t sr_full_qgt_solve_workspace_bytes(int64_t n_samples, int64_t n_p) {
   if (n_p < 1 || n_samples < 0) return 0;
-  long long sz = n_p;
-  Arena a(nullptr, 0);
-  CholSet cs{};
-  carve_chol(a, cs, &sz, 1);
-  return round256(a.used) + full_i8_ws(n_samples, n_p);
+  return full_qgt_ws(n_samples, n_p);
 }
 
 SR_API sr_status sr_full_qgt_solve(int64_t n_samples, int64_t n_p, const double* A, int64_t lda, const double* F,
@@ -653,34 +736,36 @@ SR_API sr_status sr_full_qgt_solve(int64_t n_samples, int64_t n_p, const double*
   SR_CHECK_ARG(lda >= n_p, "lda < n_p");
   SR_CHECK_ARG(A && F && dtheta && workspace, "null pointer");
   SR_CHECK_ARG(lambda >= 0.0, "lambda < 0");
-  cudaStream_t st = (cudaStream_t)stream;
-  long long sz = n_p;
-  Arena a(workspace, workspace_bytes);
-  CholSet cs{};
-  cs.info = info;
-  carve_chol(a, cs, &sz, 1);
-  if (!a.ok()) {
-    set_error("sr_full_qgt_solve: workspace too small");
-    return SR_ERR_WORKSPACE;
-  }
-  CholBlock& B = cs.b[0];
-  const double2* Ad = reinterpret_cast<const double2*>(A);
-  if (g_gram_engine == SR_GRAM_INT8 && n_samples > 0) {   // S straight into the padded factor matrix
-    const size_t used = round256(a.used);
-    const int64_t o[2] = {0, n_p};
-    SR_TRY(oz::block_qgt_i8(n_samples, 1, o, Ad, lda, B.Fm, static_cast<char*>(workspace) + used,
-                            workspace_bytes > used ? workspace_bytes - used : 0, st, B.npad));
-  } else {
-    gram::ProbSet ps{};
-    gram::add_prob(ps, Ad, lda, Ad, lda, B.Fm, B.npad, (int)n_p, (int)n_p, n_samples, true);
-    if (fp64_tma() && n_samples > 0) SR_TRY((gram::launch_tn_tma<gram::HERM_STORE>(ps, Ad, lda, n_p, n_samples, st)));
-    else SR_TRY((gram::launch<gram::TN, gram::HERM_STORE>(ps, st)));
-  }
-  if (S_out) SR_TRY(copy_matrix(B.Fm, B.npad, reinterpret_cast<double2*>(S_out), n_p, n_p, n_p, st));
-  B.F = reinterpret_cast<const double2*>(F);
-  B.out = reinterpret_cast<double2*>(dtheta);
-  return chol_solve(cs, lambda, true, -1.0, st);
+  return gram_solve_one(n_samples, n_p, reinterpret_cast<const double2*>(A), lda, reinterpret_cast<const double2*>(F),
+                        lambda, reinterpret_cast<double2*>(dtheta), reinterpret_cast<double2*>(S_out), info, false, 0,
+                        workspace, workspace_bytes, (cudaStream_t)stream);
 }
+
+SR_API size_t sr_block_qgt_solve_workspace_bytes(int64_t n_samples, int n_blocks, const int64_t* block_offsets) {
+  if (n_samples < 0 || !valid_offsets(n_blocks, block_offsets)) return 0;
+  return qgt_solve_ws(n_samples, n_blocks, block_offsets);
+}
+
+SR_API sr_status sr_block_qgt_solve(int64_t n_samples, int n_blocks, const int64_t* block_offsets, const double* A,
+                                    int64_t lda, const double* F, double lambda, double* dtheta, int32_t* info,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(valid_offsets(n_blocks, block_offsets), "block_offsets must start at 0 and increase; 1..24 blocks");
+  SR_CHECK_ARG(n_samples >= 0 && lda >= block_offsets[n_blocks], "lda < n_p");
+  SR_CHECK_ARG(block_offsets[n_blocks] < (1LL << 31) / oz::kSlices, "n_p too large for the slice tensor map");
+  SR_CHECK_ARG(A && F && dtheta && workspace, "null pointer");
+  SR_CHECK_ARG(lambda >= 0.0, "lambda < 0");
+  return qgt_solve_impl(n_samples, n_blocks, block_offsets, reinterpret_cast<const double2*>(A), lda,
+                        reinterpret_cast<const double2*>(F), lambda, reinterpret_cast<double2*>(dtheta), info,
+                        workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+SR_API int sr_set_step_schedule(int schedule) {
+  if (schedule != SR_SCHED_BATCHED && schedule != SR_SCHED_PER_BLOCK) return -1;
+  const int prev = g_step_schedule;
+  g_step_schedule = schedule;
+  return prev;
+}
+SR_API int sr_get_step_schedule(void) { return g_step_schedule; }
 
 SR_API size_t sr_ntk_solve_workspace_bytes(int64_t n_samples, int64_t n_p) {
   if (n_samples < 1 || n_p < 1) return 0;
@@ -737,7 +822,7 @@ SR_API size_t sr_step_workspace_bytes(int n_layers, const int32_t* widths, int64
 SR_API size_t sr_step_s_offset(int n_layers, const int32_t* widths, int64_t n_samples, int64_t n_bonds) {
   StepLayout L;
   if (n_samples < 1 || n_bonds < 0 || step_layout(n_layers, widths, n_samples, n_bonds, &L) != SR_OK) return 0;
-  return L.S;
+  return L.per_block ? SIZE_MAX : L.S;
 }
 
 SR_API sr_status sr_step(int n_layers, const int32_t* widths, const double* theta, const int8_t* spins,
@@ -795,7 +880,7 @@ SR_API sr_status sr_step_host(int n_layers, const int32_t* widths, const double*
     SR_CUDA(cudaMemcpyAsync(bj, bond_j_h, (size_t)n_bonds * sizeof(double), cudaMemcpyHostToDevice, st));
   }
   StepGraphKey key{workspace, std::vector<int32_t>(widths, widths + n_layers + 1), n_samples, n_bonds, lambda,
-                   g_gram_engine};
+                   g_gram_engine, g_step_schedule};
   SR_TRY(step_graphed(L, key, theta, spins, n_samples, n_bonds, bij, bj, lambda, dtheta, energy, ws, st));
   SR_CUDA(cudaMemcpyAsync(dtheta_h, dtheta, np * c16, cudaMemcpyDeviceToHost, st));
   if (energy_h) SR_CUDA(cudaMemcpyAsync(energy_h, energy, c16, cudaMemcpyDeviceToHost, st));

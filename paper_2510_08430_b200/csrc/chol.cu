@@ -527,7 +527,7 @@ sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStr
     set_error("chol_solve: info must be null with ready events");
     return SR_ERR_INVALID;
   }
-  if (cs.info) SR_CUDA(cudaMemsetAsync(cs.info, 0, sizeof(int), st));
+  if (cs.info && !cs.keep_info) SR_CUDA(cudaMemsetAsync(cs.info, 0, sizeof(int), st));
   auto init_grid = [](const CholBlock& B, int nb) {
     return dim3((unsigned)std::min<long long>((B.npad * B.npad + 255) / 256, 2 * kNumSMs), (unsigned)nb);
   };

@@ -23,6 +23,7 @@ struct CholBlock {
 struct CholSet {
   int count;
   int* info;
+  bool keep_info;   // true: do not reset *info (a caller solving blocks one call at a time)
   CholBlock b[kMaxBlocks];
 };
 

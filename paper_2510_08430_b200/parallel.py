@@ -12,11 +12,15 @@ ShardedStep, rank r of G, owning samples [r*N_s/G, (r+1)*N_s/G):
      reduce(SUM, dst=owner(b)) per block; owners hold contiguous, cost-balanced block ranges
   5. owners: sr_block_solve of their blocks; dtheta all_reduce(SUM) (non-owners hold 0)
 The arithmetic is the C ABI's; this module only moves buffers.  `ops` is injectable so
-the collective pattern can be exercised on CPU with gloo (tests/test_parallel_gloo.py).
+the collective pattern can be exercised on CPU with gloo (tests/test_parallel_gloo.py), and
+`comm` is injectable so that G ranks can run as G threads of one process on one GPU
+(LoopbackComm: the collectives are host-side copies and sums between kernels, no kernel ever
+waits on another; tests/test_gpu_loopback.py).
 """
 from __future__ import annotations
 
 import os
+import threading
 
 import numpy as np
 import torch
@@ -29,7 +33,8 @@ STAGES = ("jacobian", "local_energy", "center_force", "block_qgt", "block_solve"
 class CudaOps:
     """The C-ABI stage calls with one shared, preallocated workspace."""
 
-    def __init__(self, widths, n_local, n_bonds, device, gram_engine="int8", solve_offsets=None):
+    def __init__(self, widths, n_local, n_bonds, device, gram_engine="int8", solve_offsets=None,
+                 schedule="batched"):
         if gram_engine not in ("int8", "fp64"):
             raise ValueError(f"gram_engine must be 'int8' or 'fp64', got {gram_engine!r}")
         lib = sr.load()
@@ -37,6 +42,17 @@ class CudaOps:
         n_p = sr.n_params(widths)
         offs = sr.block_offsets(widths)
         self.gram_engine = gram_engine
+        if schedule == "per_block":   # stages (4)+(5) one block at a time: one block's factor
+            prev = sr.sr_set_gram_engine(sr.GRAM_INT8 if gram_engine == "int8" else sr.GRAM_FP64)
+            try:
+                qs = lib.sr_block_qgt_solve_workspace_bytes(n_local, len(offs) - 1, sr._offsets(offs))
+            finally:
+                sr.sr_set_gram_engine(prev)
+            need = max(lib.sr_jacobian_workspace_bytes(L, wa, n_local),
+                       lib.sr_local_energy_workspace_bytes(L, wa, n_local, n_bonds),
+                       lib.sr_center_force_workspace_bytes(n_local, n_p), qs)
+            self.ws = torch.empty(int(need), dtype=torch.uint8, device=device)
+            return
         need = max(
             lib.sr_jacobian_workspace_bytes(L, wa, n_local),
             lib.sr_local_energy_workspace_bytes(L, wa, n_local, n_bonds),
@@ -79,6 +95,14 @@ class CudaOps:
     def block_solve(self, offs, S, F, lam, dtheta, info=None):
         need = sr.load().sr_block_solve_workspace_bytes(len(offs) - 1, sr._offsets(offs))
         sr.sr_block_solve(offs, S, F, lam, dtheta, info=info, workspace=self._ws(need))
+
+    def block_qgt_solve(self, A, offs, F, lam, dtheta, info=None):
+        prev = sr.sr_set_gram_engine(sr.GRAM_INT8 if self.gram_engine == "int8" else sr.GRAM_FP64)
+        try:
+            need = sr.load().sr_block_qgt_solve_workspace_bytes(A.shape[0], len(offs) - 1, sr._offsets(offs))
+            sr.sr_block_qgt_solve(A, offs, F, lam, dtheta, info=info, workspace=self._ws(need))
+        finally:
+            sr.sr_set_gram_engine(prev)
 
     def gram_nh(self, A, B, C):
         sr.sr_gram_nh(A, B, C)
@@ -163,16 +187,26 @@ def _rec(events, i, stream):
         events[i].record(stream)
 
 
+SCHEDULES = ("batched", "per_block")
+
+
 class LocalStep:
-    """The whole step on one GPU, stage by stage through the C ABI."""
+    """The whole step on one GPU, stage by stage through the C ABI.
 
-    STAGES = STAGES
+    schedule "batched": stage (4) for all blocks (one grouped Gram launch), then stage (5)
+    for all blocks together (concurrent streams) -- every S_b is kept.  "per_block":
+    sr_block_qgt_solve, each block's Gram written into its factor matrix and solved before
+    the next block's Gram (one block's memory; configs[4] on one GPU)."""
 
-    def __init__(self, widths, spins, bij, bj, lam, device, ops=None, gram_engine="int8"):
+    def __init__(self, widths, spins, bij, bj, lam, device, ops=None, gram_engine="int8", schedule="batched"):
+        if schedule not in SCHEDULES:
+            raise ValueError(f"schedule must be one of {SCHEDULES}, got {schedule!r}")
         self.lam = lam
+        self.schedule = schedule
+        self.STAGES = STAGES if schedule == "batched" else STAGES[:3] + ("block_qgt_solve",)
         self.device = torch.device(device)
-        self.buf = _Buffers(widths, spins, bij, bj, self.device)
-        self.ops = ops or CudaOps(widths, spins.shape[0], len(bj), self.device, gram_engine)
+        self.buf = _Buffers(widths, spins, bij, bj, self.device, full_s=schedule == "batched")
+        self.ops = ops or CudaOps(widths, spins.shape[0], len(bj), self.device, gram_engine, schedule=schedule)
 
     def run(self, theta, events=None):
         b, o = self.buf, self.ops
@@ -184,6 +218,10 @@ class LocalStep:
         _rec(events, 2, st)
         o.center_force(b.O, b.e_loc, b.energy, b.e_tilde, b.F)
         _rec(events, 3, st)
+        if self.schedule == "per_block":
+            o.block_qgt_solve(b.O, b.offs, b.F, self.lam, b.dtheta)
+            _rec(events, 4, st)
+            return b.dtheta, b.energy
         o.block_qgt(b.O, b.offs, b.S)
         _rec(events, 4, st)
         o.block_solve(b.offs, b.S, b.F, self.lam, b.dtheta)
@@ -214,14 +252,204 @@ class LocalStep:
         return self.buf.dtheta, self.buf.energy
 
 
+class _Done:
+    """Work handle of a collective that completed when it was called."""
+
+    def wait(self):
+        return None
+
+
+class TorchComm:
+    """The collectives ShardedStep uses, over a torch.distributed group (NCCL on GPUs)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+
+    def all_gather(self, out_list, t):
+        self.dist.all_gather(out_list, t, group=self.group)
+
+    def all_reduce(self, t, async_op=False):
+        return self.dist.all_reduce(t, group=self.group, async_op=async_op)
+
+    def reduce(self, t, dst, async_op=False):
+        return self.dist.reduce(t, dst=dst, group=self.group, async_op=async_op)
+
+    def broadcast(self, t, src):
+        self.dist.broadcast(t, src=src, group=self.group)
+
+    @staticmethod
+    def _real(t):
+        # complex buffers travel as their (re, im) float64 pairs (not every backend takes complex)
+        return torch.view_as_real(t) if t.is_complex() else t
+
+    def gather(self, t, out_list, dst):
+        """out_list (on dst only, else None): one tensor per rank, each t's shape."""
+        self.dist.gather(self._real(t), gather_list=None if out_list is None else [self._real(x) for x in out_list],
+                         dst=dst, group=self.group)
+
+    def exchange(self, sends, recvs):
+        """Point-to-point: sends [(tensor, peer)], recvs [(tensor, peer)], all posted at once."""
+        ops = [self.dist.P2POp(self.dist.isend, self._real(t), p, group=self.group) for t, p in sends]
+        ops += [self.dist.P2POp(self.dist.irecv, self._real(t), p, group=self.group) for t, p in recvs]
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+
+
+class LoopbackHub:
+    """Shared state of G LoopbackComm ranks run as G threads of one process (one GPU).
+
+    Every collective is a rendezvous: each rank synchronises its stream (its operand is
+    complete), deposits a reference, waits for all ranks, reads what it needs (copies and sums
+    in rank order, so every rank gets bit-identical results, as NCCL's would be across ranks),
+    synchronises, and waits again before the operands may be reused.  No kernel ever waits on
+    another rank's kernel: the waiting happens on the host between launches.  Library calls
+    are serialised by `lock` (libsrblock.so's side-stream pool is process state)."""
+
+    def __init__(self, world):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [None] * world
+        self.lock = threading.RLock()
+        self.mail = {}
+        self.cv = threading.Condition()
+
+
+class LoopbackComm:
+    def __init__(self, hub, rank):
+        self.hub, self.rank = hub, rank
+
+    def _post(self, t):
+        if t is not None and t.is_cuda:
+            torch.cuda.current_stream(t.device).synchronize()
+        self.hub.slots[self.rank] = t
+        self.hub.barrier.wait()
+        return list(self.hub.slots)
+
+    def _done(self, t):
+        if t is not None and t.is_cuda:
+            torch.cuda.current_stream(t.device).synchronize()
+        self.hub.barrier.wait()
+        return _Done()
+
+    @staticmethod
+    def _sum(slots):
+        acc = slots[0].clone()
+        for x in slots[1:]:
+            acc += x
+        return acc
+
+    def all_gather(self, out_list, t):
+        slots = self._post(t)
+        for q, x in enumerate(slots):
+            out_list[q].copy_(x)
+        self._done(t)
+
+    def all_reduce(self, t, async_op=False):
+        acc = self._sum(self._post(t))
+        self.hub.barrier.wait()            # every rank has read every operand
+        t.copy_(acc)
+        return self._done(t)
+
+    def reduce(self, t, dst, async_op=False):
+        slots = self._post(t)
+        acc = self._sum(slots) if self.rank == dst else None
+        self.hub.barrier.wait()
+        if acc is not None:
+            t.copy_(acc)
+        return self._done(t)
+
+    def broadcast(self, t, src):
+        slots = self._post(t)
+        if self.rank != src:
+            t.copy_(slots[src])
+        self._done(t)
+
+    def gather(self, t, out_list, dst):
+        slots = self._post(t)
+        if self.rank == dst:
+            for q, x in enumerate(slots):
+                out_list[q].copy_(x)
+        self._done(t)
+
+    def exchange(self, sends, recvs):
+        hub = self.hub
+        if sends and sends[0][0].is_cuda:
+            torch.cuda.current_stream(sends[0][0].device).synchronize()
+        with hub.cv:
+            for t, p in sends:
+                hub.mail.setdefault((self.rank, p), []).append(t)
+            hub.cv.notify_all()
+        for t, p in recvs:
+            with hub.cv:
+                hub.cv.wait_for(lambda: hub.mail.get((p, self.rank)))
+                x = hub.mail[(p, self.rank)].pop(0)
+            t.copy_(x)
+        if recvs and recvs[0][0].is_cuda:
+            torch.cuda.current_stream(recvs[0][0].device).synchronize()
+        hub.barrier.wait()                 # the senders' buffers may be reused after this
+
+
+class _LockedOps:
+    """Serialises the library calls of loopback ranks (see LoopbackHub)."""
+
+    def __init__(self, ops, lock):
+        self._ops, self._lock = ops, lock
+
+    def __getattr__(self, name):
+        fn = getattr(self._ops, name)
+        if not callable(fn):
+            return fn
+
+        def call(*a, **k):
+            with self._lock:
+                return fn(*a, **k)
+        return call
+
+
+def run_loopback(world, make_rank, work):
+    """Run `world` ranks as threads on this process's GPU: make_rank(rank, comm, lock) builds a
+    rank's object (e.g. a ShardedStep with comm=comm and ops=locked ops), then work(rank, obj)
+    runs in every thread; returns [work's result per rank].  A failure on any rank aborts the
+    barrier so the other threads do not hang, and is re-raised here."""
+    hub = LoopbackHub(world)
+    out, errs = [None] * world, []
+
+    def body(r):
+        try:
+            obj = make_rank(r, LoopbackComm(hub, r), hub.lock)
+            out[r] = work(r, obj)
+        except BaseException as exc:       # noqa: BLE001 -- reported below
+            errs.append(exc)
+            hub.barrier.abort()
+            with hub.cv:
+                hub.cv.notify_all()
+
+    threads = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errs:
+        raise errs[0]
+    return out
+
+
+def locked(ops, lock):
+    return _LockedOps(ops, lock)
+
+
 class ShardedStep:
-    """Sample-sharded step over a torch.distributed process group (NCCL on GPUs)."""
+    """Sample-sharded step over a process group (NCCL on GPUs via TorchComm; LoopbackComm
+    for G ranks as threads of one process)."""
 
     STAGES = STAGES
 
     def __init__(self, widths, spins_all, bij, bj, lam, rank, world, device, ops=None, group=None,
-                 gram_engine="int8", per_block_gram=None):
+                 gram_engine="int8", per_block_gram=None, comm=None):
         self.lam = lam
+        self.comm = comm if comm is not None else TorchComm(group)
         self.rank, self.world = rank, world
         # per-block Gram launches, each followed by its asynchronous reduce (default when
         # partial S_b travel, world > 1); one grouped launch otherwise
@@ -250,8 +478,7 @@ class ShardedStep:
         self.owned = list(range(olo, ohi))
 
     def run(self, theta, events=None):
-        import torch.distributed as dist
-        b, o, g = self.buf, self.ops, self.group
+        b, o, c = self.buf, self.ops, self.comm
         st = torch.cuda.current_stream(self.device) if self.device.type == "cuda" else None
         _rec(events, 0, st)
         o.jacobian(b.widths, theta, b.spins, b.log_psi, b.O)
@@ -259,17 +486,17 @@ class ShardedStep:
         o.local_energy(b.widths, theta, b.bij, b.bj, b.spins, b.log_psi, b.e_loc)
         _rec(events, 2, st)
         o.column_moments(b.O, b.e_loc, self.n_total, self.moments)
-        dist.all_gather(list(self.moments_all.unbind(0)), self.moments, group=g)
+        c.all_gather(list(self.moments_all.unbind(0)), self.moments)
         o.center_force_global(b.O, b.e_loc, self.n_total, self.moments_all, b.energy, b.e_tilde, b.F)
         # the force all-reduce and each block's reduce to its owner run asynchronously: block
         # b's partial S travels while the Gram of block b+1 is computed
-        f_work = dist.all_reduce(b.F, group=g, async_op=True)
+        f_work = c.all_reduce(b.F, async_op=True)
         _rec(events, 3, st)
         nblk = len(b.offs) - 1
         if not self.per_block_gram:   # one grouped Gram launch, then the reduces
             o.block_qgt(b.O, b.offs, b.S)
-            works = [dist.reduce(b.s_block(blk), dst=block_owner(blk, self.world, self.sizes), group=g,
-                                 async_op=True) for blk in range(nblk)]
+            works = [c.reduce(b.s_block(blk), dst=block_owner(blk, self.world, self.sizes), async_op=True)
+                     for blk in range(nblk)]
         else:
             works, pending, k = [], [None, None], 0
             olo = self.ranges[self.rank][0]
@@ -287,7 +514,7 @@ class ShardedStep:
                         pending[j].wait()
                     target = self.staging[j][:n * n]
                 o.block_qgt(b.O[:, lo:hi], [0, n], target)
-                wk = dist.reduce(target, dst=owner, group=g, async_op=True)
+                wk = c.reduce(target, dst=owner, async_op=True)
                 if owner != self.rank:
                     pending[j] = wk
                 works.append(wk)
@@ -306,63 +533,101 @@ class ShardedStep:
                 spos = sum(n * n for n in self.sizes[:olo])
                 s_own = b.S[spos:spos + slen]
             o.block_solve(self.own_offs, s_own, b.F[lo:hi], self.lam, b.dtheta[lo:hi])
-        dist.all_reduce(b.dtheta, group=g)
+        c.all_reduce(b.dtheta)
         _rec(events, 5, st)
         return b.dtheta, b.energy
 
     # --- comparison paths, sharded the same way (north_star); call after run() ---
     def full_qgt_solve(self):
         """Full-QGT solve with samples sharded: each rank's partial S = A_r^H A_r over all n_p
-        columns, NCCL reduce to rank 0, which solves (S + lambda I) dtheta = -F (one blocked
-        Cholesky); dtheta broadcast.  Returns dtheta (every rank)."""
-        import torch.distributed as dist
-        b, o, g = self.buf, self.ops, self.group
+        columns, reduced to rank 0, which solves (S + lambda I) dtheta = -F (one blocked
+        Cholesky); dtheta broadcast.  Returns dtheta (every rank).  (Rank 0 holds all of S:
+        n_p^2 complex; see dist_full_qgt_solve for S distributed by block rows.)"""
+        b, o, c = self.buf, self.ops, self.comm
         n = b.n_p
         S = torch.empty(n * n, dtype=torch.complex128, device=self.device)
         o.block_qgt(b.O, [0, n], S)
-        dist.reduce(S, dst=0, group=g)
+        c.reduce(S, dst=0)
         d = torch.zeros(n, dtype=torch.complex128, device=self.device)
         if self.rank == 0:
             o.block_solve([0, n], S, b.F, self.lam, d)
-        dist.broadcast(d, src=0, group=g)
+        c.broadcast(d, src=0)
         return d
 
+    @staticmethod
+    def ntk_schedule(G):
+        """Ring schedule of the NTK block products: at step t = 0..G//2 rank r receives A_s,
+        s = (r - t) mod G, and computes the lower-triangle block T_{max(r,s), min(r,s)}; at
+        t = G/2 (G even) only ranks r >= G/2 receive, so every unordered pair {r, s} is formed
+        exactly once and each rank forms about G/2 + 1 blocks.  Returns [(t, recv_from or
+        None, send_to or None)] per rank."""
+        out = []
+        for r in range(G):
+            steps = [(0, None, None)]
+            for t in range(1, G // 2 + 1):
+                recv = (r - t) % G
+                send = (r + t) % G
+                if 2 * t == G:
+                    recv = recv if r >= G // 2 else None
+                    send = send if r < G // 2 else None
+                steps.append((t, recv, send))
+            out.append(steps)
+        return out
+
     def ntk_solve(self):
-        """Sample-space (NTK / MinSR) solve with samples sharded: T = A A^H assembled by
-        block rows -- rank r computes T_r,s = A_r A_s^H as each rank's A_s is broadcast in
-        turn -- gathered to rank 0 with the residuals e, which solves (T + lambda I) y = e;
-        y is broadcast and each rank forms -A_r^H y_r, summed by an all-reduce.  Returns
-        dtheta (every rank)."""
-        import torch.distributed as dist
-        b, o, g = self.buf, self.ops, self.group
-        c = torch.complex128
+        """Sample-space (NTK / MinSR) solve with samples sharded (§1): T = A A^H by
+        blocks T_{r,s} = A_r A_s^H, only the lower block triangle, each pair formed once by the
+        ring schedule (ntk_schedule: A travels point to point, G(G-1)/2 transfers of one shard
+        in all instead of a broadcast of every shard to every rank); the blocks and residuals
+        are gathered to rank 0 only, which solves (T + lambda I) y = e; -y is broadcast and
+        each rank forms A_r^H (-y_r), summed by an all-reduce.  Returns dtheta (every rank)."""
+        b, o, c = self.buf, self.ops, self.comm
+        cd = torch.complex128
         N, G, r = self.n_total, self.world, self.rank
         rows = [shard_range(N, q, G) for q in range(G)]
         lo, hi = rows[r]
-        T_r = torch.empty(hi - lo, N, dtype=c, device=self.device)
-        for q, (qlo, qhi) in enumerate(rows):
-            A_q = b.O if q == r else torch.empty(qhi - qlo, b.n_p, dtype=c, device=self.device)
-            dist.broadcast(A_q, src=q, group=g)
-            if qhi > qlo and hi > lo:
-                o.gram_nh(b.O, A_q, T_r[:, qlo:qhi])
         mx = max(qhi - qlo for qlo, qhi in rows)
-        T_pad = torch.zeros(mx, N, dtype=c, device=self.device)
-        T_pad[:hi - lo] = T_r
-        e_pad = torch.zeros(mx, dtype=c, device=self.device)
+        sched = self.ntk_schedule(G)
+        pack = torch.zeros(len(sched[r]), mx, mx, dtype=cd, device=self.device)
+        for t, src, dst in sched[r]:
+            if t == 0:
+                if hi > lo:
+                    o.gram_nh(b.O, b.O, pack[0, :hi - lo, :hi - lo])
+                continue
+            A_s = None
+            if src is not None:
+                slo, shi = rows[src]
+                A_s = torch.empty(shi - slo, b.n_p, dtype=cd, device=self.device)
+            c.exchange([(b.O, dst)] if dst is not None else [], [(A_s, src)] if src is not None else [])
+            if src is not None and A_s.shape[0] and hi > lo:
+                big, small = (b.O, A_s) if r > src else (A_s, b.O)
+                o.gram_nh(big, small, pack[t, :big.shape[0], :small.shape[0]])
+        e_pad = torch.zeros(mx, dtype=cd, device=self.device)
         e_pad[:hi - lo] = b.e_tilde
-        T_all = [torch.empty_like(T_pad) for _ in range(G)]
-        e_all = [torch.empty_like(e_pad) for _ in range(G)]
-        dist.all_gather(T_all, T_pad, group=g)
-        dist.all_gather(e_all, e_pad, group=g)
-        z = torch.empty(N, dtype=c, device=self.device)
+        packs = [torch.empty_like(pack) for _ in range(G)] if r == 0 else None
+        e_all = [torch.empty_like(e_pad) for _ in range(G)] if r == 0 else None
+        c.gather(pack, packs, dst=0)
+        c.gather(e_pad, e_all, dst=0)
+        del pack
+        z = torch.empty(N, dtype=cd, device=self.device)
         if r == 0:
-            T = torch.cat([T_all[q][:qhi - qlo] for q, (qlo, qhi) in enumerate(rows)]).reshape(-1)
+            T = torch.zeros(N, N, dtype=cd, device=self.device)   # the upper block triangle stays 0
+            for q in range(G):
+                for t, src, _ in sched[q]:
+                    s_ = q if t == 0 else src
+                    if s_ is None:
+                        continue
+                    bi, sm = max(q, s_), min(q, s_)
+                    (blo, bhi), (slo, shi) = rows[bi], rows[sm]
+                    T[blo:bhi, slo:shi] = packs[q][t, :bhi - blo, :shi - slo]   # lower triangle only
             e = torch.cat([e_all[q][:qhi - qlo] for q, (qlo, qhi) in enumerate(rows)])
-            o.block_solve([0, N], T, e, self.lam, z)   # z = -(T + lambda I)^{-1} e
-        dist.broadcast(z, src=0, group=g)
-        d = torch.empty(b.n_p, dtype=c, device=self.device)
+            del packs
+            o.block_solve([0, N], T.reshape(-1), e, self.lam, z)   # z = -(T + lambda I)^{-1} e (lower T)
+            del T
+        c.broadcast(z, src=0)
+        d = torch.empty(b.n_p, dtype=cd, device=self.device)
         o.aHv(b.O, z[lo:hi].contiguous(), 1.0, d)     # -A_r^H y_r = A_r^H z_r
-        dist.all_reduce(d, group=g)
+        c.all_reduce(d)
         return d
 
     # --- CUDA graph of the whole sharded step, NCCL collectives included (they are captured

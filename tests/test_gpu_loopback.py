@@ -1,0 +1,139 @@
+"""Multi-rank sample-sharded step with the REAL kernels on one GPU: G ranks of
+parallel.ShardedStep run as G threads of this process (parallel.run_loopback), each with its
+own buffers and CudaOps, the collectives done by parallel.LoopbackComm (host-side rendezvous:
+copies and rank-ordered sums between kernel launches; no kernel waits on another rank's).
+
+This exercises exactly the dataflow a G-GPU NCCL run executes -- the double-double moment
+all-gather and the n_parts = G centring (sr_column_moments / sr_center_force_global), the
+force all-reduce, per-block partial Grams reduced to cost-balanced owners, the owners'
+solves, the dtheta all-reduce, and the sharded NTK / full-QGT comparison paths -- with
+libsrblock.so's kernels, for G = 2, 4, 8.  Only one GPU is available here, so the NCCL
+transport itself is covered by tests/test_gpu_sharded.py (one rank) and the collective
+pattern on gloo by tests/test_parallel_gloo.py.
+
+Bars: dtheta within 1e-11 of the single-GPU LocalStep (same kernels, different summation
+order of the sharded reductions), energy within 1e-13; configs[0] also against the oracle
+(1e-9, north_star).
+"""
+import numpy as np
+import pytest
+import torch
+
+import workloads
+from oracle import estimators, hamiltonian, network, solvers
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(cfg, ns=None):
+    import paper_2510_08430_b200 as sr
+    sr.load()
+    w = workloads.CONFIGS[cfg] if ns is None else workloads.CONFIGS[cfg].with_samples(ns)
+    spins, params = workloads.make_inputs(w)
+    ij, jj = sr.lattice.for_workload(w)
+    dev = torch.device("cuda:0")
+    theta = torch.from_numpy(sr.model.pack(params)).to(dev)
+    return sr, w, spins, params, ij, jj, dev, theta
+
+
+def _rel(a, b):
+    return (torch.linalg.vector_norm(a - b) / torch.linalg.vector_norm(b)).item()
+
+
+def _loopback(world, w, spins, ij, jj, dev, theta, per_block=True, compare=False):
+    from paper_2510_08430_b200 import parallel
+
+    def make(r, comm, lock):
+        step = parallel.ShardedStep(w.widths, spins, ij, jj, w.lam, r, world, dev, comm=comm,
+                                    per_block_gram=per_block)
+        step.ops = parallel.locked(step.ops, lock)
+        return step
+
+    def work(r, step):
+        d, e = step.run(theta)
+        out = [d.clone(), e.clone()]
+        if compare:
+            out += [step.full_qgt_solve().clone(), step.ntk_solve().clone()]
+        torch.cuda.synchronize()
+        return out
+
+    return parallel.run_loopback(world, make, work)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_loopback_sharded_step_matches_local(world):
+    sr, w, spins, params, ij, jj, dev, theta = _setup(1)
+    from paper_2510_08430_b200 import parallel
+    d_local, e_local = (x.clone() for x in parallel.LocalStep(w.widths, spins, ij, jj, w.lam, dev).run(theta))
+    outs = _loopback(world, w, spins, ij, jj, dev, theta)
+    for r, (d, e) in enumerate(outs):
+        assert torch.equal(d, outs[0][0]) and torch.equal(e, outs[0][1]), r   # all ranks agree exactly
+    assert _rel(outs[0][0], d_local) < 1e-11
+    assert abs(outs[0][1].item() - e_local.item()) <= 1e-13 * abs(e_local.item())
+
+
+@pytest.mark.parametrize("world,per_block", [(2, False), (3, True), (4, True)])
+def test_loopback_configs0_oracle_and_comparison_paths(world, per_block):
+    """configs[0] against the oracle: the block step (grouped or per-block Gram launches), and
+    the sharded comparison paths (partial-S reduce for the full QGT; ring-scheduled NTK
+    blocks gathered to rank 0) against the oracle's full solve (push-through identity)."""
+    sr, w, spins, params, ij, jj, dev, theta = _setup(0)
+    outs = _loopback(world, w, spins, ij, jj, dev, theta, per_block=per_block, compare=True)
+    O = network.jacobian(params, spins)
+    e = hamiltonian.local_energies(params, spins, hamiltonian.bonds_for(w))
+    off = network.layer_offsets(params)
+    ref = solvers.block_solve(estimators.qgt_blocks(O, off), estimators.force(O, e), off, w.lam)
+    full = solvers.full_solve(estimators.qgt_full(O), estimators.force(O, e), w.lam)
+    d, en, d_full, d_ntk = (x.cpu().numpy() for x in outs[0])
+    assert np.linalg.norm(d - ref) / np.linalg.norm(ref) < 1e-9
+    assert abs(en[0] - estimators.energy(e)) < 1e-12 * abs(estimators.energy(e))
+    assert np.linalg.norm(d_full - full) / np.linalg.norm(full) < 1e-9
+    assert np.linalg.norm(d_ntk - full) / np.linalg.norm(full) < 1e-9
+    for r in range(world):
+        assert torch.equal(outs[r][3], outs[0][3])
+
+
+def test_local_step_per_block_schedule_matches_batched():
+    """LocalStep(schedule="per_block") -- sr_block_qgt_solve, one block's Gram written into its
+    factor matrix and solved before the next -- equals the batched schedule (same kernels;
+    the Gram tiles and the Cholesky are identical arithmetic), also through sr_step /
+    sr_step_host under SR_SCHED_PER_BLOCK, and matches the oracle on configs[0]."""
+    sr, w, spins, params, ij, jj, dev, theta = _setup(1)
+    from paper_2510_08430_b200 import parallel
+    d_b = parallel.LocalStep(w.widths, spins, ij, jj, w.lam, dev).run(theta)[0].clone()
+    step = parallel.LocalStep(w.widths, spins, ij, jj, w.lam, dev, schedule="per_block")
+    d_p = step.run(theta)[0].clone()
+    assert _rel(d_p, d_b) < 1e-12
+    step.capture(theta)
+    assert torch.equal(step.replay()[0], d_p)
+    nb = len(jj)
+    prev = sr.sr_set_step_schedule(sr.SCHED_PER_BLOCK)
+    try:
+        ws = torch.empty(sr.sr_step_workspace_bytes(w.widths, w.n_samples, nb)
+                         + sr.sr_step_host_extra_bytes(w.widths, w.n_samples, nb), dtype=torch.uint8, device=dev)
+        d = torch.empty(w.n_params, dtype=torch.complex128, device=dev)
+        en = torch.empty(1, dtype=torch.complex128, device=dev)
+        sr.sr_step(w.widths, theta, step.buf.spins, step.buf.bij, step.buf.bj, w.lam, d, en, ws)
+        dh = torch.empty(w.n_params, dtype=torch.complex128).pin_memory()
+        eh = torch.empty(1, dtype=torch.complex128).pin_memory()
+        sr.sr_step_host(w.widths, theta.cpu().pin_memory(), torch.from_numpy(spins).pin_memory(),
+                        torch.from_numpy(ij), torch.from_numpy(jj), w.lam, dh, eh, ws)
+    finally:
+        sr.sr_set_step_schedule(prev)
+    assert torch.equal(d, d_p)
+    assert torch.equal(dh, d_p.cpu())
+
+
+def test_block_qgt_solve_reports_first_failing_block():
+    """sr_block_qgt_solve's info: 0 on success, else the global row + 1 of the first failing
+    pivot (blocks are solved one call at a time; a later block does not reset it)."""
+    import paper_2510_08430_b200 as sr
+    dev = torch.device("cuda:0")
+    A = torch.zeros(4, 75, dtype=torch.complex128, device=dev)   # S = 0
+    F = torch.ones(75, dtype=torch.complex128, device=dev)
+    d = torch.empty_like(F)
+    info = torch.full((1,), -3, dtype=torch.int32, device=dev)
+    sr.sr_block_qgt_solve(A, [0, 70, 75], F, 0.0, d, info=info)    # lambda = 0: zero pivots
+    assert info.item() == 1
+    sr.sr_block_qgt_solve(A, [0, 70, 75], F, 0.5, d, info=info)
+    assert info.item() == 0 and torch.allclose(d, -F / 0.5, rtol=1e-15, atol=0)

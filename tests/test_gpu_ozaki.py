@@ -237,3 +237,39 @@ def test_block_qgt_i8_cta_pairs():
                        cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+def _wide_range_columns(rng, ns, n):
+    """Columns whose entries span six decades (|A_kj| = |g| 10^u, u ~ U(-6, 0)), plus two
+    columns with a single outlier 1e6 above the rest, and one column scaled by 1e-150."""
+    A = (rng.standard_normal((ns, n)) + 1j * rng.standard_normal((ns, n))) * 10.0 ** rng.uniform(-6, 0, (ns, n))
+    A[rng.integers(ns), 3] *= 1e6
+    A[rng.integers(ns), 7] *= 1e6
+    A[:, 11] *= 1e-150
+    return A
+
+
+@pytest.mark.parametrize("engine", ["int8", "fp64"])
+@pytest.mark.parametrize("ns,sizes", [(4096, (200, 129)), (9000, (64, 70))])
+def test_block_qgt_entrywise_bound(sr, engine, ns, sizes):
+    """north_star's 1e-11 bar "on S_b entries", entry by entry: |S_ij - S_ij^ref| <=
+    1e-11 sqrt(S_ii S_jj) for every i, j (the Cauchy-Schwarz scale of the entry), on data
+    with 1e6 dynamic range inside each column, for both Gram engines.  The int8 engine's
+    error is relative to the column maxima (R10); this checks that it stays inside
+    the entrywise bar for such columns too.  Reference: numpy's FP64 product (its own error
+    is below 1e-13 of the same scale here)."""
+    rng = np.random.default_rng(ns + sum(sizes))
+    n_p = sum(sizes)
+    offs = [0] + [int(x) for x in np.cumsum(sizes)]
+    A = _wide_range_columns(rng, ns, n_p)
+    S = torch.empty(sum(n * n for n in sizes), dtype=C128, device=dev())
+    (sr.sr_block_qgt_i8 if engine == "int8" else sr.sr_block_qgt)(T(A), offs, S)
+    got = packed_blocks(S.cpu().numpy(), offs)
+    for b, g in enumerate(got):
+        a = A[:, offs[b]:offs[b + 1]]
+        ref = a.conj().T @ a
+        d = np.sqrt(np.abs(np.diag(ref)).real)
+        scale = np.outer(d, d)
+        err = np.abs(g - ref)
+        assert np.all(err <= 1e-11 * scale), (b, float(np.max(err / np.where(scale > 0, scale, 1))))
+        assert np.array_equal(g, g.conj().T)

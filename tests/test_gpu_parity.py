@@ -499,7 +499,8 @@ def test_bench_native_json_contract():
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "2", "--warmup", "3",
-                        "--no-cpu-baseline", "--no-compare"], cwd=root, capture_output=True, text=True, timeout=900)
+                        "--workload", "heis_chain_N40", "--no-cpu-baseline"], cwd=root, capture_output=True, text=True,
+                       timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.strip()]
     assert len(lines) == 1
@@ -513,3 +514,35 @@ def test_bench_native_json_contract():
     assert 0.0 < rf["frac"] < 1.5 and d["value"] > 0 and d["gpu_launches"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["config"]["workload"] == "heis_chain_N40" and d["n_gpus"] == 1
+    assert d["fp64_engine"]["gram_frac_of_dmma_peak"] > 0.5
+    assert set(d["comparison_solves"]["ms"]) == {"block_qgt+block_solve", "full_qgt_solve", "ntk_solve"}
+    assert d["comparison_solves"]["rel_l2_full_vs_ntk"] < 1e-9
+
+
+@pytest.mark.parametrize("engine", ["int8", "fp64"])
+def test_ntk_two_chunks_configs1_network(sr, engine):
+    """The NTK solve with n_p = 16240 (configs[1]'s network; the int8 engine's row Gram then
+    needs more than one exact int32 accumulation chunk, K' = 2 n_p > 16384) against the
+    oracle's NTK solve on 256 samples; the GPU full-QGT solve on the same data agrees
+    (push-through identity)."""
+    w = workloads.CONFIGS[1].with_samples(256)
+    spins, params = workloads.make_inputs(w)
+    O = network.jacobian(params, spins)
+    e = hamiltonian.local_energies(params, spins, hamiltonian.bonds_for(w))
+    A, et = estimators.scaled_centered(O, e)
+    prev = sr.sr_set_gram_engine(sr.GRAM_INT8 if engine == "int8" else sr.GRAM_FP64)
+    try:
+        d_ntk = torch.empty(w.n_params, dtype=C128, device=dev())
+        T_out = torch.empty(w.n_samples, w.n_samples, dtype=C128, device=dev())
+        info = torch.full((1,), -5, dtype=torch.int32, device=dev())
+        sr.sr_ntk_solve(T(A), T(et), w.lam, d_ntk, T_out=T_out, info=info)
+        d_full = torch.empty(w.n_params, dtype=C128, device=dev())
+        sr.sr_full_qgt_solve(T(A), T(A.conj().T @ et), w.lam, d_full)
+        torch.cuda.synchronize()
+    finally:
+        sr.sr_set_gram_engine(prev)
+    assert info.item() == 0
+    assert rel(T_out.cpu().numpy(), estimators.ntk(O)) < 1e-11
+    ref = solvers.ntk_solve(A, et, w.lam)
+    assert rel(d_ntk.cpu().numpy(), ref) < 1e-9
+    assert rel(d_full.cpu().numpy(), ref) < 1e-9

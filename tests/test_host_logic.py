@@ -76,6 +76,18 @@ def test_bench_reference_arm_json_contract():
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "impl", "config", "cpu_baseline", "e2e"):
         assert k in d, k
-    assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["workload"] == "heis_chain_N40"
+    assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["workload"] == "j1j2_10x10_w128"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+
+
+def test_bench_workload_scaling():
+    """bench.py measures configs[3] by default (the largest single-GPU configuration, strong
+    scaling over N) and configs[4] with 8192 samples per GPU (weak scaling)."""
+    import bench
+    assert bench.DEFAULT_WORKLOAD == workloads.CONFIGS[3].name
+    for n in (1, 2, 4, 8):
+        assert bench.workload_for("j1j2_10x10_w160", n).n_samples == 8192 * n
+        assert bench.workload_for("j1j2_10x10_w128", n).n_samples == 32768
+    c = bench.config_of(bench.workload_for("j1j2_10x10_w160", 8), 8, "int8", True, "sharded")
+    assert c["samples_per_gpu"] == 8192 and c["n_samples"] == 65536 and c["scaling"].startswith("weak")

@@ -108,3 +108,27 @@ def test_kernel_timer_without_launches(lib):
     sr.sr_kernel_timer(True)
     sr.sr_kernel_timer(False)
     assert sr.sr_kernel_time_ms("gram_i8") == (0.0, 0)
+
+
+def test_per_block_schedule_workspace(lib):
+    """SR_SCHED_PER_BLOCK (sr_set_step_schedule): the step workspace holds one block's factor
+    instead of every S_b and its factor copy -- configs[4] at 8192 samples fits one B200."""
+    import paper_2510_08430_b200 as sr
+    import workloads
+    w = workloads.CONFIGS[4]
+    ns, nb = 8192, 200
+    prev = sr.sr_set_step_schedule(sr.SCHED_PER_BLOCK)
+    try:
+        assert sr.sr_get_step_schedule() == sr.SCHED_PER_BLOCK
+        per_block = sr.sr_step_workspace_bytes(w.widths, ns, nb)
+        assert sr.sr_step_s_offset(w.widths, ns, nb) == 2 ** 64 - 1
+    finally:
+        sr.sr_set_step_schedule(prev)
+    batched = sr.sr_step_workspace_bytes(w.widths, ns, nb)
+    O = ns * w.n_params * 16
+    n_max = max(w.layer_sizes)
+    assert per_block < O + 2 * 16 * (n_max + 64) ** 2 + 21 * ns * n_max + (8 << 30)
+    assert per_block < 60e9 < 150e9 < batched
+    offs = sr._lib._offsets(sr.block_offsets(w.widths))
+    assert lib.sr_block_qgt_solve_workspace_bytes(ns, len(w.layer_sizes), offs) >= 16 * n_max ** 2
+    assert lib.sr_set_step_schedule(7) == -1 and sr.sr_get_step_schedule() == prev

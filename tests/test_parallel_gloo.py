@@ -73,7 +73,9 @@ class OracleOps:
         for b in range(len(offs) - 1):
             lo, hi = offs[b], offs[b + 1]
             n = hi - lo
-            x = solvers.full_solve(S[pos:pos + n * n].reshape(n, n).numpy(), F[lo:hi].numpy(), lam)
+            M = S[pos:pos + n * n].reshape(n, n).numpy()
+            M = np.tril(M) + np.tril(M, -1).conj().T     # the C ABI reads the lower triangle only
+            x = solvers.full_solve(M, F[lo:hi].numpy(), lam)
             dtheta[lo:hi].copy_(torch.from_numpy(x))
             pos += n * n
 
@@ -106,9 +108,10 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
 def test_sharded_step_equals_unsharded_oracle(tmp_path, world):
-    """world 1: one owner of both blocks; 2: one block each; 3: a rank without a block."""
+    """world 1: one owner of both blocks; 2: one block each; 3, 4: ranks without a block (4: the
+    even-G middle step of the NTK ring schedule)."""
     out = str(tmp_path / "d.npy")
     mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     res = np.load(out)
@@ -126,3 +129,70 @@ def test_sharded_step_equals_unsharded_oracle(tmp_path, world):
     full = solvers.full_solve(estimators.qgt_full(O), estimators.force(O, e), w.lam)
     assert np.linalg.norm(got_full - full) / np.linalg.norm(full) < 1e-10
     assert np.linalg.norm(got_ntk - full) / np.linalg.norm(full) < 1e-10
+
+
+@pytest.mark.parametrize("world", [3, 8])
+def test_loopback_threads_equal_unsharded_oracle(world):
+    """parallel.run_loopback / LoopbackComm (the in-process multi-rank emulation that
+    tests/test_gpu_loopback.py runs with the real kernels on one GPU): G threads with the
+    oracle's stage arithmetic give the unsharded oracle's block, full-QGT and NTK updates."""
+    from paper_2510_08430_b200 import parallel
+    import paper_2510_08430_b200 as sr
+    w = workloads.CONFIGS[0].with_samples(64)
+    spins, params = workloads.make_inputs(w)
+    ij, jj = sr.lattice.for_workload(w)
+    theta = torch.from_numpy(sr.model.pack(params))
+
+    def make(r, comm, lock):
+        return parallel.ShardedStep(w.widths, spins, ij, jj, w.lam, r, world, "cpu", comm=comm,
+                                    ops=parallel.locked(OracleOps(), lock))
+
+    def work(r, step):
+        d, e = step.run(theta)
+        return d.clone(), e.clone(), step.full_qgt_solve().clone(), step.ntk_solve().clone()
+
+    outs = parallel.run_loopback(world, make, work)
+    O = network.jacobian(params, spins)
+    e = hamiltonian.local_energies(params, spins, hamiltonian.bonds_for(w))
+    off = network.layer_offsets(params)
+    ref = solvers.block_solve(estimators.qgt_blocks(O, off), estimators.force(O, e), off, w.lam)
+    full = solvers.full_solve(estimators.qgt_full(O), estimators.force(O, e), w.lam)
+    for d, en, d_full, d_ntk in outs:
+        assert np.linalg.norm(d.numpy() - ref) / np.linalg.norm(ref) < 1e-10
+        assert abs(en.item() - estimators.energy(e)) < 1e-12
+        assert np.linalg.norm(d_full.numpy() - full) / np.linalg.norm(full) < 1e-10
+        assert np.linalg.norm(d_ntk.numpy() - full) / np.linalg.norm(full) < 1e-10
+
+
+def test_loopback_failure_does_not_hang():
+    """A rank that raises aborts the rendezvous: the others return and the error is re-raised."""
+    from paper_2510_08430_b200 import parallel
+
+    def make(r, comm, lock):
+        return comm
+
+    def work(r, comm):
+        if r == 1:
+            raise ValueError("rank 1 failed")
+        t = torch.ones(3)
+        comm.all_reduce(t)
+        return t
+
+    with pytest.raises(Exception):
+        parallel.run_loopback(3, make, work)
+
+
+def test_ntk_ring_schedule_covers_each_pair_once():
+    from paper_2510_08430_b200.parallel import ShardedStep
+    for G in range(1, 10):
+        sched = ShardedStep.ntk_schedule(G)
+        pairs = []
+        for r in range(G):
+            for t, src, dst in sched[r]:
+                if t == 0:
+                    pairs.append((r, r))
+                elif src is not None:
+                    pairs.append((max(r, src), min(r, src)))
+                    assert dst is None or sched[dst][t][1] == r     # the receiver expects it
+        assert sorted(pairs) == sorted((i, j) for i in range(G) for j in range(i + 1)), G
+        assert max(len([s for s in sched[r] if s[0] == 0 or s[1] is not None]) for r in range(G)) <= G // 2 + 1
