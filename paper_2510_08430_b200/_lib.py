@@ -18,6 +18,8 @@ from . import build as _build
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsrblock.so")
+# measurement tools only (tools/gram_energy.py): load a variant build of the same library
+_LIB_OVERRIDE = os.environ.get("SR_LIB_VARIANT")
 
 _vp, _i64, _i32, _sz, _dbl = C.c_void_p, C.c_int64, C.c_int, C.c_size_t, C.c_double
 _I32P = C.POINTER(C.c_int32)
@@ -86,11 +88,14 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if build_if_missing and not _build.up_to_date():
-        _build.build()
-    if not os.path.exists(LIB_PATH):
-        raise SRError(f"{LIB_PATH} is missing; run python -m paper_2510_08430_b200.build")
-    lib = C.CDLL(LIB_PATH)
+    if _LIB_OVERRIDE:
+        lib = C.CDLL(_LIB_OVERRIDE)
+    else:
+        if build_if_missing and not _build.up_to_date():
+            _build.build()
+        if not os.path.exists(LIB_PATH):
+            raise SRError(f"{LIB_PATH} is missing; run python -m paper_2510_08430_b200.build")
+        lib = C.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res

@@ -31,14 +31,16 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out=None) -> str:
     """Compile every translation unit to an object file in parallel (one nvcc each), then
-    link the shared library (static cudart)."""
-    if not force and up_to_date():
+    link the shared library (static cudart).  defines/out: a measurement variant (extra -D
+    macros, written to `out` with its own object directory) -- tools only."""
+    if out is None and not force and up_to_date():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    target = out or LIB
+    objdir = os.path.join(HERE, "build" if out is None else "build_" + os.path.basename(out).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
-    cflags = [f for f in FLAGS if f != "-shared"]
+    cflags = [f for f in FLAGS if f != "-shared"] + [f"-D{d}" for d in defines]
     jobs = []
     for s in SOURCES:
         obj = os.path.join(objdir, s.replace(".cu", ".o"))
@@ -50,21 +52,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
         log_txt += " ".join(cmd) + "\n" + out + err
         failed |= p.returncode != 0
     link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
-            *[o for _, o, _ in jobs], "-o", LIB + ".tmp"]
+            *[o for _, o, _ in jobs], "-o", target + ".tmp"]
     if not failed:
         r = subprocess.run(link, capture_output=True, text=True)
         log_txt += " ".join(link) + "\n" + r.stdout + r.stderr
         failed = r.returncode != 0
-    log = os.path.join(HERE, "build.log")
+    log = os.path.join(HERE, "build.log" if out is None else "build_variant.log")
     with open(log, "w") as f:
         f.write(log_txt)
     if failed:
         sys.stderr.write(log_txt[-6000:])
         raise RuntimeError(f"nvcc failed (see {log})")
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(target + ".tmp", target)
     if verbose:
         sys.stderr.write(log_txt)
-    return LIB
+    return target
 
 
 if __name__ == "__main__":

@@ -56,7 +56,9 @@ constexpr int kChunkK = 16384;            // K' per exact int32 accumulation
 constexpr bool kATmem = SR_OZ_A_TMEM;     // operand A staged into TMEM by tcgen05.cp
 constexpr uint32_t kACol = kSlices * BN;  // TMEM columns [448, 504): the A digits of one K step
 #ifndef SR_OZ_EXP
-#define SR_OZ_EXP 0   // energy experiments (tools only): 1 no S stores, 2 no epilogue, 3 L2-resident operands
+#define SR_OZ_EXP 0   // energy experiments (tools only): 1 no S stores, 2 no epilogue, 3 L2-resident operands,
+                      // 4 CRT-like MMA mix (16 N=64 MMAs per K step), 5 = 4 + doubled TMA bytes,
+                      // 6 = doubled TMA bytes with the normal mix (results of 4-6 are wrong by design)
 #endif
 #ifndef SR_OZ_BAND
 #define SR_OZ_BAND 8
@@ -271,10 +273,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kB = pass ? (int)P.Kp : 0;
         for (int kk = 0; kk < P.kstages; kk++) {
           mbar_wait(empty0 + 8 * s, ph ^ 1);
-          mbar_expect_tx(full0 + 8 * s, kStageBytes);
+          constexpr int kRep = (SR_OZ_EXP == 5 || SR_OZ_EXP == 6) ? 2 : 1;
+          mbar_expect_tx(full0 + 8 * s, kRep * kStageBytes);
           const uint32_t sa = smem_base + s * kStageBytes;
-          tma_load_3d(sa, &tm_a, kk * BKB, rowA, 0, full0 + 8 * s);
-          tma_load_3d(sa + kAStage, &tm_b, kB + kk * BKB, rowB, 0, full0 + 8 * s);
+#pragma unroll
+          for (int rep = 0; rep < kRep; rep++) {
+            tma_load_3d(sa, &tm_a, kk * BKB, rowA, 0, full0 + 8 * s);
+            tma_load_3d(sa + kAStage, &tm_b, kB + kk * BKB, rowB, 0, full0 + 8 * s);
+          }
           if (++s == kStages) {
             s = 0;
             ph ^= 1;
@@ -306,6 +312,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               // overtake the MMAs of step ks that read the same columns.
 #pragma unroll
               for (int p = 0; p < kSlices; p++) tmem_cp_128x256b(tmem + kACol + 8 * p, sdesc(sa + p * kASlice + ks * 32));
+            }
+            if (SR_OZ_EXP == 4 || SR_OZ_EXP == 5) {   // CRT-like mix: 16 independent N = 64 products
+#pragma unroll
+              for (int m = 0; m < 16; m++)
+                mma_i8(tmem + (uint32_t)((m & 7) * BN), sdesc(sa + (m % kSlices) * kASlice + ks * 32),
+                       sdesc(sb + (m % kSlices) * kBSlice + ks * 32), (kin > 0 || ks > 0 || m > 7) ? 1u : 0u,
+                       idesc_n(BN));
+              continue;
             }
 #pragma unroll
             for (int p = 0; p < kSlices; p++) {
