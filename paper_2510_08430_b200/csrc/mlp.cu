@@ -283,6 +283,17 @@ __global__ void energy_rows(const int8_t* __restrict__ spins, long long ns, int 
 // 0.721 / 0.751 / 0.747 ms, configs[2] 35.4 / 33.2 / 33.2 ms
 constexpr int kEnergyMG = SR_ENERGY_MG;
 
+// h = lncosh(b_j + z), applied by dense_z to its accumulators in registers (the activation is
+// fused into the DMMA pass: no separate shared-memory pass and barrier per layer).
+struct LncoshBias {
+  const double2* __restrict__ b;
+  __device__ __forceinline__ double2 operator()(int j, double2 z) const { return lncosh(cadd(b[j], z)); }
+};
+
+#ifndef SR_ENERGY_FUSED
+#define SR_ENERGY_FUSED 1
+#endif
+
 // Persistent over tiles of RB connected rows: ln psi(x') then 2 J exp(ln psi(x') - ln psi(x)).
 template <int RB>
 __global__ void __launch_bounds__(kThreads) energy_eval(NetDesc net, const double2* __restrict__ theta,
@@ -330,14 +341,21 @@ __global__ void __launch_bounds__(kThreads) energy_eval(NetDesc net, const doubl
     __syncthreads();
     for (int l = 1; l < net.L; l++) {
       const int fout = net.w[l + 1];
-      dense_z<RB, (RB / 8 < kEnergyMG ? RB / 8 : kEnergyMG), true>(wt + net.toff[l], net.w[l], fout, cur, ld, nxt, ld);
-      __syncthreads();
       const double2* bl = theta + net.boff[l];
-      for (int e = threadIdx.x; e < RB * fout; e += kThreads) {
-        const int r = e / fout, j = e - r * fout;
-        nxt[r * ld + j] = lncosh(cadd(bl[j], nxt[r * ld + j]));
+      if (SR_ENERGY_FUSED) {
+        dense_z<RB, (RB / 8 < kEnergyMG ? RB / 8 : kEnergyMG), true>(wt + net.toff[l], net.w[l], fout, cur, ld, nxt,
+                                                                      ld, LncoshBias{bl});
+        __syncthreads();
+      } else {
+        dense_z<RB, (RB / 8 < kEnergyMG ? RB / 8 : kEnergyMG), true>(wt + net.toff[l], net.w[l], fout, cur, ld, nxt,
+                                                                      ld);
+        __syncthreads();
+        for (int e = threadIdx.x; e < RB * fout; e += kThreads) {
+          const int r = e / fout, j = e - r * fout;
+          nxt[r * ld + j] = lncosh(cadd(bl[j], nxt[r * ld + j]));
+        }
+        __syncthreads();
       }
-      __syncthreads();
       double2* tmp = cur;
       cur = nxt;
       nxt = tmp;

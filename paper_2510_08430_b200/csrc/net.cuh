@@ -52,9 +52,14 @@ __device__ __forceinline__ void net_dmma(double& c0, double& c1, double a, doubl
 #ifndef SR_DENSE_BQ
 #define SR_DENSE_BQ 8
 #endif
-template <int RB, int MG = 1, bool BATCH = false>
+// Epilogue applied to each output element in registers before it is stored (Identity: z).
+struct ZIdentity {
+  __device__ __forceinline__ double2 operator()(int /*j*/, double2 z) const { return z; }
+};
+
+template <int RB, int MG = 1, bool BATCH = false, class Epi = ZIdentity>
 __device__ __forceinline__ void dense_z(const double2* __restrict__ M, int n_in, int n_out, const double2* hin,
-                                        int ldin, double2* zout, int ldz) {
+                                        int ldin, double2* zout, int ldz, Epi epi = Epi()) {
   static_assert(RB % (8 * MG) == 0, "RB must be a multiple of 8 MG");
   constexpr int MU = RB / (8 * MG);          // row-tile groups; a unit is MG row tiles x 8 columns
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -115,7 +120,7 @@ __device__ __forceinline__ void dense_z(const double2* __restrict__ M, int n_in,
       for (int e = 0; e < 2; e++) {
         const int j = nt * 8 + 2 * gc + e;
         if (j < n_out)
-          zout[((mu * MG + g) * 8 + gr) * ldz + j] = make_double2(rr[g][e] - ii[g][e], ri[g][e] + ir[g][e]);
+          zout[((mu * MG + g) * 8 + gr) * ldz + j] = epi(j, make_double2(rr[g][e] - ii[g][e], ri[g][e] + ir[g][e]));
       }
   }
 }

@@ -89,8 +89,11 @@ struct Blk {
 enum { MODE_HERM = 0, MODE_SUB = 1 };
 struct Params {
   int nblk;
-  int kstages;           // K' / BKB
+  int kstages;           // K' / BKB of this launch
   int spc;               // stages per exact accumulation chunk
+  long long kbase;       // first K stage of this launch (K-split launches, see launch_herm)
+  int acc_in;            // 1: add to the partial S a previous K-split launch wrote (MODE_HERM)
+  int defer;             // 1: a later K-split launch continues the sum (no mirror / final diagonal yet)
   long long Kp;          // padded sample count (bytes per slice-row segment)
   long long total_tiles;
   const int* expo;
@@ -278,8 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sa = smem_base + s * kStageBytes;
 #pragma unroll
           for (int rep = 0; rep < kRep; rep++) {
-            tma_load_3d(sa, &tm_a, kk * BKB, rowA, 0, full0 + 8 * s);
-            tma_load_3d(sa + kAStage, &tm_b, kB + kk * BKB, rowB, 0, full0 + 8 * s);
+            const int kc = (int)(P.kbase + kk) * BKB;
+            tma_load_3d(sa, &tm_a, kc, rowA, 0, full0 + 8 * s);
+            tma_load_3d(sa + kAStage, &tm_b, kB + kc, rowB, 0, full0 + 8 * s);
           }
           if (++s == kStages) {
             s = 0;
@@ -423,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             atomicAdd(dp + 2 * e, -val);
             continue;
           }
-          if (nchunks == 1) {
+          if (nchunks == 1 && !P.acc_in && !P.defer) {
             if (i == j) {
               dp[2 * e] = pass ? 0.0 : val;
             } else {
@@ -433,8 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
           double acc = val;
-          if (ch > 0) acc += dp[2 * e];
-          if (ch + 1 < nchunks) {
+          if (ch > 0 || P.acc_in) acc += dp[2 * e];
+          if (ch + 1 < nchunks || P.defer) {
             dp[2 * e] = acc;
           } else if (i == j) {
             dp[2 * e] = pass ? 0.0 : acc;
@@ -1003,6 +1007,42 @@ long long gram_ctas() {
   return v;
 }
 
+// K' per launch of the block-QGT / NTK Gram (SR_OZ_KSPLIT, default 16384).  A tile's K
+// stream is K' x 7 slices x 192 rows; the concurrently running tiles share panels only while
+// they stay within an L2-sized window of one another, and over a long K they drift apart:
+// at K' = 65536 (configs[3]) ncu measured 2.47 TB of DRAM reads for one 16512-column block
+// (216x the slice bytes, L2 hit rate 41%), at K' = 16384 64.6 GB (85% hits), and the
+// sustained rate 1793 vs 2645 int8 TOPS (0.547 vs 0.374 pJ/op; profiles/README.md).  So a
+// long K is cut into launches of K' <= SR_OZ_KSPLIT, each adding its FP64 partial to S in a
+// fixed order (the first writes, later ones read-add-write, the last writes the mirror): the
+// results stay deterministic and differ from one launch only in FP64 summation order.
+long long ksplit_stages() {
+  static long long v = -1;
+  if (v < 0) {
+    const char* e = getenv("SR_OZ_KSPLIT");
+    const long long k = e && atoll(e) > 0 ? atoll(e) : 16384;
+    v = std::max<long long>(1, k / BKB);
+  }
+  return v;
+}
+
+sr_status launch_herm(const CUtensorMap& ma, const CUtensorMap& mb, Params P, long long total_stages,
+                      cudaStream_t st) {
+  const long long split = ksplit_stages();
+  const unsigned grid = (unsigned)std::min<long long>(P.total_tiles, gram_ctas());
+  for (long long s0 = 0; s0 < total_stages; s0 += split) {
+    P.kbase = s0;
+    P.kstages = (int)std::min(split, total_stages - s0);
+    P.acc_in = s0 > 0;
+    P.defer = s0 + split < total_stages;
+    timer_begin("gram_i8", st);
+    gram_i8<MODE_HERM><<<grid, kThreads, kSmem, st>>>(ma, mb, P);
+    timer_end(st);
+    SR_LAUNCHED();
+  }
+  return SR_OK;
+}
+
 sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double2* A, long long lda, double2* S,
                        void* ws, size_t ws_bytes, cudaStream_t st, long long ldc) {
   long long s_total = 0;
@@ -1078,11 +1118,7 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
       SR_LAUNCHED();
     } else {
       SR_TRY(make_map(mb2, E, Kp, nc, BN));
-      const unsigned grid = (unsigned)std::min<long long>(tiles, gram_ctas());
-      timer_begin("gram_i8", st);
-      gram_i8<MODE_HERM><<<grid, kThreads, kSmem, st>>>(ma, mb2, P);
-      timer_end(st);
-      SR_LAUNCHED();
+      SR_TRY(launch_herm(ma, mb2, P, 2 * Kp / BKB, st));
     }
   }
   return SR_OK;
@@ -1196,12 +1232,7 @@ sr_status gram_rows_i8(const double2* L, long long ldl, long long m, long long K
   CUtensorMap ma, mb;
   SR_TRY(make_map(ma, E, Kp, m, BM));
   SR_TRY(make_map(mb, E, Kp, m, BN));
-  const unsigned grid = (unsigned)std::min<long long>(P.total_tiles, kNumSMs);
-  timer_begin("gram_i8", st);
-  gram_i8<MODE_HERM><<<grid, kThreads, kSmem, st>>>(ma, mb, P);
-  timer_end(st);
-  SR_LAUNCHED();
-  return SR_OK;
+  return launch_herm(ma, mb, P, 2 * Kp / BKB, st);
 }
 
 }  // namespace oz

@@ -273,3 +273,21 @@ def test_block_qgt_entrywise_bound(sr, engine, ns, sizes):
         err = np.abs(g - ref)
         assert np.all(err <= 1e-11 * scale), (b, float(np.max(err / np.where(scale > 0, scale, 1))))
         assert np.array_equal(g, g.conj().T)
+
+
+@pytest.mark.parametrize("ksplit", ["4096", "1000000"])
+def test_block_qgt_i8_ksplit_switch(ksplit):
+    """The Gram's K' per launch (SR_OZ_KSPLIT, default 16384: long K cut into launches that add
+    their FP64 partials in a fixed order) only changes FP64 summation order: the parity cases
+    pass with short launches (4096) and with one launch per group (in-kernel int32 chunks)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_ozaki.py"),
+                        "-k", "test_block_qgt_i8_parity or matches_fp64 or entrywise or full_and_ntk_int8"],
+                       cwd=root, env=dict(os.environ, SR_OZ_KSPLIT=ksplit), capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
