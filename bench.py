@@ -469,8 +469,17 @@ def compare_solves(sr, torch, step, w, dev):
     else:
         block_call = lambda ws: (step.ops.block_qgt(b.O, b.offs, b.S),  # noqa: E731
                                  step.ops.block_solve(b.offs, b.S, b.F, w.lam, b.dtheta))
+    cg_info = {}
+
+    def full_cg(ws):
+        from paper_2510_08430_b200 import parallel
+        x, it, res = parallel.full_qgt_cg(step.ops, parallel.SelfComm(), b.O, b.F, w.lam)
+        out_d["full_qgt_cg"] = x
+        cg_info.update(iterations=it, rel_residual=res)
+
     calls = {"block_qgt+block_solve": block_call,
              "full_qgt_solve": lambda ws: sr.sr_full_qgt_solve(b.O, b.F, w.lam, out_d["full_qgt_solve"], workspace=ws),
+             "full_qgt_cg": full_cg,
              "ntk_solve": lambda ws: sr.sr_ntk_solve(b.O, b.e_tilde, w.lam, out_d["ntk_solve"], workspace=ws)}
     need = {"full_qgt_solve": lib.sr_full_qgt_solve_workspace_bytes(ns, b.n_p) + 16 * b.n_p,
             "ntk_solve": lib.sr_ntk_solve_workspace_bytes(ns, b.n_p) + 16 * b.n_p}
@@ -501,11 +510,16 @@ def compare_solves(sr, torch, step, w, dev):
     nrm = lambda x: float(torch.linalg.vector_norm(x).item())   # noqa: E731
     out = {"ms": ms, "sizes": {"full_qgt": b.n_p, "ntk": int(ns), "blocks": [int(x) for x in block_sizes(w)]},
            "note": "eager, one timed call each after a warm call; A, F, e from the step above"}
-    ref = "full_qgt_solve" if "full_qgt_solve" in ms else ("ntk_solve" if "ntk_solve" in ms else None)
+    ref = next((k for k in ("full_qgt_solve", "full_qgt_cg", "ntk_solve") if k in ms), None)
     if "full_qgt_solve" in ms and "ntk_solve" in ms:
         out["rel_l2_full_vs_ntk"] = nrm(out_d["full_qgt_solve"] - out_d["ntk_solve"]) / nrm(out_d["full_qgt_solve"])
+    if "full_qgt_cg" in ms and "ntk_solve" in ms:
+        out["rel_l2_full_cg_vs_ntk"] = nrm(out_d["full_qgt_cg"] - out_d["ntk_solve"]) / nrm(out_d["ntk_solve"])
+    if cg_info:
+        out["full_qgt_cg"] = dict(cg_info, note="matrix-free: S p = A^H (A p), S never formed (parallel.full_qgt_cg)")
     if ref:
-        out[f"rel_l2_block_vs_{ref.split('_')[0]}"] = nrm(b.dtheta - out_d[ref]) / nrm(out_d[ref])
+        out["rel_l2_block_vs_full"] = nrm(b.dtheta - out_d[ref]) / nrm(out_d[ref])
+        out["block_vs_full_reference"] = ref
     if skipped:
         out["skipped"] = skipped
     return out

@@ -28,6 +28,9 @@
  *   query returns (256-byte aligned base required).
  * - Threads: calls may come from any host thread, but not concurrently -- the side-stream
  *   pool, the graph cache and the timer are shared, unsynchronised process state.
+ * - Devices: one device per process (the multi-GPU path runs one process per GPU).  The
+ *   side-stream pool and the CUDA-graph cache are created on the device current at their
+ *   first use; the kernels' shared-memory opt-ins are set once per device.
  * - `stream` is a cudaStream_t (NULL = legacy default stream).  All device work is
  *   enqueued on it; calls return without synchronising, except sr_step_host.
  * - Network: complex MLP with widths[0..n_layers] (widths[0] = N sites),
@@ -311,6 +314,27 @@ SR_API sr_status sr_gram_nh(int64_t m, int64_t n, int64_t k, const double* A, in
 SR_API size_t sr_aHv_workspace_bytes(int64_t n_rows, int64_t n_p);
 SR_API sr_status sr_aHv(int64_t n_rows, int64_t n_p, const double* A, int64_t lda, const double* v, double alpha,
                         double* out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Matrix-free full-QGT solve support (the sharded comparison path parallel.full_qgt_cg):
+ * (S + lambda I) dtheta = -F with S = A^H A applied as A^H (A p) by conjugate gradients,
+ * never formed (configs[3]'s full QGT is 146 GB).  With samples sharded, S p = sum_r
+ * A_r^H (A_r p) -- each rank's sr_av + sr_aHv, then one all-reduce of n_p values.
+ *   sr_av      out = alpha A v for A (n_rows x n_p, lda), v [n_p], out [n_rows]; one warp per
+ *              row, fixed summation order (deterministic).
+ *   sr_zdotc   out (device complex [1]) = sum_i conj(x_i) y_i, fixed-order two-level
+ *              reduction; workspace sr_zdotc_workspace_bytes().
+ *   sr_cg_axpy y += sign * (num / den) x ;  sr_cg_xpby  y = x + (num / den) y
+ *              (num, den: device complex scalars, e.g. sr_zdotc outputs; the CG step sizes
+ *              are formed on the device, no host round trip). */
+SR_API sr_status sr_av(int64_t n_rows, int64_t n_p, const double* A, int64_t lda, const double* v, double alpha,
+                       double* out, void* stream);
+SR_API size_t sr_zdotc_workspace_bytes(void);
+SR_API sr_status sr_zdotc(int64_t n, const double* x, const double* y, double* out, void* workspace,
+                          size_t workspace_bytes, void* stream);
+SR_API sr_status sr_cg_axpy(int64_t n, const double* x, double* y, const double* num, const double* den,
+                            double sign, void* stream);
+SR_API sr_status sr_cg_xpby(int64_t n, const double* x, double* y, const double* num, const double* den,
+                            void* stream);
 
 /* ---------------------------------------------------------------- full step ---
  * sr_step — stages (1)-(5) back to back on device buffers (uniform weights):

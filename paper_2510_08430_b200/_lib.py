@@ -38,6 +38,11 @@ SIGNATURES = {
     "sr_gram_nh": (_i32, [_i64, _i64, _i64, C.c_void_p, _i64, C.c_void_p, _i64, C.c_void_p, _i64, C.c_void_p]),
     "sr_aHv_workspace_bytes": (_sz, [_i64, _i64]),
     "sr_aHv": (_i32, [_i64, _i64, C.c_void_p, _i64, C.c_void_p, _dbl, C.c_void_p, C.c_void_p, _sz, C.c_void_p]),
+    "sr_av": (_i32, [_i64, _i64, _vp, _i64, _vp, _dbl, _vp, _vp]),
+    "sr_zdotc_workspace_bytes": (_sz, []),
+    "sr_zdotc": (_i32, [_i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "sr_cg_axpy": (_i32, [_i64, _vp, _vp, _vp, _vp, _dbl, _vp]),
+    "sr_cg_xpby": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp]),
     "sr_graph_capture_begin": (_i32, [C.c_void_p]),
     "sr_graph_capture_end": (_i32, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "sr_graph_launch": (_i32, [C.c_void_p, C.c_void_p]),
@@ -352,6 +357,33 @@ def sr_aHv(A, v, alpha, out, workspace=None):
     ws = _workspace(lib.sr_aHv_workspace_bytes(A.shape[0], A.shape[1]), A.device, workspace)
     _check(lib.sr_aHv(A.shape[0], A.shape[1], _ptr(A), lda, _ptr(v), float(alpha), _ptr(out), *_ws_args(ws),
                       _stream(A.device)), "sr_aHv")
+
+
+def sr_av(A, v, alpha, out):
+    """out = alpha A v (A may be a column slice)."""
+    lda = _cols(A, "A")
+    for t, n in ((v, "v"), (out, "out")):
+        _dev(t, torch.complex128, n)
+    _check(load().sr_av(A.shape[0], A.shape[1], _ptr(A), lda, _ptr(v), float(alpha), _ptr(out), _stream(A.device)),
+           "sr_av")
+
+
+def sr_zdotc(x, y, out, workspace=None):
+    """out[0] = sum conj(x) y (device complex scalar)."""
+    lib = load()
+    ws = _workspace(lib.sr_zdotc_workspace_bytes(), x.device, workspace)
+    _check(lib.sr_zdotc(x.numel(), _ptr(x), _ptr(y), _ptr(out), *_ws_args(ws), _stream(x.device)), "sr_zdotc")
+
+
+def sr_cg_axpy(x, y, num, den, sign):
+    """y += sign (num / den) x  (num, den: device complex scalars)."""
+    _check(load().sr_cg_axpy(x.numel(), _ptr(x), _ptr(y), _ptr(num), _ptr(den), float(sign), _stream(x.device)),
+           "sr_cg_axpy")
+
+
+def sr_cg_xpby(x, y, num, den):
+    """y = x + (num / den) y."""
+    _check(load().sr_cg_xpby(x.numel(), _ptr(x), _ptr(y), _ptr(num), _ptr(den), _stream(x.device)), "sr_cg_xpby")
 
 
 # ------------------------------------------------------------------ full step

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsrblock.so")
-SOURCES = ["mlp.cu", "center.cu", "chol.cu", "ozaki.cu", "capi.cu"]
+SOURCES = ["mlp.cu", "center.cu", "chol.cu", "ozaki.cu", "cg.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -538,11 +538,10 @@ sr_status chol_solve(CholSet& cs, double lam, bool inplace, double sign, cudaStr
     chol_init<<<g, 256, 0, st>>>(cs, lam, inplace ? 1 : 0, 0);
     SR_LAUNCHED();
   }
-  static bool diag_attr = false;
-  if (!diag_attr) {
+  static unsigned long long diag_attr = 0;
+  if (first_on_device(diag_attr)) {
     SR_CUDA(cudaFuncSetAttribute(chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDiagSmem));
     SR_CUDA(cudaFuncSetAttribute(chol_back_strip, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBackSmem));
-    diag_attr = true;
   }
   SidePool* pool;
   SR_TRY(side_pool(pool));

@@ -145,6 +145,18 @@ enum TraceKind {
     if (s_ != SR_OK) return s_;      \
   } while (0)
 
+// True the first time it is called on the current device for this mask: kernel attributes
+// (the dynamic shared-memory opt-ins) are per device, so their one-time set-up is keyed by
+// the device rather than by a process-wide flag.
+inline bool first_on_device(unsigned long long& mask) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const unsigned long long bit = 1ull << (d & 63);
+  if (mask & bit) return false;
+  mask |= bit;
+  return true;
+}
+
 constexpr int kNumSMs = 148;
 
 // Bump allocator over the caller's workspace (256-byte aligned chunks).

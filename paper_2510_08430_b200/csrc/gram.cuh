@@ -427,11 +427,10 @@ inline void add_prob(ProbSet& ps, const double2* A, long long lda, const double2
 template <int FL, int EP>
 inline sr_status launch(const ProbSet& ps, cudaStream_t st) {
   if (ps.total_tiles == 0) return SR_OK;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set = 0;
+  if (first_on_device(attr_set)) {
     SR_CUDA(cudaFuncSetAttribute(tile_kernel<FL, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_bytes<FL>()));
-    attr_set = true;
   }
   tile_kernel<FL, EP><<<(unsigned)ps.total_tiles, kThreads, smem_bytes<FL>(), st>>>(ps);
   SR_LAUNCHED();
@@ -551,11 +550,10 @@ __global__ void __launch_bounds__(SK_THREADS, 2) skinny_kernel(const __grid_cons
 template <int EP, int SK_TM, bool KLOOP>
 inline sr_status launch_skinny_k(const ProbSet& ps, long long total, cudaStream_t st, bool pdl) {
   constexpr size_t kSkinnySmem = skinny_smem<SK_TM>();
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set = 0;
+  if (first_on_device(attr_set)) {
     SR_CUDA(cudaFuncSetAttribute(skinny_kernel<EP, SK_TM, KLOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kSkinnySmem));
-    attr_set = true;
   }
   if (pdl)
     SR_CUDA(launch_pdl(skinny_kernel<EP, SK_TM, KLOOP>, dim3((unsigned)total), dim3(SK_THREADS), kSkinnySmem, st, ps));
@@ -590,6 +588,15 @@ template <int EP>
 inline sr_status launch_tn_tma(const ProbSet& ps, const double2* X, long long ld, long long ncols, long long K,
                                cudaStream_t st) {
   if (ps.total_tiles == 0) return SR_OK;
+  // The one tensor map covers X: every problem must be a Hermitian Gram of a column range of
+  // X (A == B inside [X, X + ncols), the same ld and K).  Anything else takes the cp.async
+  // kernel, which reads each problem's own pointers.
+  for (int i = 0; i < ps.count; i++) {
+    const Prob& p = ps.p[i];
+    const long long c0 = p.A - X;
+    if (p.A != p.B || p.lda != ld || p.ldb != ld || p.K != K || c0 < 0 || c0 + p.N > ncols || p.M != p.N)
+      return launch<TN, EP>(ps, st);
+  }
   static TmaEncode enc = nullptr;
   if (!enc) {
     void* p = nullptr;
@@ -613,10 +620,9 @@ inline sr_status launch_tn_tma(const ProbSet& ps, const double2* X, long long ld
     set_error("cuTensorMapEncodeTiled failed (FP64 Gram): " + std::to_string((int)r));
     return SR_ERR_CUDA;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set = 0;
+  if (first_on_device(attr_set)) {
     SR_CUDA(cudaFuncSetAttribute(tn_tma_kernel<EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
-    attr_set = true;
   }
   tn_tma_kernel<EP><<<(unsigned)ps.total_tiles, kThreads, kTmaSmem, st>>>(ps, map, X);
   SR_LAUNCHED();

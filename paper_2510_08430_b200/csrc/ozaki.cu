@@ -931,14 +931,13 @@ sr_status make_map(CUtensorMap& m, void* base, long long Kp, long long ncols, in
 long long pad_k(long long ns) { return std::max<long long>(64, (ns + 63) / 64 * 64); }
 
 sr_status set_attrs() {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (first_on_device(attr)) {
     SR_CUDA(cudaFuncSetAttribute(gram_i8<MODE_HERM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
     SR_CUDA(cudaFuncSetAttribute(gram_i8<MODE_SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
     SR_CUDA(cudaFuncSetAttribute(gram_i8_2sm<MODE_HERM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2));
     SR_CUDA(cudaFuncSetAttribute(gram_i8_2sm<MODE_SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2));
     SR_CUDA(cudaFuncSetAttribute(oz_split, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSplitSmem));
-    attr = true;
   }
   return SR_OK;
 }

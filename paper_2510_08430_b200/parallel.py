@@ -110,6 +110,71 @@ class CudaOps:
     def aHv(self, A, v, alpha, out):
         sr.sr_aHv(A, v, alpha, out)
 
+    # matrix-free full-QGT CG (full_qgt_cg)
+    def av(self, A, v, alpha, out):
+        sr.sr_av(A, v, alpha, out)
+
+    def zdotc(self, x, y, out):
+        sr.sr_zdotc(x, y, out)
+
+    def cg_axpy(self, x, y, num, den, sign):
+        sr.sr_cg_axpy(x, y, num, den, sign)
+
+    def cg_xpby(self, x, y, num, den):
+        sr.sr_cg_xpby(x, y, num, den)
+
+
+class SelfComm:
+    """The collectives of a one-rank group (nothing to exchange)."""
+
+    def all_reduce(self, t, async_op=False):
+        return _Done()
+
+
+def full_qgt_cg(ops, comm, A, F, lam, tol=1e-12, maxit=500):
+    """Full-QGT solve (S + lambda I) x = -F, S = A^H A summed over ranks, by conjugate
+    gradients without forming S (§2 "S . delta theta = -F"; the full QGT of
+    configs[3] is 146 GB, configs[4]'s 618 GB).  Each iteration: u = A_r p (sr_av) and
+    w_r = A_r^H u (sr_aHv) on the rank's own rows, one all-reduce of n_p values, then
+    identical vector updates on every rank (sr_zdotc / sr_cg_axpy / sr_cg_xpby, step sizes
+    formed on the device).  Stops when ||r|| <= tol ||F||.  Returns (x, iterations,
+    relative residual)."""
+    c = torch.complex128
+    dev = F.device
+    n = F.numel()
+    x = torch.zeros(n, dtype=c, device=dev)
+    r = torch.zeros(n, dtype=c, device=dev)
+    w = torch.empty(n, dtype=c, device=dev)
+    u = torch.empty(A.shape[0], dtype=c, device=dev)
+    one = torch.ones(1, dtype=c, device=dev)
+    lam_s = torch.full((1,), complex(lam, 0.0), dtype=c, device=dev)
+    rho, rho_new, pw = (torch.empty(1, dtype=c, device=dev) for _ in range(3))
+    ops.cg_axpy(F, r, one, one, -1.0)                # r = -F (x = 0)
+    p = r.clone()
+    ops.zdotc(r, r, rho)
+    f_norm = abs(rho.item()) ** 0.5
+    if f_norm == 0.0:
+        return x, 0, 0.0
+    res, it = 1.0, 0
+    for it in range(1, maxit + 1):
+        if A.shape[0]:
+            ops.av(A, p, 1.0, u)
+            ops.aHv(A, u, 1.0, w)
+        else:
+            w.zero_()
+        comm.all_reduce(w)
+        ops.cg_axpy(p, w, lam_s, one, 1.0)           # w = (S + lambda) p
+        ops.zdotc(p, w, pw)
+        ops.cg_axpy(p, x, rho, pw, 1.0)              # x += alpha p
+        ops.cg_axpy(w, r, rho, pw, -1.0)             # r -= alpha w
+        ops.zdotc(r, r, rho_new)
+        res = abs(rho_new.item()) ** 0.5 / f_norm
+        if res <= tol:
+            break
+        ops.cg_xpby(r, p, rho_new, rho)              # p = r + beta p
+        rho, rho_new = rho_new, rho
+    return x, it, res
+
 
 def shard_range(n, rank, world):
     """Contiguous, balanced split of n rows over world ranks."""
@@ -538,12 +603,21 @@ class ShardedStep:
         return b.dtheta, b.energy
 
     # --- comparison paths, sharded the same way (north_star); call after run() ---
-    def full_qgt_solve(self):
-        """Full-QGT solve with samples sharded: each rank's partial S = A_r^H A_r over all n_p
-        columns, reduced to rank 0, which solves (S + lambda I) dtheta = -F (one blocked
-        Cholesky); dtheta broadcast.  Returns dtheta (every rank).  (Rank 0 holds all of S:
-        n_p^2 complex; see dist_full_qgt_solve for S distributed by block rows.)"""
+    DENSE_FULL_MAX = 40000   # n_p above which the full QGT is not formed (method "auto")
+
+    def full_qgt_solve(self, method="auto", tol=1e-12):
+        """Full-QGT solve with samples sharded.  method "dense": each rank's partial
+        S = A_r^H A_r over all n_p columns is reduced to rank 0, which solves
+        (S + lambda I) dtheta = -F by one blocked Cholesky and broadcasts dtheta (rank 0 holds
+        n_p^2 complex: configs[0]-[2]).  "cg": full_qgt_cg, S applied as sum_r A_r^H (A_r p)
+        with one all-reduce per iteration, never formed (configs[3]/[4]).  "auto": dense up to
+        DENSE_FULL_MAX parameters.  Returns dtheta (every rank); self.cg_info holds
+        (iterations, relative residual) of the last CG solve."""
         b, o, c = self.buf, self.ops, self.comm
+        if method == "cg" or (method == "auto" and b.n_p > self.DENSE_FULL_MAX):
+            d, it, res = full_qgt_cg(o, c, b.O, b.F, self.lam, tol=tol)
+            self.cg_info = (it, res)
+            return d
         n = b.n_p
         S = torch.empty(n * n, dtype=torch.complex128, device=self.device)
         o.block_qgt(b.O, [0, n], S)

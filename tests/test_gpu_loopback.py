@@ -53,7 +53,8 @@ def _loopback(world, w, spins, ij, jj, dev, theta, per_block=True, compare=False
         d, e = step.run(theta)
         out = [d.clone(), e.clone()]
         if compare:
-            out += [step.full_qgt_solve().clone(), step.ntk_solve().clone()]
+            out += [step.full_qgt_solve().clone(), step.ntk_solve().clone(),
+                    step.full_qgt_solve(method="cg").clone()]
         torch.cuda.synchronize()
         return out
 
@@ -84,11 +85,12 @@ def test_loopback_configs0_oracle_and_comparison_paths(world, per_block):
     off = network.layer_offsets(params)
     ref = solvers.block_solve(estimators.qgt_blocks(O, off), estimators.force(O, e), off, w.lam)
     full = solvers.full_solve(estimators.qgt_full(O), estimators.force(O, e), w.lam)
-    d, en, d_full, d_ntk = (x.cpu().numpy() for x in outs[0])
+    d, en, d_full, d_ntk, d_cg = (x.cpu().numpy() for x in outs[0])
     assert np.linalg.norm(d - ref) / np.linalg.norm(ref) < 1e-9
     assert abs(en[0] - estimators.energy(e)) < 1e-12 * abs(estimators.energy(e))
     assert np.linalg.norm(d_full - full) / np.linalg.norm(full) < 1e-9
     assert np.linalg.norm(d_ntk - full) / np.linalg.norm(full) < 1e-9
+    assert np.linalg.norm(d_cg - full) / np.linalg.norm(full) < 1e-9
     for r in range(world):
         assert torch.equal(outs[r][3], outs[0][3])
 
@@ -137,3 +139,74 @@ def test_block_qgt_solve_reports_first_failing_block():
     assert info.item() == 1
     sr.sr_block_qgt_solve(A, [0, 70, 75], F, 0.5, d, info=info)
     assert info.item() == 0 and torch.allclose(d, -F / 0.5, rtol=1e-15, atol=0)
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_full_qgt_cg_matches_dense_o1_conditioned(world):
+    """The matrix-free full-QGT solve (parallel.full_qgt_cg: S p = sum_r A_r^H (A_r p) by
+    sr_av / sr_aHv, one all-reduce per iteration, sr_zdotc / sr_cg_axpy / sr_cg_xpby updates)
+    on an O(1)-conditioned A (||S|| ~ 1 >> lambda = 1e-3), sharded over `world` loopback
+    ranks, against numpy's dense solve of the same system (1e-9) and the library's dense
+    sr_full_qgt_solve."""
+    import paper_2510_08430_b200 as sr
+    from paper_2510_08430_b200 import parallel
+    sr.load()
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(world)
+    ns, n_p, lam = 600, 380, 1e-3
+    A = (rng.standard_normal((ns, n_p)) + 1j * rng.standard_normal((ns, n_p))) / np.sqrt(2 * ns)
+    F = rng.standard_normal(n_p) + 1j * rng.standard_normal(n_p)
+    ref = -np.linalg.solve(A.conj().T @ A + lam * np.eye(n_p), F)
+    At, Ft = torch.from_numpy(A).to(dev), torch.from_numpy(F).to(dev)
+    bounds = [parallel.shard_range(ns, r, world) for r in range(world)]
+
+    def make(r, comm, lock):
+        return comm, lock
+
+    def work(r, cl):
+        comm, lock = cl
+        ops = parallel.locked(parallel.CudaOps([4, 4], 1, 1, dev), lock)
+        lo, hi = bounds[r]
+        x, it, res = parallel.full_qgt_cg(ops, comm, At[lo:hi].contiguous(), Ft, lam)
+        torch.cuda.synchronize()
+        return x.cpu().numpy(), it, res
+
+    outs = parallel.run_loopback(world, make, work)
+    x, it, res = outs[0]
+    assert res <= 1e-12 and it < 500
+    assert np.linalg.norm(x - ref) / np.linalg.norm(ref) < 1e-9
+    for o in outs[1:]:
+        assert np.array_equal(o[0], x)
+    d = torch.empty_like(Ft)
+    sr.sr_full_qgt_solve(At, Ft, lam, d)
+    assert np.linalg.norm(d.cpu().numpy() - ref) / np.linalg.norm(ref) < 1e-9
+
+
+def test_av_zdotc_cg_kernels():
+    """sr_av (alpha A v, column-slice A, ragged sizes), sr_zdotc, sr_cg_axpy / sr_cg_xpby
+    against numpy."""
+    import paper_2510_08430_b200 as sr
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(5)
+    for nr, n in ((1, 1), (37, 129), (300, 4099)):
+        Aw = rng.standard_normal((nr, n + 3)) + 1j * rng.standard_normal((nr, n + 3))
+        v = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        out = torch.empty(nr, dtype=torch.complex128, device=dev)
+        sr.sr_av(torch.from_numpy(Aw).to(dev)[:, 2:2 + n], torch.from_numpy(v).to(dev), -0.5, out)
+        ref = -0.5 * (Aw[:, 2:2 + n] @ v)
+        assert np.linalg.norm(out.cpu().numpy() - ref) / np.linalg.norm(ref) < 1e-14
+        x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        y = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        xd, yd = torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev)
+        dot = torch.empty(1, dtype=torch.complex128, device=dev)
+        sr.sr_zdotc(xd, yd, dot)
+        assert abs(dot.item() - np.vdot(x, y)) < 1e-13 * np.linalg.norm(x) * np.linalg.norm(y)
+        num = torch.tensor([2.0 + 1.0j], dtype=torch.complex128, device=dev)
+        den = torch.tensor([0.5 - 0.5j], dtype=torch.complex128, device=dev)
+        a = (2.0 + 1.0j) / (0.5 - 0.5j)
+        y2 = yd.clone()
+        sr.sr_cg_axpy(xd, y2, num, den, -1.0)
+        assert np.linalg.norm(y2.cpu().numpy() - (y - a * x)) < 1e-13 * np.linalg.norm(y)
+        y3 = yd.clone()
+        sr.sr_cg_xpby(xd, y3, num, den)
+        assert np.linalg.norm(y3.cpu().numpy() - (x + a * y)) < 1e-13 * np.linalg.norm(y)

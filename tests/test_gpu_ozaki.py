@@ -291,3 +291,41 @@ def test_block_qgt_i8_ksplit_switch(ksplit):
                        timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+_FP64_TMA_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2510_08430_b200 as sr
+dev = torch.device("cuda:0")
+g = torch.Generator(device=dev).manual_seed(9)
+W = torch.complex(torch.randn(333, 700, dtype=torch.float64, device=dev, generator=g),
+                  torch.randn(333, 700, dtype=torch.float64, device=dev, generator=g))
+A = W[:, 37:37 + 601]            # a column slice: lda = 700
+offs = [0, 1, 130, 193, 601]
+S = torch.empty(sum((offs[b + 1] - offs[b]) ** 2 for b in range(4)), dtype=torch.complex128, device=dev)
+sr.sr_block_qgt(A, offs, S)
+torch.cuda.synchronize()
+np.save(sys.argv[2], S.cpu().numpy())
+"""
+
+
+def test_fp64_tma_staging_is_bit_identical(tmp_path):
+    """The FP64 engine's TMA-staged Gram (default) and its cp.async fallback (SR_FP64_TMA=0)
+    give bit-identical S on ragged blocks of a column-slice A (same fragments, same order)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "s.py"
+    script.write_text(_FP64_TMA_SCRIPT)
+    outs = []
+    for v in ("1", "0"):
+        out = tmp_path / f"S{v}.npy"
+        r = subprocess.run([sys.executable, str(script), root, str(out)], env=dict(os.environ, SR_FP64_TMA=v),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
+    A = outs[0]
+    assert np.all(np.isfinite(A))

@@ -68,6 +68,18 @@ class OracleOps:
     def aHv(self, A, v, alpha, out):
         out.copy_(alpha * (A.conj().T @ v))
 
+    def av(self, A, v, alpha, out):
+        out.copy_(alpha * (A @ v))
+
+    def zdotc(self, x, y, out):
+        out.copy_(torch.vdot(x, y).reshape(1))
+
+    def cg_axpy(self, x, y, num, den, sign):
+        y.add_(sign * (num / den) * x)
+
+    def cg_xpby(self, x, y, num, den):
+        y.copy_(x + (num / den) * y)
+
     def block_solve(self, offs, S, F, lam, dtheta, info=None):
         pos = 0
         for b in range(len(offs) - 1):
@@ -93,9 +105,10 @@ def _worker(rank, world, port, result_path):
                        per_block_gram=world != 2)   # world 2 also covers the grouped launch
     d, e = step.run(torch.from_numpy(sr.model.pack(params)))
     d_full = step.full_qgt_solve()   # comparison paths, sharded the same way
+    d_cg = step.full_qgt_solve(method="cg")
     d_ntk = step.ntk_solve()
     if rank == 0:
-        np.save(result_path, np.concatenate([d.numpy(), e.numpy(), d_full.numpy(), d_ntk.numpy()]))
+        np.save(result_path, np.concatenate([d.numpy(), e.numpy(), d_full.numpy(), d_ntk.numpy(), d_cg.numpy()]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -117,7 +130,8 @@ def test_sharded_step_equals_unsharded_oracle(tmp_path, world):
     res = np.load(out)
     w = workloads.CONFIGS[0].with_samples(64)
     n_p = w.n_params
-    got, got_full, got_ntk = res[:n_p + 1], res[n_p + 1:2 * n_p + 1], res[2 * n_p + 1:]
+    got, got_full, got_ntk, got_cg = (res[:n_p + 1], res[n_p + 1:2 * n_p + 1], res[2 * n_p + 1:3 * n_p + 1],
+                                      res[3 * n_p + 1:])
     spins, params = workloads.make_inputs(w)
     O = network.jacobian(params, spins)
     e = hamiltonian.local_energies(params, spins, hamiltonian.bonds_for(w))
@@ -129,6 +143,7 @@ def test_sharded_step_equals_unsharded_oracle(tmp_path, world):
     full = solvers.full_solve(estimators.qgt_full(O), estimators.force(O, e), w.lam)
     assert np.linalg.norm(got_full - full) / np.linalg.norm(full) < 1e-10
     assert np.linalg.norm(got_ntk - full) / np.linalg.norm(full) < 1e-10
+    assert np.linalg.norm(got_cg - full) / np.linalg.norm(full) < 1e-10
 
 
 @pytest.mark.parametrize("world", [3, 8])
