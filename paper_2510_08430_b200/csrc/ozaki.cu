@@ -201,8 +201,10 @@ __device__ __forceinline__ void decode(const Params& P, long long t, int& b, int
     I = J = 0;
     return;
   }
-  for (int I0 = 0; I0 < RT; I0 += kBand) {
-    const int I1 = min(RT, I0 + kBand), h = I1 - I0;
+  // a band spans the same number of A rows for 128-row (R = 2) and 256-row (R = 4) tiles
+  constexpr int band = kBand * 2 / R > 0 ? kBand * 2 / R : 1;
+  for (int I0 = 0; I0 < RT; I0 += band) {
+    const int I1 = min(RT, I0 + band), h = I1 - I0;
     long long cnt = 0;
     for (int i = I0; i < I1; i++) cnt += min(CT, R * i + R);
     if (u >= cnt) {
@@ -574,7 +576,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (rank == 0) mbar_expect_tx(full0 + 8 * s, 2 * kStage2);
           const uint32_t sa = smem_base + s * kStage2, sb = sa + kSlices * kASlice;
           const uint32_t fb = full0_lead + 8 * s;
-          const int kc = kk * BKB;
+          const int kc = (int)(P.kbase + kk) * BKB;
           tma_load_3d_pair(sa, &tm_a, kc, rowA, 0, fb);
           tma_load_3d_pair(sb, &tm_b2, kB + kc, rowB, rank ? 2 : 0, fb);                       // R0
           tma_load_3d_pair(sb + kR0 * BKB, &tm_b1, kB + kc, rowB, rank ? 5 : 4, fb);          // R1
@@ -696,7 +698,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             atomicAdd(dp + 2 * e, -val);
             continue;
           }
-          if (nchunks == 1) {
+          if (nchunks == 1 && !P.acc_in && !P.defer) {
             if (i == j) {
               dp[2 * e] = pass ? 0.0 : val;
             } else {
@@ -706,8 +708,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             continue;
           }
           double acc = val;
-          if (ch > 0) acc += dp[2 * e];
-          if (ch + 1 < nchunks) {
+          if (ch > 0 || P.acc_in) acc += dp[2 * e];
+          if (ch + 1 < nchunks || P.defer) {
             dp[2 * e] = acc;
           } else if (i == j) {
             dp[2 * e] = pass ? 0.0 : acc;
@@ -1111,10 +1113,17 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
       SR_TRY(make_map(mbb1, E, Kp, nc, BN, 1));
       SR_TRY(make_map(mbh, E, Kp, nc, BN / 2, 1));
       const unsigned grid = 2 * (unsigned)std::min<long long>(tiles, kNumSMs / 2);
-      timer_begin("gram_i8", st);
-      gram_i8_2sm<MODE_HERM><<<grid, kThreads, kSmem2, st>>>(ma, mbb2, mbb1, mbh, P);
-      timer_end(st);
-      SR_LAUNCHED();
+      const long long total = 2 * Kp / BKB, split = ksplit_stages();
+      for (long long s0 = 0; s0 < total; s0 += split) {   // K-split launches as launch_herm
+        P.kbase = s0;
+        P.kstages = (int)std::min(split, total - s0);
+        P.acc_in = s0 > 0;
+        P.defer = s0 + split < total;
+        timer_begin("gram_i8", st);
+        gram_i8_2sm<MODE_HERM><<<grid, kThreads, kSmem2, st>>>(ma, mbb2, mbb1, mbh, P);
+        timer_end(st);
+        SR_LAUNCHED();
+      }
     } else {
       SR_TRY(make_map(mb2, E, Kp, nc, BN));
       SR_TRY(launch_herm(ma, mb2, P, 2 * Kp / BKB, st));
