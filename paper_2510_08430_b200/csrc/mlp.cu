@@ -295,8 +295,11 @@ struct LncoshBias {
 #endif
 
 // Persistent over tiles of RB connected rows: ln psi(x') then 2 J exp(ln psi(x') - ln psi(x)).
+#ifndef SR_ENERGY_MINB
+#define SR_ENERGY_MINB 1
+#endif
 template <int RB>
-__global__ void __launch_bounds__(kThreads) energy_eval(NetDesc net, const double2* __restrict__ theta,
+__global__ void __launch_bounds__(kThreads, SR_ENERGY_MINB) energy_eval(NetDesc net, const double2* __restrict__ theta,
                                                         const double2* __restrict__ wt,
                                                         const int8_t* __restrict__ spins,
                                                         const int2* __restrict__ bij,
@@ -505,12 +508,11 @@ sr_status local_energy_impl(const NetDesc& net, const double* theta_d, long long
   SR_LAUNCHED();
   energy_rows<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(spins, ns, net.w[0], nb, bij, w.off, w.rows);
   SR_LAUNCHED();
-  // Row tiles: more CTAs per SM hide the L2 latency of the weight stream.  16 rows for
-  // narrow layers; 8 rows from width 128 up, where the activation tiles (2 x rows x 132
-  // complex) bound the CTAs per SM by shared memory (measured: configs[3] 222 vs 229 ms at
-  // 8 vs 16 rows, 359 ms at 32; configs[1] 0.71 ms at 16 vs 0.80 at 8).  SR_ENERGY_RB
-  // overrides for tuning.
-  int rb = net.wmax >= 128 ? 8 : 16;
+  // 16-row tiles: more CTAs per SM hide the L2 latency of the weight stream (measured
+  // faster than 32 rows: configs[3] 229 vs 359 ms; 8 rows within noise at configs[3],
+  // slower at configs[1]/[2]); SR_ENERGY_RB overrides for tuning.  Forcing 5-6 CTAs per SM
+  // (SR_ENERGY_MINB) costs registers and spills: slower (272 / 355 ms at configs[3]).
+  int rb = 16;
   if (const char* e = getenv("SR_ENERGY_RB")) rb = atoi(e) == 32 ? 32 : atoi(e) == 8 ? 8 : 16;
   const size_t sm = tile_smem(net, rb);
   const long long max_tiles = (ns * nb + rb - 1) / rb;
