@@ -63,6 +63,9 @@ constexpr uint32_t kACol = kSlices * BN;  // TMEM columns [448, 504): the A digi
 #ifndef SR_OZ_BAND
 #define SR_OZ_BAND 8
 #endif
+#ifndef SR_OZ_PF
+#define SR_OZ_PF 0   // > 0: the producer prefetches the boxes of stage kk + SR_OZ_PF into L2
+#endif
 constexpr int kBand = SR_OZ_BAND;         // row panels per rasterisation band
 constexpr int kNonFinite = 1 << 20;       // column exponent marking a column with Inf / NaN
 constexpr int kMaxBlk = 24;
@@ -134,6 +137,12 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       "[%5];\n" ::"r"(dst),
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
+}
+// L2 prefetch of a future stage's box (no shared-memory write, no barrier).
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(map), "r"(c0), "r"(c1),
+               "r"(c2)
+               : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -286,6 +295,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int kc = (int)(P.kbase + kk) * BKB;
             tma_load_3d(sa, &tm_a, kc, rowA, 0, full0 + 8 * s);
             tma_load_3d(sa + kAStage, &tm_b, kB + kc, rowB, 0, full0 + 8 * s);
+          }
+          if (SR_OZ_PF > 0 && kk + SR_OZ_PF < P.kstages) {
+            const int kp = (int)(P.kbase + kk + SR_OZ_PF) * BKB;
+            tma_prefetch_3d(&tm_a, kp, rowA, 0);
+            tma_prefetch_3d(&tm_b, kB + kp, rowB, 0);
           }
           if (++s == kStages) {
             s = 0;
