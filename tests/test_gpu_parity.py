@@ -546,3 +546,24 @@ def test_ntk_two_chunks_configs1_network(sr, engine):
     ref = solvers.ntk_solve(A, et, w.lam)
     assert rel(d_ntk.cpu().numpy(), ref) < 1e-9
     assert rel(d_full.cpu().numpy(), ref) < 1e-9
+
+
+@pytest.mark.parametrize("scale", [3.0, 30.0])
+def test_large_activation_branches(sr, scale):
+    """Weights scaled up so the pre-activations span the small-argument series (|z| <= 1/4),
+    the log1p(2 sinh^2(z/2)) branch and |Re z| >= 20: ln psi, O and E_loc against the oracle."""
+    w = workloads.CONFIGS[0]
+    spins, params = workloads.make_inputs(w, 64)
+    params = [(W * scale, b * scale) for W, b in params]
+    theta = T(sr.model.pack(params))
+    lp = torch.empty(64, dtype=C128, device=dev())
+    O = torch.empty(64, w.n_params, dtype=C128, device=dev())
+    sr.sr_jacobian(w.widths, theta, T(spins), lp, O)
+    lp_ref = network.log_psi(params, spins)
+    assert rel(lp.cpu().numpy().real, lp_ref.real) < 1e-12
+    assert rel(np.exp(1j * lp.cpu().numpy().imag), np.exp(1j * lp_ref.imag)) < 1e-11
+    assert rel(O.cpu().numpy(), network.jacobian(params, spins)) < 1e-11
+    ij, jj = sr.lattice.for_workload(w)
+    e = torch.empty(64, dtype=C128, device=dev())
+    sr.sr_local_energy(w.widths, theta, T(ij), T(jj), T(spins), lp, e)
+    assert rel(e.cpu().numpy(), hamiltonian.local_energies(params, spins, hamiltonian.bonds_for(w))) < 1e-10

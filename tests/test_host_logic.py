@@ -91,3 +91,22 @@ def test_bench_workload_scaling():
         assert bench.workload_for("j1j2_10x10_w128", n).n_samples == 32768
     c = bench.config_of(bench.workload_for("j1j2_10x10_w160", 8), 8, "int8", True, "sharded")
     assert c["samples_per_gpu"] == 8192 and c["n_samples"] == 65536 and c["scaling"].startswith("weak")
+
+
+def test_lncosh_series_constants_and_accuracy():
+    """The small-argument lncosh / tanh series of the CUDA kernels (csrc/common.cuh): the
+    constants are the Bernoulli-number coefficients c_n = 2^{2n}(2^{2n}-1) B_{2n}/(2n (2n)!)
+    (lncosh z = z^2/2 - z^4/12 + ..., tanh z = z - z^3/3 + ...), and 11 terms in float64 are
+    within 5e-16 relative of 40-digit log cosh / tanh on |z| <= 1/4."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import lncosh_series as ls
+    from fractions import Fraction
+    c, t = ls.coefficients()
+    assert c[0] == Fraction(1, 2) and c[1] == Fraction(-1, 12) and c[2] == Fraction(1, 45)
+    assert t[0] == 1 and t[1] == Fraction(-1, 3) and t[2] == Fraction(2, 15)
+    h = ls.header_constants()
+    assert h["c"] == [float(x) for x in c] and h["t"] == [float(x) for x in t]
+    el, et = ls.max_rel_errors(n=800)
+    assert el < 5e-16 and et < 5e-16
