@@ -296,7 +296,7 @@ struct LncoshBias {
 
 // Persistent over tiles of RB connected rows: ln psi(x') then 2 J exp(ln psi(x') - ln psi(x)).
 #ifndef SR_ENERGY_MINB
-#define SR_ENERGY_MINB 1
+#define SR_ENERGY_MINB 3   // 85 registers: 3 CTAs per SM (measured: configs[3] 182 vs 189 ms at 1, 193 at 4; configs[1] 0.61 vs 0.64 ms)
 #endif
 template <int RB>
 __global__ void __launch_bounds__(kThreads, SR_ENERGY_MINB) energy_eval(NetDesc net, const double2* __restrict__ theta,
