@@ -33,7 +33,22 @@ namespace {
 using cholk::NB;
 using cholk::chol_diag;
 using cholk::kDiagSmem;
-constexpr int kStrip = SR_KSTRIP;   // panels per strip (deferred trailing update with K = 64 kStrip)
+constexpr int kStrip = SR_KSTRIP;   // panels per back-substitution strip (one cluster CTA each)
+// Panels per factorisation strip (deferred trailing update with K = 64 x strip), by block
+// size: 8 below 20000 rows (chain-bound blocks: the strip's panels are on the chain), 16 from
+// 20000 (throughput-bound: half the read-modify-write passes over the trailing matrix).
+// Measured: configs[4]'s 25760 blocks 4350 -> 4146 ms per step at 16 (4207 at 12); configs[3]
+// (16512) and configs[1] (6480) equal or slower at 12/16.  SR_KSTRIP_F forces one value.
+constexpr int kFStripMax = 16;
+int fstrip(long long n) {
+  static int forced = -2;
+  if (forced == -2) {
+    const char* e = getenv("SR_KSTRIP_F");
+    forced = e ? std::max(1, std::min(kFStripMax, atoi(e))) : -1;
+  }
+  if (forced > 0) return forced;
+  return n >= 20000 ? 16 : kStrip;
+}
 
 __global__ void chol_init(CholSet cs, double lam, int inplace, int b0) {
   TraceScope trace_(TR_INIT, b0);
@@ -222,7 +237,7 @@ void carve_chol(Arena& a, CholSet& cs, const long long* sizes, int nblk) {
     B.rhs = a.take<double2>(B.npad);
     B.xout = a.take<double2>(B.npad);
     B.linv = a.take<double2>((size_t)B.P * NB * NB);
-    B.tws_bytes = oz::trail_workspace_bytes(B.npad, (long long)kStrip * NB);
+    B.tws_bytes = oz::trail_workspace_bytes(B.npad, (long long)fstrip(B.n) * NB);
     B.tws = a.take<char>(B.tws_bytes);
   }
 }
@@ -324,8 +339,9 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
   // ec / eb are waited on only once recorded by this call (inside a CUDA-graph capture, a
   // wait on an event last recorded outside it is an error, not a no-op)
   bool ec_rec = false, eb_rec = false;
-  for (int p0 = 0; p0 < B.P; p0 += kStrip) {
-    const int pend = std::min(p0 + kStrip, B.P);
+  const int kFStrip = fstrip(B.n);
+  for (int p0 = 0; p0 < B.P; p0 += kFStrip) {
+    const int pend = std::min(p0 + kFStrip, B.P);
     for (int p = p0; p < pend; p++) {
       timer_begin("chol_diag", st);
       if (pdl_chain()) SR_CUDA(launch_pdl(chol_diag, dim3(1), dim3(256), kDiagSmem, st, B, cs.info, p, p0));
@@ -431,7 +447,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
       const double2* lp = B.Fm + (long long)pend * NB * B.npad + (long long)p0 * NB;
       double2* trailing = B.Fm + (long long)pend * NB * B.npad + (long long)pend * NB;
       const long long K = (long long)(pend - p0) * NB;
-      const long long look = (long long)kStrip * NB;   // the next strip's columns
+      const long long look = (long long)kFStrip * NB;   // the next strip's columns
       if (i8 && lookahead(cs.count) && m > look) {
         // Lookahead: the chain needs only the next strip's columns (a), so the rest of the
         // trailing matrix (b) is updated on s4 (lowest priority, non-persistent grid) while
@@ -441,7 +457,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
         if (pending_b) SR_CUDA(cudaStreamWaitEvent(st, Q.et, 0));
         SR_TRY(oz::trail_split_i8(lp, B.npad, m, K, B.tws, B.tws_bytes, st));
         SR_CUDA(cudaEventRecord(Q.es, st));
-        SR_TRY(oz::trail_apply_i8(m, K, trailing, B.npad, B.tws, 0, kStrip, trail_ctas(cs.count), st));
+        SR_TRY(oz::trail_apply_i8(m, K, trailing, B.npad, B.tws, 0, kFStrip, trail_ctas(cs.count), st));
         SR_CUDA(cudaStreamWaitEvent(Q.s4, Q.es, 0));
         static const int b_ctas = env_int("SR_TRAIL_B_CTAS", 120);   // > 0: persistent (b) on that many CTAs
         SR_TRY(oz::trail_apply_i8(m, K, trailing, B.npad, B.tws, look, 0, b_ctas > 0 ? b_ctas : -trail_b_tpc(), Q.s4));

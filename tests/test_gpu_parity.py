@@ -453,7 +453,9 @@ def test_library_graph_capture(sr):
     {"SR_INSTRIP_LEFT": "0", "SR_TRSM_SPLIT": "0"},
     {"SR_LOOKAHEAD": "1", "SR_SIDE_AFTER_NEXT": "0"},
     {"SR_LOOKAHEAD": "0", "SR_PDL": "0"},
-], ids=["pipe", "right_looking_whole_trsm", "lookahead_all", "no_lookahead_no_pdl"])
+    {"SR_KSTRIP_F": "16"},
+    {"SR_KSTRIP_F": "3", "SR_OZ_KSPLIT": "4096"},
+], ids=["pipe", "right_looking_whole_trsm", "lookahead_all", "no_lookahead_no_pdl", "fstrip16", "fstrip3_ksplit4096"])
 def test_switches_keep_parity(env):
     """The measurement switches change scheduling only: the step, the block
     solve and the full/NTK solves stay within tolerance under each non-default setting (run
