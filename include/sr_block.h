@@ -336,6 +336,28 @@ SR_API sr_status sr_cg_axpy(int64_t n, const double* x, double* y, const double*
 SR_API sr_status sr_cg_xpby(int64_t n, const double* x, double* y, const double* num, const double* den,
                             void* stream);
 
+/* Distributed dense full-QGT solve support (parallel.dist_full_qgt: S held by block rows
+ * across ranks, right-looking blocked Cholesky with the panels broadcast; §2
+ * "S . delta theta = -F" with the full QGT):
+ *   sr_gram_tn      C = A^H B for A (k x m, lda) and B (k x n, ldb) row-major, C (m x n, ldc):
+ *                   the partial QGT rows A_r[:, rows]^H A_r[:, cols] (FP64 DMMA).  k = 0
+ *                   writes C = 0.
+ *   sr_gram_nh_sub  C -= A B^H for A (m x k), B (n x k), C (m x n) row-major (FP64 DMMA): the
+ *                   trailing update S_qj -= L_qp L_jp^H.
+ *   sr_chol_inv     M + lambda I = L L^H for one n x n Hermitian block M (contiguous, ld n,
+ *                   lower triangle read) by the library's blocked Cholesky, and the explicit
+ *                   inverse Linv = L^{-1} (one CTA per 64-column tile column, forward
+ *                   substitution with the factorisation's 64x64 diagonal-tile inverses):
+ *                   L (ldl) and Linv (ldv) are written lower triangular with zeros above;
+ *                   info as for sr_block_solve.  Workspace sr_chol_inv_workspace_bytes(n). */
+SR_API sr_status sr_gram_tn(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                            int64_t ldb, double* C, int64_t ldc, void* stream);
+SR_API sr_status sr_gram_nh_sub(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                                int64_t ldb, double* C, int64_t ldc, void* stream);
+SR_API size_t sr_chol_inv_workspace_bytes(int64_t n);
+SR_API sr_status sr_chol_inv(int64_t n, const double* M, double lambda, double* L, int64_t ldl, double* Linv,
+                             int64_t ldv, int32_t* info, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---------------------------------------------------------------- full step ---
  * sr_step — stages (1)-(5) back to back on device buffers (uniform weights):
  *   theta complex [n_p], spins int8 [n_samples][N], bonds as in stage (2);

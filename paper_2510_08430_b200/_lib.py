@@ -43,6 +43,10 @@ SIGNATURES = {
     "sr_zdotc": (_i32, [_i64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "sr_cg_axpy": (_i32, [_i64, _vp, _vp, _vp, _vp, _dbl, _vp]),
     "sr_cg_xpby": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp]),
+    "sr_gram_tn": (_i32, [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
+    "sr_gram_nh_sub": (_i32, [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
+    "sr_chol_inv_workspace_bytes": (_sz, [_i64]),
+    "sr_chol_inv": (_i32, [_i64, _vp, _dbl, _vp, _i64, _vp, _i64, _vp, _vp, _sz, _vp]),
     "sr_graph_capture_begin": (_i32, [C.c_void_p]),
     "sr_graph_capture_end": (_i32, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "sr_graph_launch": (_i32, [C.c_void_p, C.c_void_p]),
@@ -357,6 +361,34 @@ def sr_aHv(A, v, alpha, out, workspace=None):
     ws = _workspace(lib.sr_aHv_workspace_bytes(A.shape[0], A.shape[1]), A.device, workspace)
     _check(lib.sr_aHv(A.shape[0], A.shape[1], _ptr(A), lda, _ptr(v), float(alpha), _ptr(out), *_ws_args(ws),
                       _stream(A.device)), "sr_aHv")
+
+
+def sr_gram_tn(A, B, C_out):
+    """C_out = A^H B (A: k x m, B: k x n; column slices allowed)."""
+    lda, ldb, ldc = _cols(A, "A"), _cols(B, "B"), _cols(C_out, "C")
+    if A.shape[0] != B.shape[0] or C_out.shape[0] != A.shape[1] or C_out.shape[1] != B.shape[1]:
+        raise SRError("sr_gram_tn: shape mismatch")
+    _check(load().sr_gram_tn(A.shape[1], B.shape[1], A.shape[0], _ptr(A), lda, _ptr(B), ldb, _ptr(C_out), ldc,
+                             _stream(A.device)), "sr_gram_tn")
+
+
+def sr_gram_nh_sub(A, B, C_out):
+    """C_out -= A B^H (rows of A against rows of B; slices allowed)."""
+    lda, ldb, ldc = _cols(A, "A"), _cols(B, "B"), _cols(C_out, "C")
+    if A.shape[1] != B.shape[1] or C_out.shape[0] != A.shape[0] or C_out.shape[1] != B.shape[0]:
+        raise SRError("sr_gram_nh_sub: shape mismatch")
+    _check(load().sr_gram_nh_sub(A.shape[0], B.shape[0], A.shape[1], _ptr(A), lda, _ptr(B), ldb, _ptr(C_out), ldc,
+                                 _stream(A.device)), "sr_gram_nh_sub")
+
+
+def sr_chol_inv(M, lam, L_out, Linv_out, info=None, workspace=None):
+    """M + lam I = L L^H (M contiguous n x n, lower triangle read); L_out, Linv_out = L, L^{-1}."""
+    lib = load()
+    n = M.shape[0]
+    _dev(M, torch.complex128, "M")
+    ws = _workspace(lib.sr_chol_inv_workspace_bytes(n), M.device, workspace)
+    _check(lib.sr_chol_inv(n, _ptr(M), float(lam), _ptr(L_out), _cols(L_out, "L"), _ptr(Linv_out),
+                           _cols(Linv_out, "Linv"), _ptr(info), *_ws_args(ws), _stream(M.device)), "sr_chol_inv")
 
 
 def sr_av(A, v, alpha, out):

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsrblock.so")
-SOURCES = ["mlp.cu", "center.cu", "chol.cu", "ozaki.cu", "cg.cu", "capi.cu"]
+SOURCES = ["mlp.cu", "center.cu", "chol.cu", "ozaki.cu", "cg.cu", "panel.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -48,8 +48,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out=None) -> s
         jobs.append((cmd, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
     log_txt, failed = "", False
     for cmd, obj, p in jobs:
-        out, err = p.communicate()
-        log_txt += " ".join(cmd) + "\n" + out + err
+        so, se = p.communicate()
+        log_txt += " ".join(cmd) + "\n" + so + se
         failed |= p.returncode != 0
     link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
             *[o for _, o, _ in jobs], "-o", target + ".tmp"]

@@ -110,6 +110,16 @@ class CudaOps:
     def aHv(self, A, v, alpha, out):
         sr.sr_aHv(A, v, alpha, out)
 
+    # distributed dense full QGT (dist_full_qgt)
+    def gram_tn(self, A, B, C):
+        sr.sr_gram_tn(A, B, C)
+
+    def gram_nh_sub(self, A, B, C):
+        sr.sr_gram_nh_sub(A, B, C)
+
+    def chol_inv(self, M, lam, L, Linv):
+        sr.sr_chol_inv(M, lam, L, Linv)
+
     # matrix-free full-QGT CG (full_qgt_cg)
     def av(self, A, v, alpha, out):
         sr.sr_av(A, v, alpha, out)
@@ -174,6 +184,117 @@ def full_qgt_cg(ops, comm, A, F, lam, tol=1e-12, maxit=500):
         ops.cg_xpby(r, p, rho_new, rho)              # p = r + beta p
         rho, rho_new = rho_new, rho
     return x, it, res
+
+
+def dist_full_qgt(ops, comm, rank, world, A, F, lam, nb=1024):
+    """Full-QGT solve with S = sum_r A_r^H A_r FORMED and factorised across ranks (§2
+    "S . delta theta = -F"; north_star "full-QGT ... baselines shard the same way").
+
+    Layout: S is cut into P panels of nb rows; rank r holds the panels p = r, r + G, ...
+    (block-cyclic rows), each as its rows x columns [0, end of panel p) (lower part only):
+    n_p^2 / (2G) complex per rank (configs[3] on 8 GPUs: 9 GB instead of 146 GB on one).
+      formation    every rank forms its partial rows A_r[:, rows_q]^H A_r[:, :end_q]
+                   (sr_gram_tn) for every panel q, reduced to the owner of q;
+      step p       owner: M_pp + lambda I = L_pp L_pp^H and L_pp^{-1} (sr_chol_inv),
+                   y_p = L_pp^{-1} b_p (sr_av); L_pp^{-1} and y_p broadcast;
+                   every rank: L_qp = S_qp L_pp^{-H} for its panels q > p (sr_gram_nh),
+                   b_q -= L_qp y_p; the panel column L_{>p,p} all-gathered; trailing
+                   update S_qj -= L_qp L_jp^H for its panels q (sr_gram_nh_sub);
+      back         x_p = L_pp^{-H} (y_p - sum_{q>p} L_qp^H x_q): each rank's part of the sum
+                   (sr_aHv), all-reduced, the owner forms x_p, broadcast.
+    b = -F, so x = dtheta.  Returns dtheta on every rank."""
+    c = torch.complex128
+    dev = F.device
+    n = F.numel()
+    P = (n + nb - 1) // nb
+    rows = [(p * nb, min(n, (p + 1) * nb)) for p in range(P)]
+    owner = [p % world for p in range(P)]
+    mine = [p for p in range(P) if owner[p] == rank]
+    R = {p: torch.empty(rows[p][1] - rows[p][0], rows[p][1], dtype=c, device=dev) for p in mine}
+    stage = None
+    for q in range(P):                                   # formation, panel by panel
+        lo, hi = rows[q]
+        tgt = R[q] if owner[q] == rank else None
+        if tgt is None:
+            if stage is None or stage.numel() < (hi - lo) * hi:
+                stage = torch.empty((nb * n,), dtype=c, device=dev)
+            tgt = stage[:(hi - lo) * hi].view(hi - lo, hi)
+        if A.shape[0]:
+            ops.gram_tn(A[:, lo:hi], A[:, :hi], tgt)
+        else:
+            tgt.zero_()
+        comm.reduce(tgt, dst=owner[q])
+    one = torch.ones(1, dtype=c, device=dev)
+    b = {}
+    for p in mine:                                       # right-hand side b = -F
+        lo, hi = rows[p]
+        b[p] = torch.zeros(hi - lo, dtype=c, device=dev)
+        ops.cg_axpy(F[lo:hi].contiguous(), b[p], one, one, -1.0)
+    linv_own, y = {}, {}
+    for p in range(P):                                   # factorisation + forward substitution
+        lo, hi = rows[p]
+        h = hi - lo
+        Linv = torch.empty(h, h, dtype=c, device=dev)
+        yp = torch.empty(h, dtype=c, device=dev)
+        if owner[p] == rank:
+            D = R[p][:, lo:hi].contiguous()
+            L = torch.empty(h, h, dtype=c, device=dev)
+            ops.chol_inv(D, lam, L, Linv)
+            R[p][:, lo:hi].copy_(L)
+            ops.av(Linv, b[p], 1.0, yp)
+            linv_own[p] = Linv
+        comm.broadcast(Linv, src=owner[p])
+        comm.broadcast(yp, src=owner[p])
+        y[p] = yp
+        later = [q for q in mine if q > p]
+        for q in later:                                  # TRSM and right-hand side
+            Sqp = R[q][:, lo:hi]
+            Lqp = torch.empty_like(Sqp)
+            ops.gram_nh(Sqp, Linv, Lqp)                  # S_qp L_pp^{-H}
+            Sqp.copy_(Lqp)
+            t = torch.empty(Lqp.shape[0], dtype=c, device=dev)
+            ops.av(Lqp, yp, -1.0, t)
+            ops.cg_axpy(t, b[q], one, one, 1.0)
+        if p + 1 == P:
+            break
+        # the panel column L_{q,p}, q > p, on every rank: all-gather each rank's later panels
+        cnt = [len([q for q in range(p + 1, P) if owner[q] == g]) for g in range(world)]
+        mx = max(cnt)
+        if mx == 0:
+            continue
+        pack = torch.zeros(mx, nb, h, dtype=c, device=dev)
+        for i, q in enumerate(later):
+            pack[i, :R[q].shape[0]].copy_(R[q][:, lo:hi])
+        packs = [torch.empty_like(pack) for _ in range(world)]
+        comm.all_gather(packs, pack)
+        col = torch.empty(n - hi, h, dtype=c, device=dev)
+        for g in range(world):
+            for i, q in enumerate([q for q in range(p + 1, P) if owner[q] == g]):
+                qlo, qhi = rows[q]
+                col[qlo - hi:qhi - hi].copy_(packs[g][i, :qhi - qlo])
+        del packs, pack
+        for q in later:                                  # trailing update of this rank's panels
+            qlo, qhi = rows[q]
+            ops.gram_nh_sub(R[q][:, lo:hi], col[:qhi - hi], R[q][:, hi:qhi])
+        del col
+    x = {}
+    for p in reversed(range(P)):                         # back substitution
+        lo, hi = rows[p]
+        h = hi - lo
+        s_ = torch.zeros(h, dtype=c, device=dev)
+        for q in [q for q in mine if q > p]:
+            t = torch.empty(h, dtype=c, device=dev)
+            ops.aHv(R[q][:, lo:hi], x[q], 1.0, t)
+            ops.cg_axpy(t, s_, one, one, 1.0)
+        comm.all_reduce(s_)
+        xp = torch.empty(h, dtype=c, device=dev)
+        if owner[p] == rank:
+            r_ = y[p].clone()
+            ops.cg_axpy(s_, r_, one, one, -1.0)
+            ops.aHv(linv_own[p], r_, 1.0, xp)            # L_pp^{-H} (y_p - sum)
+        comm.broadcast(xp, src=owner[p])
+        x[p] = xp
+    return torch.cat([x[p] for p in range(P)])
 
 
 def shard_range(n, rank, world):
@@ -603,7 +724,8 @@ class ShardedStep:
         return b.dtheta, b.energy
 
     # --- comparison paths, sharded the same way (north_star); call after run() ---
-    DENSE_FULL_MAX = 40000   # n_p above which the full QGT is not formed (method "auto")
+    DENSE_FULL_MAX = 40000   # n_p above which the full QGT is not formed on one rank (method "auto")
+    dist_nb = 1024           # panel rows of the distributed dense full QGT (method "dist")
 
     def full_qgt_solve(self, method="auto", tol=1e-12):
         """Full-QGT solve with samples sharded.  method "dense": each rank's partial
@@ -614,6 +736,8 @@ class ShardedStep:
         DENSE_FULL_MAX parameters.  Returns dtheta (every rank); self.cg_info holds
         (iterations, relative residual) of the last CG solve."""
         b, o, c = self.buf, self.ops, self.comm
+        if method == "dist":
+            return dist_full_qgt(o, c, self.rank, self.world, b.O, b.F, self.lam, nb=self.dist_nb)
         if method == "cg" or (method == "auto" and b.n_p > self.DENSE_FULL_MAX):
             d, it, res = full_qgt_cg(o, c, b.O, b.F, self.lam, tol=tol)
             self.cg_info = (it, res)

@@ -55,6 +55,8 @@ def _loopback(world, w, spins, ij, jj, dev, theta, per_block=True, compare=False
         if compare:
             out += [step.full_qgt_solve().clone(), step.ntk_solve().clone(),
                     step.full_qgt_solve(method="cg").clone()]
+            step.dist_nb = 128
+            out += [step.full_qgt_solve(method="dist").clone()]
         torch.cuda.synchronize()
         return out
 
@@ -85,12 +87,13 @@ def test_loopback_configs0_oracle_and_comparison_paths(world, per_block):
     off = network.layer_offsets(params)
     ref = solvers.block_solve(estimators.qgt_blocks(O, off), estimators.force(O, e), off, w.lam)
     full = solvers.full_solve(estimators.qgt_full(O), estimators.force(O, e), w.lam)
-    d, en, d_full, d_ntk, d_cg = (x.cpu().numpy() for x in outs[0])
+    d, en, d_full, d_ntk, d_cg, d_dist = (x.cpu().numpy() for x in outs[0])
     assert np.linalg.norm(d - ref) / np.linalg.norm(ref) < 1e-9
     assert abs(en[0] - estimators.energy(e)) < 1e-12 * abs(estimators.energy(e))
     assert np.linalg.norm(d_full - full) / np.linalg.norm(full) < 1e-9
     assert np.linalg.norm(d_ntk - full) / np.linalg.norm(full) < 1e-9
     assert np.linalg.norm(d_cg - full) / np.linalg.norm(full) < 1e-9
+    assert np.linalg.norm(d_dist - full) / np.linalg.norm(full) < 1e-9
     for r in range(world):
         assert torch.equal(outs[r][3], outs[0][3])
 
@@ -210,3 +213,89 @@ def test_av_zdotc_cg_kernels():
         y3 = yd.clone()
         sr.sr_cg_xpby(xd, y3, num, den)
         assert np.linalg.norm(y3.cpu().numpy() - (x + a * y)) < 1e-13 * np.linalg.norm(y)
+
+
+def test_panel_kernels():
+    """sr_gram_tn (C = A^H B), sr_gram_nh_sub (C -= A B^H) and sr_chol_inv (L and L^{-1} of
+    M + lambda I) against numpy on ragged sizes, column-slice operands."""
+    import paper_2510_08430_b200 as sr
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(12)
+    cx = lambda *s: rng.standard_normal(s) + 1j * rng.standard_normal(s)   # noqa: E731
+    T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)        # noqa: E731
+    for k, m, n in ((1, 1, 1), (70, 63, 130), (300, 65, 64)):
+        Aw, Bw = cx(k, m + 3), cx(k, n + 1)
+        C = torch.full((m, n), 5.0 + 0j, dtype=torch.complex128, device=dev)
+        sr.sr_gram_tn(T(Aw)[:, 2:2 + m], T(Bw)[:, :n], C)
+        ref = Aw[:, 2:2 + m].conj().T @ Bw[:, :n]
+        assert np.linalg.norm(C.cpu().numpy() - ref) / np.linalg.norm(ref) < 1e-14
+        A2, B2, C0 = cx(m, k), cx(n, k), cx(m, n)
+        C2 = T(C0)
+        sr.sr_gram_nh_sub(T(A2), T(B2), C2)
+        ref2 = C0 - A2 @ B2.conj().T
+        assert np.linalg.norm(C2.cpu().numpy() - ref2) / np.linalg.norm(ref2) < 1e-14
+    for n in (1, 63, 64, 65, 200, 1024):
+        X = cx(2 * n, n) / np.sqrt(4 * n)
+        M = X.conj().T @ X
+        lam = 1e-2
+        L = torch.empty(n, n, dtype=torch.complex128, device=dev)
+        Li = torch.empty(n, n, dtype=torch.complex128, device=dev)
+        info = torch.full((1,), -1, dtype=torch.int32, device=dev)
+        sr.sr_chol_inv(T(np.tril(M) + np.triu(cx(n, n), 1)), lam, L, Li, info=info)   # upper triangle ignored
+        Lh, Lih = L.cpu().numpy(), Li.cpu().numpy()
+        assert info.item() == 0
+        Mref = M + lam * np.eye(n)
+        assert np.linalg.norm(Lh @ Lh.conj().T - Mref) / np.linalg.norm(Mref) < 1e-13
+        assert np.allclose(np.triu(Lh, 1), 0) and np.allclose(np.triu(Lih, 1), 0)
+        assert np.linalg.norm(Lih @ Lh - np.eye(n)) / np.sqrt(n) < 1e-12
+
+
+@pytest.mark.parametrize("world,nb", [(1, 1024), (3, 200)])
+def test_dist_full_qgt_gpu(world, nb):
+    """parallel.dist_full_qgt with the real kernels (sr_gram_tn formation reduced to panel
+    owners, sr_chol_inv diagonal blocks, sr_gram_nh TRSM, sr_gram_nh_sub trailing updates,
+    sr_av / sr_aHv substitutions) over loopback ranks: an O(1)-conditioned QGT against numpy,
+    and configs[1]'s centred Jacobian (n_p = 16240, 4096 samples) against the single-GPU dense
+    sr_full_qgt_solve."""
+    import paper_2510_08430_b200 as sr
+    from paper_2510_08430_b200 import parallel
+    sr.load()
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(world)
+    ns, n_p, lam = 700, 450, 1e-3
+    A = (rng.standard_normal((ns, n_p)) + 1j * rng.standard_normal((ns, n_p))) / np.sqrt(2 * ns)
+    F = rng.standard_normal(n_p) + 1j * rng.standard_normal(n_p)
+    ref = -np.linalg.solve(A.conj().T @ A + lam * np.eye(n_p), F)
+
+    def solve(Ad, Fd, nb_):
+        bounds = [parallel.shard_range(Ad.shape[0], r, world) for r in range(world)]
+
+        def make(r, comm, lock):
+            return comm, lock
+
+        def work(r, cl):
+            comm, lock = cl
+            ops = parallel.locked(parallel.CudaOps([4, 4], 1, 1, dev), lock)
+            lo, hi = bounds[r]
+            x = parallel.dist_full_qgt(ops, comm, r, world, Ad[lo:hi], Fd, lam, nb=nb_)
+            torch.cuda.synchronize()
+            return x
+        outs = parallel.run_loopback(world, make, work)
+        for o in outs[1:]:
+            assert torch.equal(o, outs[0])
+        return outs[0]
+
+    x = solve(torch.from_numpy(A).to(dev), torch.from_numpy(F).to(dev), min(nb, 128))
+    assert np.linalg.norm(x.cpu().numpy() - ref) / np.linalg.norm(ref) < 1e-10
+    # configs[1] at full size
+    sr_, w, spins, params, ij, jj, dev, theta = _setup(1)
+    step = parallel.LocalStep(w.widths, spins, ij, jj, w.lam, dev)
+    step.run(theta)
+    b = step.buf
+    step.buf.S = None
+    step.ops.ws = None
+    torch.cuda.empty_cache()
+    d_ref = torch.empty_like(b.F)
+    sr.sr_full_qgt_solve(b.O, b.F, w.lam, d_ref)
+    d = solve(b.O, b.F, nb)
+    assert _rel(d, d_ref) < 1e-10

@@ -71,6 +71,19 @@ class OracleOps:
     def av(self, A, v, alpha, out):
         out.copy_(alpha * (A @ v))
 
+    def gram_tn(self, A, B, C):
+        C.copy_(A.conj().T @ B)
+
+    def gram_nh_sub(self, A, B, C):
+        C.sub_(A @ B.conj().T)
+
+    def chol_inv(self, M, lam, L, Linv):
+        m = M.numpy()
+        m = np.tril(m) + np.tril(m, -1).conj().T + lam * np.eye(m.shape[0])
+        l_ = np.linalg.cholesky(m)
+        L.copy_(torch.from_numpy(l_))
+        Linv.copy_(torch.from_numpy(np.tril(np.linalg.inv(l_))))
+
     def zdotc(self, x, y, out):
         out.copy_(torch.vdot(x, y).reshape(1))
 
@@ -106,9 +119,12 @@ def _worker(rank, world, port, result_path):
     d, e = step.run(torch.from_numpy(sr.model.pack(params)))
     d_full = step.full_qgt_solve()   # comparison paths, sharded the same way
     d_cg = step.full_qgt_solve(method="cg")
+    step.dist_nb = 100                # 7 panels of the 640-parameter QGT, block-cyclic over ranks
+    d_dist = step.full_qgt_solve(method="dist")
     d_ntk = step.ntk_solve()
     if rank == 0:
-        np.save(result_path, np.concatenate([d.numpy(), e.numpy(), d_full.numpy(), d_ntk.numpy(), d_cg.numpy()]))
+        np.save(result_path, np.concatenate([d.numpy(), e.numpy(), d_full.numpy(), d_ntk.numpy(), d_cg.numpy(),
+                                             d_dist.numpy()]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -130,8 +146,8 @@ def test_sharded_step_equals_unsharded_oracle(tmp_path, world):
     res = np.load(out)
     w = workloads.CONFIGS[0].with_samples(64)
     n_p = w.n_params
-    got, got_full, got_ntk, got_cg = (res[:n_p + 1], res[n_p + 1:2 * n_p + 1], res[2 * n_p + 1:3 * n_p + 1],
-                                      res[3 * n_p + 1:])
+    got, got_full, got_ntk, got_cg, got_dist = (res[:n_p + 1], res[n_p + 1:2 * n_p + 1], res[2 * n_p + 1:3 * n_p + 1],
+                                                res[3 * n_p + 1:4 * n_p + 1], res[4 * n_p + 1:])
     spins, params = workloads.make_inputs(w)
     O = network.jacobian(params, spins)
     e = hamiltonian.local_energies(params, spins, hamiltonian.bonds_for(w))
@@ -144,6 +160,7 @@ def test_sharded_step_equals_unsharded_oracle(tmp_path, world):
     assert np.linalg.norm(got_full - full) / np.linalg.norm(full) < 1e-10
     assert np.linalg.norm(got_ntk - full) / np.linalg.norm(full) < 1e-10
     assert np.linalg.norm(got_cg - full) / np.linalg.norm(full) < 1e-10
+    assert np.linalg.norm(got_dist - full) / np.linalg.norm(full) < 1e-10
 
 
 @pytest.mark.parametrize("world", [3, 8])
@@ -211,3 +228,30 @@ def test_ntk_ring_schedule_covers_each_pair_once():
                     assert dst is None or sched[dst][t][1] == r     # the receiver expects it
         assert sorted(pairs) == sorted((i, j) for i in range(G) for j in range(i + 1)), G
         assert max(len([s for s in sched[r] if s[0] == 0 or s[1] is not None]) for r in range(G)) <= G // 2 + 1
+
+
+@pytest.mark.parametrize("world,nb", [(1, 64), (3, 50), (4, 37)])
+def test_dist_full_qgt_o1_conditioned(world, nb):
+    """parallel.dist_full_qgt (S formed and factorised by block-cyclic panel rows across ranks)
+    on an O(1)-conditioned S = A^H A (||S|| ~ 1 >> lambda), ragged panels, loopback ranks with
+    the oracle's arithmetic, against numpy's dense solve."""
+    from paper_2510_08430_b200 import parallel
+    rng = np.random.default_rng(world * 100 + nb)
+    ns, n_p, lam = 300, 210, 1e-3
+    A = (rng.standard_normal((ns, n_p)) + 1j * rng.standard_normal((ns, n_p))) / np.sqrt(2 * ns)
+    F = rng.standard_normal(n_p) + 1j * rng.standard_normal(n_p)
+    ref = -np.linalg.solve(A.conj().T @ A + lam * np.eye(n_p), F)
+    bounds = [parallel.shard_range(ns, r, world) for r in range(world)]
+
+    def make(r, comm, lock):
+        return comm, lock
+
+    def work(r, cl):
+        comm, lock = cl
+        lo, hi = bounds[r]
+        return parallel.dist_full_qgt(parallel.locked(OracleOps(), lock), comm, r, world,
+                                      torch.from_numpy(A[lo:hi].copy()), torch.from_numpy(F), lam, nb=nb).numpy()
+
+    outs = parallel.run_loopback(world, make, work)
+    for x in outs:
+        assert np.linalg.norm(x - ref) / np.linalg.norm(ref) < 1e-10
