@@ -29,11 +29,11 @@ sizes = w.layer_sizes
 ranges = parallel.block_ranges(sizes, world)
 olo, ohi = ranges[rank]
 offs = sr.block_offsets(w.widths)
-own_offs = [offs[b] - offs[olo] for b in range(olo, ohi + 1)]
+own_offs = [offs[b] - offs[olo] for b in range(olo, ohi + 1)] if ohi > olo else None
 ops = parallel.CudaOps(w.widths, hi - lo, len(jj), dev, "int8", solve_offsets=own_offs)
 buf = parallel._Buffers(w.widths, spins, ij, jj, dev, full_s=False)
 theta = torch.from_numpy(sr.model.pack(params)).to(dev)
-S_own = torch.empty(sum(n * n for n in sizes[olo:ohi]), dtype=torch.complex128, device=dev)
+S_own = torch.empty(max(1, sum(n * n for n in sizes[olo:ohi])), dtype=torch.complex128, device=dev)
 others = [n * n for b, n in enumerate(sizes) if not olo <= b < ohi]
 staging = [torch.empty(max(others), dtype=torch.complex128, device=dev) for _ in range(min(2, len(others)))]
 
@@ -73,7 +73,8 @@ def grams():
 ms["partial_grams"] = t(grams)
 F_own = buf.F[offs[olo]:offs[ohi]]
 d_own = torch.empty_like(F_own)
-ms["owner_solve"] = t(lambda: ops.block_solve(own_offs, S_own, F_own, w.lam, d_own))
+if own_offs is not None:
+    ms["owner_solve"] = t(lambda: ops.block_solve(own_offs, S_own, F_own, w.lam, d_own))
 total = sum(ms.values())
 bytes_s = 16 * sum(n * n for b, n in enumerate(sizes) if not olo <= b < ohi)
 print(f"{w.name}, rank {rank} of {world}: {hi - lo} samples, owns blocks {list(range(olo, ohi))} "
