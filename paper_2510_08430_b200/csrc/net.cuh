@@ -50,7 +50,7 @@ __device__ __forceinline__ void net_dmma(double& c0, double& c1, double a, doubl
 // in flight; measured: local energy 0.722 -> 0.695 ms at configs[1], 35.5 -> 31.8 ms at
 // configs[2]; the Jacobian kernels are faster without it, 0.258 vs 0.299 ms).
 #ifndef SR_DENSE_BQ
-#define SR_DENSE_BQ 8
+#define SR_DENSE_BQ 4   // measured with the fused series epilogue: 4 / 8 / 16 -> configs[1] 0.575 / 0.61 / 0.65 ms, configs[3] 180 / 182 / 195 ms
 #endif
 // Epilogue applied to each output element in registers before it is stored (Identity: z).
 struct ZIdentity {
