@@ -371,6 +371,8 @@ def test_full_size_config(sr, cfg):
         got = blocks[i][loc][:, loc].cpu().numpy()
         ref = estimators.qgt_full(O_gpu[:, sel])
         assert rel(got, ref) < 1e-11
+        d_ = np.sqrt(np.abs(np.diag(ref)).real)      # entrywise: |dS_ij| <= 1e-11 sqrt(S_ii S_jj)
+        assert np.all(np.abs(got - ref) <= 1e-11 * np.outer(d_, d_))
         Sb = blocks[i]
         assert torch.equal(Sb, Sb.conj().T.resolve_conj())   # exactly Hermitian as stored
     # F = A^H e_tilde and the solve residual (S_b + lambda) dtheta_b = -F_b, checked with
