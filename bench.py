@@ -148,17 +148,19 @@ def workload_for(name, world):
     return w
 
 
-def config_of(w, world, engine, sharded, schedule="batched"):
+def config_of(w, world, engine, sharded, schedule="batched", chunk=0):
     """The workload description shared by both arms' JSON lines."""
-    weak = w.name in WEAK_WORKLOADS
+    weak = w.name in WEAK_WORKLOADS and w.n_samples == WEAK_WORKLOADS[w.name] * world
+    rows = min(chunk, w.n_samples) if chunk else w.n_samples // world
     return {"workload": w.name, "lattice": f"{w.lattice}{'x'.join(map(str, w.extent))}",
             "widths": list(w.widths), "n_samples": w.n_samples, "n_params": w.n_params, "blocks": block_sizes(w),
             "lambda": w.lam, "gram_engine": engine, "step_schedule": schedule,
             "samples_per_gpu": w.n_samples // world,
             "parallelism": f"samples sharded x{world} (NCCL)" if sharded else "single GPU",
-            "scaling": "weak (8192 samples per GPU)" if weak else "strong (fixed N_s)",
-            "l2": f"inputs larger than L2 (O = {16.0 * w.n_samples / world * w.n_params / 1e9:.2f} GB per GPU per step "
-                  "vs 126 MB L2); no flush"}
+            "scaling": ("weak (8192 samples per GPU)" if weak else "strong (fixed N_s)"),
+            "l2": f"inputs larger than L2 (O = {16.0 * rows * w.n_params / 1e9:.2f} GB resident per GPU"
+                  + (f", {16.0 * w.n_samples * w.n_params / 1e9:.0f} GB over the chunks" if chunk else "")
+                  + " vs 126 MB L2); no flush"}
 
 
 def _quiet_fd1(fn):
@@ -210,7 +212,7 @@ def run_gpu(args):
             dist.init_process_group("nccl", device_id=dev)
             dist.barrier()
         _quiet_fd1(_init)
-    w = workload_for(args.workload, world)
+    w = workloads.BY_NAME[args.workload] if args.full_samples else workload_for(args.workload, world)
     spins_all, params = workloads.make_inputs(w)
     ij, jj = sr.lattice.for_workload(w)
     theta_h = sr.model.pack(params)
@@ -220,8 +222,12 @@ def run_gpu(args):
     engine = args.gram_engine
     sr.sr_set_gram_engine(sr.GRAM_INT8 if engine == "int8" else sr.GRAM_FP64)   # for sr_step_host (e2e)
     schedule = "sharded" if sharded else choose_schedule(sr, torch, w, ns, len(jj), dev, args.schedule)
+    if args.chunk and not sharded:
+        schedule = f"chunked ({args.chunk} samples per pass; parallel.ChunkedStep)"
     if sharded:
         step = parallel.ShardedStep(w.widths, spins_all, ij, jj, w.lam, rank, world, dev, gram_engine=engine)
+    elif args.chunk:
+        step = parallel.ChunkedStep(w.widths, spins_all, ij, jj, w.lam, dev, chunk=args.chunk)
     else:
         step = parallel.LocalStep(w.widths, spins_all, ij, jj, w.lam, dev, gram_engine=engine, schedule=schedule)
     theta = torch.from_numpy(theta_h).to(dev)
@@ -301,10 +307,12 @@ def run_gpu(args):
     fp64 = comparison = None
     if sharded:
         e2e = run_e2e_sharded(torch, dist, step, theta_h, dev, args, theta if use_graph else None, e2e_steps)
+    elif args.chunk:
+        e2e = run_e2e_api(torch, step, theta_h, dev, theta if use_graph else None, e2e_steps)
     else:
-        if engine == "int8" and not args.no_fp64_engine:
+        if engine == "int8" and not args.no_fp64_engine and not args.chunk:
             fp64 = fp64_engine_record(sr, torch, step, theta, w, dev)
-        comparison = None if args.no_compare else compare_solves(sr, torch, step, w, dev)
+        comparison = None if (args.no_compare or args.chunk) else compare_solves(sr, torch, step, w, dev)
         del step                      # the e2e run allocates its own sr_step workspace
         torch.cuda.empty_cache()
         e2e = run_e2e(sr, torch, w, theta_h, spins_all, ij, jj, dev, args, schedule, e2e_steps)
@@ -354,9 +362,12 @@ def run_gpu(args):
     O_bytes = 16.0 * n_local * n_p
     lo, hi = parallel.shard_range(ns, rank, world) if sharded else (0, ns)
     en_flops = energy_flops(w, spins_all[lo:hi], ij)
-    jac_ms = stage_ms["jacobian"]
+    jac_ms = stage_ms.get("jacobian")
     qgt_ms = stage_ms.get("block_qgt", gram_kernel_ms)
     solve_ms = stage_ms.get("block_solve", stage_ms.get("block_qgt_solve", 0.0) - gram_kernel_ms)
+    chunked = jac_ms is None    # the chunked step times passes, not stages
+    if chunked:
+        jac_ms = 1.0
     stage_roofline = {
         "block_qgt": {"engine": engine, "fp64_equivalent_tflops": gflop / (qgt_ms * 1e-3) / 1e12,
                       "fp64_dmma_peak": FP64_PEAK_TFLOPS, "ratio": gflop / (qgt_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
@@ -366,17 +377,20 @@ def run_gpu(args):
                      "peak_gbs": peaks["hbm_gbs"], "frac": O_bytes / (jac_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                      "algorithmic": "16 B x N_s x n_p written (O)"},
         "center_force": {"bound": "hbm",
-                         "achieved_gbs": 3 * O_bytes / (stage_ms["center_force"] * 1e-3) / 1e9,
+                         "achieved_gbs": 3 * O_bytes / (stage_ms.get("center_force", 1.0) * 1e-3) / 1e9,
                          "peak_gbs": peaks["hbm_gbs"],
-                         "frac": 3 * O_bytes / (stage_ms["center_force"] * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                         "frac": 3 * O_bytes / (stage_ms.get("center_force", 1.0) * 1e-3) / 1e9 / peaks["hbm_gbs"],
                          "algorithmic": "O read twice, A written once"},
         "local_energy": {"bound": "fp64 tensor (DMMA dense layers) + FP64 ALU (lncosh)",
-                         "achieved_tflops": en_flops / (stage_ms["local_energy"] * 1e-3) / 1e12,
+                         "achieved_tflops": en_flops / (stage_ms.get("local_energy", 1.0) * 1e-3) / 1e12,
                          "peak_tflops": FP64_PEAK_TFLOPS,
-                         "frac": en_flops / (stage_ms["local_energy"] * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                         "frac": en_flops / (stage_ms.get("local_energy", 1.0) * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
                          "algorithmic": "8 x sum over connected configurations of (2 w_1 + sum_{l>=1} w_l w_{l+1}) "
                                         f"= {en_flops:.4e} flop (lncosh not counted)"},
     }
+    if chunked:
+        stage_roofline = {"block_qgt": stage_roofline["block_qgt"],
+                          "note": "chunked step: stages_ms are the two passes over the sample chunks and the solves"}
     if not sharded:
         cf = chol_flops(w)
         stage_roofline["block_solve"] = {
@@ -400,7 +414,7 @@ def run_gpu(args):
         "dtype": "f64 (int8 Ozaki-7 emulation: exact int8 digit products, FP64 recombination)" if engine == "int8"
                  else "f64 (DMMA)",
         "data": "synthetic (seeded uniform S^z=0 spins, complex-normal weights; workloads.py)",
-        "config": config_of(w, world, engine, sharded, schedule),
+        "config": config_of(w, world, engine, sharded, schedule, args.chunk),
         "roofline": roofline,
         "stage_roofline": stage_roofline,
         "stages_ms": stage_ms,
@@ -555,6 +569,32 @@ def run_e2e_sharded(torch, dist, step, theta_h, dev, args, theta_graph, steps):
                     " (C ABI + NCCL), pinned theta in, dtheta out, host-clock timed")}
 
 
+def run_e2e_api(torch, step, theta_h, dev, theta_graph, steps):
+    """e2e of a one-GPU step object through the public Python API (ChunkedStep): theta copied
+    from pinned host memory, the step (its CUDA graph when captured), dtheta read back; host
+    clock, synchronised per step."""
+    th = torch.from_numpy(theta_h).pin_memory()
+    dth = torch.empty(theta_h.shape[0], dtype=torch.complex128).pin_memory()
+    theta = theta_graph if theta_graph is not None else torch.empty(theta_h.shape[0], dtype=torch.complex128,
+                                                                     device=dev)
+
+    def one():
+        theta.copy_(th, non_blocking=True)
+        d, _ = step.replay() if theta_graph is not None else step.run(theta)
+        dth.copy_(d, non_blocking=True)
+        torch.cuda.synchronize(dev)
+
+    one()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    dt = time.perf_counter() - t0
+    return {"value": steps / dt, "unit": "steps/s", "steps": steps, "h2d_bytes_per_step": int(th.numel() * 16),
+            "d2h_bytes_per_step": int(dth.numel() * 16),
+            "api": "parallel.ChunkedStep (C ABI) " + ("graph replay" if theta_graph is not None else "run")
+                   + ", pinned theta in, dtheta out, host-clock timed"}
+
+
 def run_e2e(sr, torch, w, theta_h, spins, ij, jj, dev, args, schedule, steps):
     """e2e through sr_step_host (host buffers in and out every step), one warm call (it
     captures the step's CUDA graph) then `steps` timed calls on the host clock."""
@@ -706,6 +746,10 @@ def main():
     ap.add_argument("--schedule", default="auto", choices=["auto", "batched", "per_block"],
                     help="stages (4)-(5): all Grams then all solves, or block by block (one block's memory)")
     ap.add_argument("--no-fp64-engine", action="store_true", help="skip the FP64-engine sub-record")
+    ap.add_argument("--chunk", type=int, default=0,
+                    help="process the samples in chunks of this many (parallel.ChunkedStep; one GPU, int8 engine)")
+    ap.add_argument("--full-samples", action="store_true",
+                    help="configs[4]: all 65536 samples on this run's GPUs instead of 8192 per GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -221,6 +221,14 @@ SR_API sr_status sr_block_qgt_i8(int64_t n_samples, int n_blocks,
                                  const int64_t* block_offsets /*host*/, const double* A, int64_t lda,
                                  double* S, void* workspace, size_t workspace_bytes, void* stream);
 
+/* sr_block_qgt_i8_acc — S_b += A_b^H A_b (same layout, engine, workspace and errors as
+ * sr_block_qgt_i8; S must hold a previous result): the sample-chunked step
+ * (parallel.ChunkedStep) sums the Grams of sample chunks whose centred Jacobians are formed
+ * one after another, so that N_s x n_p never has to be resident (configs[4]: 206 GB). */
+SR_API sr_status sr_block_qgt_i8_acc(int64_t n_samples, int n_blocks, const int64_t* block_offsets /*host*/,
+                                     const double* A, int64_t lda, double* S, void* workspace,
+                                     size_t workspace_bytes, void* stream);
+
 /* sr_set_gram_engine — engine of the dense contractions: sr_step's stage (4), the Grams of
  * the comparison solves (the full QGT A^H A of sr_full_qgt_solve, the NTK A A^H of
  * sr_ntk_solve) and the deferred trailing updates (A_22 -= L_21 L_21^H, K = 512) of every

@@ -8,7 +8,7 @@ bench.py, and the sample-sharded multi-GPU orchestration over torch.distributed.
 from ._lib import (  # noqa: F401
     SRError, LIB_PATH, load, n_params, block_offsets,
     sr_jacobian, sr_local_energy, sr_center_force, sr_column_moments, sr_center_force_global,
-    sr_block_qgt, sr_block_qgt_i8, sr_set_gram_engine, sr_get_gram_engine, GRAM_FP64, GRAM_INT8,
+    sr_block_qgt, sr_block_qgt_i8, sr_block_qgt_i8_acc, sr_set_gram_engine, sr_get_gram_engine, GRAM_FP64, GRAM_INT8,
     sr_block_solve, sr_full_qgt_solve, sr_ntk_solve, sr_gram_nh, sr_aHv,
     sr_av, sr_zdotc, sr_cg_axpy, sr_cg_xpby, sr_gram_tn, sr_gram_nh_sub, sr_chol_inv,
     sr_block_qgt_solve, sr_set_step_schedule, sr_get_step_schedule, SCHED_BATCHED, SCHED_PER_BLOCK,

@@ -65,6 +65,7 @@ SIGNATURES = {
     "sr_block_qgt": (_i32, [_i64, _i32, _I64P, _vp, _i64, _vp, _vp, _sz, _vp]),
     "sr_block_qgt_i8_workspace_bytes": (_sz, [_i64, _i32, _I64P]),
     "sr_block_qgt_i8": (_i32, [_i64, _i32, _I64P, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "sr_block_qgt_i8_acc": (_i32, [_i64, _i32, _I64P, _vp, _i64, _vp, _vp, _sz, _vp]),
     "sr_set_gram_engine": (_i32, [_i32]),
     "sr_get_gram_engine": (_i32, []),
     "sr_block_solve_workspace_bytes": (_sz, [_i32, _I64P]),
@@ -267,6 +268,21 @@ def sr_block_qgt_i8(A, offsets, S, workspace=None):
     ws = _workspace(lib.sr_block_qgt_i8_workspace_bytes(A.shape[0], nblk, off), A.device, workspace)
     _check(lib.sr_block_qgt_i8(A.shape[0], nblk, off, _ptr(A), lda, _ptr(S), *_ws_args(ws),
                                _stream(A.device)), "sr_block_qgt_i8")
+
+
+def sr_block_qgt_i8_acc(A, offsets, S, workspace=None):
+    """S += A_b^H A_b per block (int8 engine; the sample-chunked step)."""
+    lib = load()
+    lda = _cols(A, "A")
+    _dev(S, torch.complex128, "S")
+    nblk = len(offsets) - 1
+    need = sum((offsets[b + 1] - offsets[b]) ** 2 for b in range(nblk))
+    if S.numel() < need:
+        raise SRError("S too small for the packed blocks")
+    off = _offsets(offsets)
+    ws = _workspace(lib.sr_block_qgt_i8_workspace_bytes(A.shape[0], nblk, off), A.device, workspace)
+    _check(lib.sr_block_qgt_i8_acc(A.shape[0], nblk, off, _ptr(A), lda, _ptr(S), *_ws_args(ws), _stream(A.device)),
+           "sr_block_qgt_i8_acc")
 
 
 GRAM_FP64, GRAM_INT8 = 0, 1

@@ -585,6 +585,17 @@ SR_API sr_status sr_block_qgt_i8(int64_t n_samples, int n_blocks, const int64_t*
                           reinterpret_cast<double2*>(S), workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
+SR_API sr_status sr_block_qgt_i8_acc(int64_t n_samples, int n_blocks, const int64_t* block_offsets, const double* A,
+                                     int64_t lda, double* S, void* workspace, size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(valid_offsets(n_blocks, block_offsets), "block_offsets must start at 0 and increase; 1..24 blocks");
+  SR_CHECK_ARG(n_samples >= 0 && lda >= block_offsets[n_blocks], "lda < n_p");
+  SR_CHECK_ARG(block_offsets[n_blocks] < (1LL << 31) / oz::kSlices, "n_p too large for the slice tensor map");
+  SR_CHECK_ARG(n_samples <= (1LL << 31) / 8, "n_samples too large");
+  SR_CHECK_ARG(S && (A || n_samples == 0), "null pointer");
+  return oz::block_qgt_i8(n_samples, n_blocks, block_offsets, reinterpret_cast<const double2*>(A), lda,
+                          reinterpret_cast<double2*>(S), workspace, workspace_bytes, (cudaStream_t)stream, 0, true);
+}
+
 SR_API void sr_kernel_timer(int enable) { g_timer = enable != 0; }
 
 SR_API sr_status sr_gram_nh(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,

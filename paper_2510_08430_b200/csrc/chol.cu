@@ -34,6 +34,10 @@ using cholk::NB;
 using cholk::chol_diag;
 using cholk::kDiagSmem;
 constexpr int kStrip = SR_KSTRIP;   // panels per back-substitution strip (one cluster CTA each)
+#ifndef SR_SIDE_TM
+#define SR_SIDE_TM 16   // rows per CTA of the off-chain skinny launches (the chain's stay at 16)
+#endif
+constexpr int kSideTM = SR_SIDE_TM;
 // Panels per factorisation strip (deferred trailing update with K = 64 x strip), by block
 // size: 8 below 20000 rows (chain-bound blocks: the strip's panels are on the chain), 16 from
 // 20000 (throughput-bound: half the read-modify-write passes over the trailing matrix).
@@ -410,16 +414,16 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
         if (p > p0 && !left && eb_rec) SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.eb, 0));
         if (split) {
           timer_begin("chol_trsm_rest", Q.s3);
-          SR_TRY((gram::launch_skinny<gram::STORE>(trsm_rest, Q.s3)));
+          SR_TRY((gram::launch_skinny<gram::STORE, kSideTM>(trsm_rest, Q.s3)));
           timer_end(Q.s3);
           SR_CUDA(cudaEventRecord(Q.er, Q.s3));   // all of L column p: the s2 job may start
         }
         timer_begin("chol_next_rows", Q.s3);
-        if (next_rows.count) SR_TRY((gram::launch_skinny<gram::SUB>(next_rows, Q.s3)));
+        if (next_rows.count) SR_TRY((gram::launch_skinny<gram::SUB, kSideTM>(next_rows, Q.s3)));
         // left-looking: column p+2 first takes the s2 job of the previous step (panels
         // p0..p-1), which began right after that step's TRSM
         if (next_rows2.count && eb_rec) SR_CUDA(cudaStreamWaitEvent(Q.s3, Q.eb, 0));
-        if (next_rows2.count) SR_TRY((gram::launch_skinny<gram::SUB>(next_rows2, Q.s3)));
+        if (next_rows2.count) SR_TRY((gram::launch_skinny<gram::SUB, kSideTM>(next_rows2, Q.s3)));
         timer_end(Q.s3);
         SR_CUDA(cudaEventRecord(Q.ec, Q.s3));
         ec_rec = true;
@@ -429,7 +433,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
         else SR_CUDA(cudaStreamWaitEvent(Q.s2, side_go, 0));
         if (split && !left) SR_CUDA(cudaStreamWaitEvent(Q.s2, Q.er, 0));
         timer_begin("chol_inner_rest", Q.s2);
-        SR_TRY((gram::launch_skinny<gram::SUB>(inner_rest, Q.s2)));
+        SR_TRY((gram::launch_skinny<gram::SUB, kSideTM>(inner_rest, Q.s2)));
         timer_end(Q.s2);
         SR_CUDA(cudaEventRecord(Q.eb, Q.s2));
         eb_rec = true;

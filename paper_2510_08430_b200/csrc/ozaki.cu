@@ -1042,13 +1042,13 @@ long long ksplit_stages() {
 }
 
 sr_status launch_herm(const CUtensorMap& ma, const CUtensorMap& mb, Params P, long long total_stages,
-                      cudaStream_t st) {
+                      cudaStream_t st, bool accumulate = false) {
   const long long split = ksplit_stages();
   const unsigned grid = (unsigned)std::min<long long>(P.total_tiles, gram_ctas());
   for (long long s0 = 0; s0 < total_stages; s0 += split) {
     P.kbase = s0;
     P.kstages = (int)std::min(split, total_stages - s0);
-    P.acc_in = s0 > 0;
+    P.acc_in = s0 > 0 || accumulate;
     P.defer = s0 + split < total_stages;
     timer_begin("gram_i8", st);
     gram_i8<MODE_HERM><<<grid, kThreads, kSmem, st>>>(ma, mb, P);
@@ -1059,9 +1059,10 @@ sr_status launch_herm(const CUtensorMap& ma, const CUtensorMap& mb, Params P, lo
 }
 
 sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double2* A, long long lda, double2* S,
-                       void* ws, size_t ws_bytes, cudaStream_t st, long long ldc) {
+                       void* ws, size_t ws_bytes, cudaStream_t st, long long ldc, bool accumulate) {
   long long s_total = 0;
   for (int b = 0; b < nblk; b++) s_total += (offs[b + 1] - offs[b]) * (offs[b + 1] - offs[b]);
+  if (ns == 0 && accumulate) return SR_OK;
   if (ns == 0) {   // empty batch: S = 0, nothing read
     SR_CUDA(cudaMemsetAsync(S, 0, (size_t)s_total * sizeof(double2), st));
     return SR_OK;
@@ -1131,7 +1132,7 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
       for (long long s0 = 0; s0 < total; s0 += split) {   // K-split launches as launch_herm
         P.kbase = s0;
         P.kstages = (int)std::min(split, total - s0);
-        P.acc_in = s0 > 0;
+        P.acc_in = s0 > 0 || accumulate;
         P.defer = s0 + split < total;
         timer_begin("gram_i8", st);
         gram_i8_2sm<MODE_HERM><<<grid, kThreads, kSmem2, st>>>(ma, mbb2, mbb1, mbh, P);
@@ -1140,7 +1141,7 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
       }
     } else {
       SR_TRY(make_map(mb2, E, Kp, nc, BN));
-      SR_TRY(launch_herm(ma, mb2, P, 2 * Kp / BKB, st));
+      SR_TRY(launch_herm(ma, mb2, P, 2 * Kp / BKB, st, accumulate));
     }
   }
   return SR_OK;

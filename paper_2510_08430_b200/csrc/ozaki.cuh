@@ -14,7 +14,8 @@ size_t workspace_bytes(long long ns, int nblk, const int64_t* offs);
 // digit slices of the column-scaled A with tcgen05 kind::i8 MMAs accumulated exactly in
 // TMEM (int32) and recombined in FP64.
 sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double2* A, long long lda, double2* S,
-                       void* ws, size_t ws_bytes, cudaStream_t st, long long ldc = 0);
+                       void* ws, size_t ws_bytes, cudaStream_t st, long long ldc = 0, bool accumulate = false);
+// (accumulate: S += A_b^H A_b instead of S = ..., the sample-chunked step.)
 // (ldc > 0, one block: the result is written with that leading dimension, e.g. straight into
 // a padded Cholesky matrix -- the full-QGT solve.)
 

@@ -92,6 +92,12 @@ class CudaOps:
         else:
             sr.sr_block_qgt(A, offs, S)
 
+    def block_qgt_acc(self, A, offs, S):
+        if self.gram_engine != "int8":
+            raise ValueError("the sample-chunked Gram accumulation runs on the int8 engine")
+        need = sr.load().sr_block_qgt_i8_workspace_bytes(A.shape[0], len(offs) - 1, sr._offsets(offs))
+        sr.sr_block_qgt_i8_acc(A, offs, S, workspace=self._ws(need))
+
     def block_solve(self, offs, S, F, lam, dtheta, info=None):
         need = sr.load().sr_block_solve_workspace_bytes(len(offs) - 1, sr._offsets(offs))
         sr.sr_block_solve(offs, S, F, lam, dtheta, info=info, workspace=self._ws(need))
@@ -436,6 +442,92 @@ class LocalStep:
     def replay(self):
         self.graph.replay()
         return self.buf.dtheta, self.buf.energy
+
+
+class ChunkedStep:
+    """The whole step on one GPU with the samples in chunks, so that N_s x n_p is never resident
+    (configs[4]'s full 65536 samples: O would be 206 GB).  Two passes over the chunks:
+      1. Jacobian, local energy, and the chunk's double-double moment row (sr_column_moments);
+      2. the Jacobian again (it is cheap next to the Gram), the n_parts = n_chunks centring of
+         the chunk (sr_center_force_global: the chunk's A and partial force), F += F_c, and
+         the chunk's Gram added to every S_b (sr_block_qgt_i8 for the first chunk,
+         sr_block_qgt_i8_acc after);
+    then each block's shifted solve, one block at a time (one block's factor copy).  The same
+    arithmetic as the sharded step with the chunks as ranks (exactly the moment rows and partial
+    Grams those ranks would exchange), summed in chunk order: deterministic."""
+
+    STAGES = ("pass1_jacobian_energy_moments", "pass2_center_force_gram", "block_solve")
+
+    def __init__(self, widths, spins, bij, bj, lam, device, chunk=8192, ops=None):
+        self.lam = lam
+        self.device = torch.device(device)
+        self.n_total = spins.shape[0]
+        self.bounds = [(lo, min(lo + chunk, self.n_total)) for lo in range(0, self.n_total, chunk)]
+        c = torch.complex128
+        self.widths = list(widths)
+        self.n_p = sr.n_params(widths)
+        self.offs = sr.block_offsets(widths)
+        self.sizes = [self.offs[b + 1] - self.offs[b] for b in range(len(self.offs) - 1)]
+        dev = self.device
+        self.spins = torch.as_tensor(np.ascontiguousarray(spins)).to(dev)
+        self.bij = torch.as_tensor(np.ascontiguousarray(bij, dtype=np.int32)).to(dev)
+        self.bj = torch.as_tensor(np.ascontiguousarray(bj, dtype=np.float64)).to(dev)
+        self.log_psi = torch.empty(self.n_total, dtype=c, device=dev)
+        self.e_loc = torch.empty(self.n_total, dtype=c, device=dev)
+        self.e_tilde = torch.empty(self.n_total, dtype=c, device=dev)
+        self.O = torch.empty(min(chunk, self.n_total), self.n_p, dtype=c, device=dev)
+        self.F = torch.empty(self.n_p, dtype=c, device=dev)
+        self.Fp = torch.empty(self.n_p, dtype=c, device=dev)
+        self.S = torch.empty(sum(n * n for n in self.sizes), dtype=c, device=dev)
+        self.dtheta = torch.empty(self.n_p, dtype=c, device=dev)
+        self.energy = torch.empty(1, dtype=c, device=dev)
+        self.rows = torch.empty(len(self.bounds), 2 * self.n_p + 2, dtype=c, device=dev)
+        self.one = torch.ones(1, dtype=c, device=dev)
+        n_max = max(self.sizes)
+        self.ops = ops or CudaOps(widths, self.O.shape[0], len(bj), dev, "int8", solve_offsets=[0, n_max])
+
+    def run(self, theta, events=None):
+        o = self.ops
+        st = torch.cuda.current_stream(self.device) if self.device.type == "cuda" else None
+        _rec(events, 0, st)
+        for c, (lo, hi) in enumerate(self.bounds):
+            O_c = self.O[:hi - lo]
+            o.jacobian(self.widths, theta, self.spins[lo:hi], self.log_psi[lo:hi], O_c)
+            o.local_energy(self.widths, theta, self.bij, self.bj, self.spins[lo:hi], self.log_psi[lo:hi],
+                           self.e_loc[lo:hi])
+            o.column_moments(O_c, self.e_loc[lo:hi], self.n_total, self.rows[c])
+        _rec(events, 1, st)
+        self.F.zero_()
+        for c, (lo, hi) in enumerate(self.bounds):
+            O_c = self.O[:hi - lo]
+            o.jacobian(self.widths, theta, self.spins[lo:hi], self.log_psi[lo:hi], O_c)
+            o.center_force_global(O_c, self.e_loc[lo:hi], self.n_total, self.rows, self.energy,
+                                  self.e_tilde[lo:hi], self.Fp)
+            o.cg_axpy(self.Fp, self.F, self.one, self.one, 1.0)
+            if c == 0:
+                o.block_qgt(O_c, self.offs, self.S)
+            else:
+                o.block_qgt_acc(O_c, self.offs, self.S)
+        _rec(events, 2, st)
+        pos = 0
+        for b, n in enumerate(self.sizes):
+            lo, hi = self.offs[b], self.offs[b + 1]
+            o.block_solve([0, n], self.S[pos:pos + n * n], self.F[lo:hi], self.lam, self.dtheta[lo:hi])
+            pos += n * n
+        _rec(events, 3, st)
+        return self.dtheta, self.energy
+
+    def capture(self, theta):
+        self.run(theta)
+        torch.cuda.synchronize(self.device)
+        self.graph = sr.Graph(self.device)
+        with self.graph.capture():
+            self.run(theta)
+        return self.graph
+
+    def replay(self):
+        self.graph.replay()
+        return self.dtheta, self.energy
 
 
 class _Done:

@@ -299,3 +299,46 @@ def test_dist_full_qgt_gpu(world, nb):
     sr.sr_full_qgt_solve(b.O, b.F, w.lam, d_ref)
     d = solve(b.O, b.F, nb)
     assert _rel(d, d_ref) < 1e-10
+
+
+@pytest.mark.parametrize("cfg,chunk", [(0, 100), (1, 1024), (1, 4096)])
+def test_chunked_step_matches_local(cfg, chunk):
+    """parallel.ChunkedStep (samples in chunks, Gram accumulated with sr_block_qgt_i8_acc, the
+    n_parts = n_chunks centring) equals the one-pass LocalStep (1e-12) and, on configs[0], the
+    oracle (1e-9); its CUDA-graph replay equals its eager run."""
+    sr, w, spins, params, ij, jj, dev, theta = _setup(cfg)
+    from paper_2510_08430_b200 import parallel
+    d_local, e_local = (x.clone() for x in parallel.LocalStep(w.widths, spins, ij, jj, w.lam, dev).run(theta))
+    step = parallel.ChunkedStep(w.widths, spins, ij, jj, w.lam, dev, chunk=chunk)
+    d, e = (x.clone() for x in step.run(theta))
+    assert _rel(d, d_local) < 1e-12
+    assert abs(e.item() - e_local.item()) <= 1e-13 * abs(e_local.item())
+    step.capture(theta)
+    assert torch.equal(step.replay()[0], d)
+    if cfg == 0:
+        O = network.jacobian(params, spins)
+        el = hamiltonian.local_energies(params, spins, hamiltonian.bonds_for(w))
+        off = network.layer_offsets(params)
+        ref = solvers.block_solve(estimators.qgt_blocks(O, off), estimators.force(O, el), off, w.lam)
+        assert np.linalg.norm(d.cpu().numpy() - ref) / np.linalg.norm(ref) < 1e-9
+
+
+def test_block_qgt_i8_acc():
+    """sr_block_qgt_i8_acc adds the Gram of its rows to S: two row halves summed equal the
+    whole (to FP64 rounding), and N_s = 0 leaves S unchanged."""
+    import paper_2510_08430_b200 as sr
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device=dev).manual_seed(3)
+    A = torch.complex(torch.randn(900, 300, dtype=torch.float64, device=dev, generator=g),
+                      torch.randn(900, 300, dtype=torch.float64, device=dev, generator=g))
+    offs = [0, 100, 300]
+    n_s = 100 * 100 + 200 * 200
+    S1 = torch.empty(n_s, dtype=torch.complex128, device=dev)
+    S2 = torch.empty(n_s, dtype=torch.complex128, device=dev)
+    sr.sr_block_qgt_i8(A, offs, S1)
+    sr.sr_block_qgt_i8(A[:400], offs, S2)
+    sr.sr_block_qgt_i8_acc(A[400:], offs, S2)
+    before = S2.clone()
+    sr.sr_block_qgt_i8_acc(A[:0], offs, S2)
+    assert torch.equal(S2, before)
+    assert _rel(S2, S1) < 1e-14
