@@ -513,7 +513,7 @@ sr_status local_energy_impl(const NetDesc& net, const double* theta_d, long long
   // slower at configs[1]/[2]); SR_ENERGY_RB overrides for tuning.  Forcing 5-6 CTAs per SM
   // (SR_ENERGY_MINB) costs registers and spills: slower (272 / 355 ms at configs[3]).
   int rb = 16;
-  if (const char* e = getenv("SR_ENERGY_RB")) rb = atoi(e) == 32 ? 32 : atoi(e) == 8 ? 8 : 16;
+  if (const char* e = getenv("SR_ENERGY_RB")) rb = atoi(e) == 32 ? 32 : atoi(e) == 24 ? 24 : atoi(e) == 8 ? 8 : 16;
   const size_t sm = tile_smem(net, rb);
   const long long max_tiles = (ns * nb + rb - 1) / rb;
   const double2* lp = reinterpret_cast<const double2*>(log_psi);
@@ -529,6 +529,11 @@ sr_status local_energy_impl(const NetDesc& net, const double* theta_d, long long
     SR_TRY(set_smem(energy_eval<32>, sm));
     const unsigned grid = grid_of(energy_eval<32>);
     energy_eval<32><<<grid, kThreads, sm, st>>>(net, theta, w.wt, spins, bij, bond_j, w.z0, lp, w.off, ns, w.rows,
+                                                w.contrib);
+  } else if (rb == 24) {
+    SR_TRY(set_smem(energy_eval<24>, sm));
+    const unsigned grid = grid_of(energy_eval<24>);
+    energy_eval<24><<<grid, kThreads, sm, st>>>(net, theta, w.wt, spins, bij, bond_j, w.z0, lp, w.off, ns, w.rows,
                                                 w.contrib);
   } else if (rb == 16) {
     SR_TRY(set_smem(energy_eval<16>, sm));
