@@ -750,7 +750,9 @@ class ShardedStep:
             others = [n * n for b, n in enumerate(self.sizes) if not olo <= b < ohi]
             self.staging = [torch.empty(max(others), dtype=c, device=self.device)
                             for _ in range(min(2, len(others)))] if others else []
-        self.ops = ops or CudaOps(widths, hi - lo, len(bj), self.device, gram_engine, solve_offsets=self.own_offs)
+        # a rank that owns no block needs no factor storage (a one-column placeholder partition)
+        self.ops = ops or CudaOps(widths, hi - lo, len(bj), self.device, gram_engine,
+                                  solve_offsets=self.own_offs if self.own_offs else [0, 1])
         self.moments = torch.empty(2 * self.buf.n_p + 2, dtype=torch.complex128, device=self.device)
         self.moments_all = torch.empty(world, 2 * self.buf.n_p + 2, dtype=torch.complex128, device=self.device)
         self.owned = list(range(olo, ohi))
