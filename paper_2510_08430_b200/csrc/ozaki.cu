@@ -21,8 +21,11 @@
 //
 // Kernels: oz_colmax (column maxima), oz_split (digits, transposed to K-major int8 rows
 // [slice][column][Re A | Im A | -Re A]), gram_i8 (persistent, warp-specialised: one TMA
-// producer lane, one MMA-issuing lane, four epilogue warps; 128 x 64 tiles of the
-// lower triangle, 28 tcgen05.mma per 32-byte K step into 7 TMEM accumulators).
+// producer lane, one MMA-issuing lane, eight epilogue warps; 128 x 64 tiles of the lower
+// triangle, the 28 digit-slice products of a 32-byte K step as 10 tcgen05.mma of N = 64 k into
+// 7 TMEM accumulators), launched once per K' <= 16384 range (launch_herm: the launches add
+// their FP64 partials to S in a fixed order, which keeps the concurrently running tiles'
+// operand streams inside L2).
 #include <cuda.h>
 
 #include <algorithm>
