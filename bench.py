@@ -491,10 +491,26 @@ def compare_solves(sr, torch, step, w, dev):
         out_d["full_qgt_cg"] = x
         cg_info.update(iterations=it, rel_residual=res)
 
+    def full_dist(ws):
+        from paper_2510_08430_b200 import parallel
+
+        class _One(parallel.SelfComm):     # the distributed dense path as one rank
+            def reduce(self, t, dst, async_op=False):
+                return parallel._Done()
+
+            def broadcast(self, t, src):
+                pass
+
+            def all_gather(self, out, t):
+                out[0].copy_(t)
+        out_d["full_qgt_dist"] = parallel.dist_full_qgt(step.ops, _One(), 0, 1, b.O, b.F, w.lam)
+
     calls = {"block_qgt+block_solve": block_call,
              "full_qgt_solve": lambda ws: sr.sr_full_qgt_solve(b.O, b.F, w.lam, out_d["full_qgt_solve"], workspace=ws),
              "full_qgt_cg": full_cg,
              "ntk_solve": lambda ws: sr.sr_ntk_solve(b.O, b.e_tilde, w.lam, out_d["ntk_solve"], workspace=ws)}
+    if b.n_p <= 40000:   # the formed-and-factorised distributed path, as one rank (configs[3]: 72 s, not timed here)
+        calls["full_qgt_dist"] = full_dist
     need = {"full_qgt_solve": lib.sr_full_qgt_solve_workspace_bytes(ns, b.n_p) + 16 * b.n_p,
             "ntk_solve": lib.sr_ntk_solve_workspace_bytes(ns, b.n_p) + 16 * b.n_p}
     ms, skipped = {}, {}
@@ -527,6 +543,9 @@ def compare_solves(sr, torch, step, w, dev):
     ref = next((k for k in ("full_qgt_solve", "full_qgt_cg", "ntk_solve") if k in ms), None)
     if "full_qgt_solve" in ms and "ntk_solve" in ms:
         out["rel_l2_full_vs_ntk"] = nrm(out_d["full_qgt_solve"] - out_d["ntk_solve"]) / nrm(out_d["full_qgt_solve"])
+    if "full_qgt_dist" in ms and "full_qgt_solve" in ms:
+        out["rel_l2_full_dist_vs_full"] = (nrm(out_d["full_qgt_dist"] - out_d["full_qgt_solve"])
+                                           / nrm(out_d["full_qgt_solve"]))
     if "full_qgt_cg" in ms and "ntk_solve" in ms:
         out["rel_l2_full_cg_vs_ntk"] = nrm(out_d["full_qgt_cg"] - out_d["ntk_solve"]) / nrm(out_d["ntk_solve"])
     if cg_info:

@@ -519,7 +519,9 @@ def test_bench_native_json_contract():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["config"]["workload"] == "heis_chain_N40" and d["n_gpus"] == 1
     assert d["fp64_engine"]["gram_frac_of_dmma_peak"] > 0.5
-    assert set(d["comparison_solves"]["ms"]) == {"block_qgt+block_solve", "full_qgt_solve", "full_qgt_cg", "ntk_solve"}
+    assert set(d["comparison_solves"]["ms"]) == {"block_qgt+block_solve", "full_qgt_solve", "full_qgt_cg", "ntk_solve",
+                                                 "full_qgt_dist"}
+    assert d["comparison_solves"]["rel_l2_full_dist_vs_full"] < 1e-9
     assert d["comparison_solves"]["rel_l2_full_vs_ntk"] < 1e-9
 
 
