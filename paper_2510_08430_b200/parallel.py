@@ -734,6 +734,8 @@ class ShardedStep:
         self.per_block_gram = world > 1 if per_block_gram is None else per_block_gram
         self.group = group
         self.n_total = spins_all.shape[0]
+        if self.n_total < world:
+            raise ValueError(f"{self.n_total} samples cannot be sharded over {world} ranks (one sample per rank at least)")
         lo, hi = shard_range(self.n_total, rank, world)
         self.device = torch.device(device)
         # per-block launches keep only the owned blocks of S plus one or two staging buffers

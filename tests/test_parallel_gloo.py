@@ -255,3 +255,39 @@ def test_dist_full_qgt_o1_conditioned(world, nb):
     outs = parallel.run_loopback(world, make, work)
     for x in outs:
         assert np.linalg.norm(x - ref) / np.linalg.norm(ref) < 1e-10
+
+
+def test_loopback_ragged_tiny_shards_all_paths():
+    """5 samples over 4 ranks (shards of 2, 1, 1, 1): the block step and every comparison path
+    (dense reduce-to-rank-0, ring NTK, CG, distributed dense with ragged panels) against the
+    oracle; fewer samples than ranks is rejected."""
+    from paper_2510_08430_b200 import parallel
+    import paper_2510_08430_b200 as sr
+    w = workloads.CONFIGS[0].with_samples(5)
+    spins, params = workloads.make_inputs(w)
+    ij, jj = sr.lattice.for_workload(w)
+    theta = torch.from_numpy(sr.model.pack(params))
+
+    def make(r, comm, lock):
+        return parallel.ShardedStep(w.widths, spins, ij, jj, w.lam, r, 4, "cpu", comm=comm,
+                                    ops=parallel.locked(OracleOps(), lock))
+
+    def work(r, step):
+        d, _ = step.run(theta)
+        out = [d.clone(), step.full_qgt_solve(method="dense").clone(), step.ntk_solve().clone(),
+               step.full_qgt_solve(method="cg").clone()]
+        step.dist_nb = 100
+        return out + [step.full_qgt_solve(method="dist").clone()]
+
+    outs = parallel.run_loopback(4, make, work)
+    O = network.jacobian(params, spins)
+    e = hamiltonian.local_energies(params, spins, hamiltonian.bonds_for(w))
+    off = network.layer_offsets(params)
+    ref = solvers.block_solve(estimators.qgt_blocks(O, off), estimators.force(O, e), off, w.lam)
+    full = solvers.full_solve(estimators.qgt_full(O), estimators.force(O, e), w.lam)
+    got = [x.numpy() for x in outs[0]]
+    assert np.linalg.norm(got[0] - ref) / np.linalg.norm(ref) < 1e-10
+    for x in got[1:]:
+        assert np.linalg.norm(x - full) / np.linalg.norm(full) < 1e-10
+    with pytest.raises(ValueError):
+        parallel.ShardedStep(w.widths, spins[:3], ij, jj, w.lam, 0, 4, "cpu", ops=OracleOps())
