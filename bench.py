@@ -122,6 +122,14 @@ class ClockSampler:
                 if len(parts) >= 8:
                     rows.append(parts)
         os.unlink(self.path)
+        if not rows:   # a timed region shorter than the sampling interval: one query now
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20)
+                rows = [[p.strip() for p in line.split(",")] for line in out.stdout.splitlines()
+                        if len(line.split(",")) >= 8]
+            except (OSError, subprocess.SubprocessError):
+                rows = []
         if not rows:
             return None
         sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
