@@ -69,6 +69,11 @@ constexpr uint32_t kACol = kSlices * BN;  // TMEM columns [448, 504): the A digi
 #ifndef SR_OZ_PF
 #define SR_OZ_PF 0   // > 0: the producer prefetches the boxes of stage kk + SR_OZ_PF into L2
 #endif
+#ifndef SR_OZ_SPLITBAR
+#define SR_OZ_SPLITBAR 0   // 1: per-slice TMA boxes completing on three barriers per stage, so the
+                           // first MMAs of a stage start once A0 and B0-3 have arrived
+#endif
+constexpr bool kSplitBar = SR_OZ_SPLITBAR;
 constexpr int kBand = SR_OZ_BAND;         // row panels per rasterisation band
 constexpr int kNonFinite = 1 << 20;       // column exponent marking a column with Inf / NaN
 constexpr int kMaxBlk = 24;
@@ -254,12 +259,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
   const uint32_t tfull = smem_u32(bars + 2 * kStages), tempty = smem_u32(bars + 2 * kStages + 1);
+  // split barriers (kSplitBar): fullB = B slices 4-6, fullC = A slices 1-6 (full0 = A0 + B0-3)
+  const uint32_t fullB0 = smem_u32(bars + 2 * kStages + 4), fullC0 = smem_u32(bars + 3 * kStages + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; s++) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
+      if (kSplitBar) {
+        mbar_init(fullB0 + 8 * s, 1);
+        mbar_init(fullC0 + 8 * s, 1);
+      }
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, kEpiWarps);
@@ -290,6 +301,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kB = pass ? (int)P.Kp : 0;
         for (int kk = 0; kk < P.kstages; kk++) {
           mbar_wait(empty0 + 8 * s, ph ^ 1);
+          if (kSplitBar) {   // per-slice boxes (maps of one slice per box), three barriers
+            const uint32_t sa = smem_base + s * kStageBytes, sbq = sa + kAStage;
+            const int kc = (int)(P.kbase + kk) * BKB;
+            mbar_expect_tx(full0 + 8 * s, kASlice + 4 * kBSlice);
+            mbar_expect_tx(fullB0 + 8 * s, 3 * kBSlice);
+            mbar_expect_tx(fullC0 + 8 * s, (kSlices - 1) * kASlice);
+            tma_load_3d(sa, &tm_a, kc, rowA, 0, full0 + 8 * s);
+#pragma unroll
+            for (int q = 0; q < 4; q++) tma_load_3d(sbq + q * kBSlice, &tm_b, kB + kc, rowB, q, full0 + 8 * s);
+#pragma unroll
+            for (int q = 4; q < kSlices; q++) tma_load_3d(sbq + q * kBSlice, &tm_b, kB + kc, rowB, q, fullB0 + 8 * s);
+#pragma unroll
+            for (int p = 1; p < kSlices; p++) tma_load_3d(sa + p * kASlice, &tm_a, kc, rowA, p, fullC0 + 8 * s);
+            if (++s == kStages) {
+              s = 0;
+              ph ^= 1;
+            }
+            continue;
+          }
           constexpr int kRep = (SR_OZ_EXP == 5 || SR_OZ_EXP == 6) ? 2 : 1;
           mbar_expect_tx(full0 + 8 * s, kRep * kStageBytes);
           const uint32_t sa = smem_base + s * kStageBytes;
@@ -322,6 +352,40 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(tempty, acc_ph ^ 1);
             acc_ph ^= 1;
             tc_fence_after();
+          }
+          if (kSplitBar && MODE >= 0) {
+            const uint32_t sa = smem_base + s * kStageBytes, sb = sa + kAStage;
+            mbar_wait(full0 + 8 * s, ph);   // A0, B0-3: (p = 0, q = 0..3)
+            tc_fence_after();
+#pragma unroll
+            for (int ks = 0; ks < BKB / 32; ks++)
+              mma_i8(tmem, sdesc(sa + ks * 32), sdesc(sb + ks * 32), (kin > 0 || ks > 0) ? 1u : 0u, idesc_n(4 * BN));
+            mbar_wait(fullB0 + 8 * s, ph);  // B4-6: (p = 0, q = 4..6)
+            tc_fence_after();
+#pragma unroll
+            for (int ks = 0; ks < BKB / 32; ks++)
+              mma_i8(tmem + (uint32_t)(4 * BN), sdesc(sa + ks * 32), sdesc(sb + 4 * kBSlice + ks * 32),
+                     (kin > 0 || ks > 0) ? 1u : 0u, idesc_n(3 * BN));
+            mbar_wait(fullC0 + 8 * s, ph);  // A1-6: p >= 1
+            tc_fence_after();
+#pragma unroll
+            for (int ks = 0; ks < BKB / 32; ks++)
+#pragma unroll
+              for (int p = 1; p < kSlices; p++) {
+                const uint64_t ad = sdesc(sa + p * kASlice + ks * 32);
+#pragma unroll
+                for (int q = 0; q + p < kSlices; q += 4) {
+                  const int nq = (kSlices - p - q) < 4 ? (kSlices - p - q) : 4;
+                  mma_i8(tmem + (uint32_t)((p + q) * BN), ad, sdesc(sb + q * kBSlice + ks * 32), 1u, idesc_n(BN * nq));
+                }
+              }
+            tc_commit(empty0 + 8 * s);
+            if (kin == P.spc - 1 || kk == P.kstages - 1) tc_commit(tfull);
+            if (++s == kStages) {
+              s = 0;
+              ph ^= 1;
+            }
+            continue;
           }
           mbar_wait(full0 + 8 * s, ph);
           tc_fence_after();
@@ -1124,7 +1188,7 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
     }
     P.total_tiles = tiles;
     CUtensorMap ma, mb2;
-    SR_TRY(make_map(ma, E, Kp, nc, BM));
+    SR_TRY(make_map(ma, E, Kp, nc, BM, kSplitBar && !gram_pairs() ? 1 : kSlices));
     if (pair) {
       CUtensorMap mbb2, mbb1, mbh;
       SR_TRY(make_map(mbb2, E, Kp, nc, BN, 2));
@@ -1143,7 +1207,7 @@ sr_status block_qgt_i8(long long ns, int nblk, const int64_t* offs, const double
         SR_LAUNCHED();
       }
     } else {
-      SR_TRY(make_map(mb2, E, Kp, nc, BN));
+      SR_TRY(make_map(mb2, E, Kp, nc, BN, kSplitBar ? 1 : kSlices));
       SR_TRY(launch_herm(ma, mb2, P, 2 * Kp / BKB, st, accumulate));
     }
   }
@@ -1200,8 +1264,8 @@ sr_status trail_apply_i8(long long m, long long K, double2* C, long long ldc, vo
   B.tile_begin = 0;
   P.total_tiles = 2 * lower_tiles(B.n, jlim);
   CUtensorMap ma, mb;
-  SR_TRY(make_map(ma, E, Kp, m, BM));
-  SR_TRY(make_map(mb, E, Kp, m, BN));
+  SR_TRY(make_map(ma, E, Kp, m, BM, kSplitBar ? 1 : kSlices));
+  SR_TRY(make_map(mb, E, Kp, m, BN, kSplitBar ? 1 : kSlices));
   const long long want = ctas > 0 ? ctas : ctas < 0 ? (P.total_tiles + (-ctas) - 1) / (-ctas) : kNumSMs;
   const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(P.total_tiles, want));
   timer_begin("trail_i8", st);
@@ -1256,8 +1320,8 @@ sr_status gram_rows_i8(const double2* L, long long ldl, long long m, long long K
   B.tile_begin = 0;
   P.total_tiles = 2 * lower_tiles(B.n);
   CUtensorMap ma, mb;
-  SR_TRY(make_map(ma, E, Kp, m, BM));
-  SR_TRY(make_map(mb, E, Kp, m, BN));
+  SR_TRY(make_map(ma, E, Kp, m, BM, kSplitBar ? 1 : kSlices));
+  SR_TRY(make_map(mb, E, Kp, m, BN, kSplitBar ? 1 : kSlices));
   return launch_herm(ma, mb, P, 2 * Kp / BKB, st);
 }
 
