@@ -359,6 +359,7 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
       const long long m = B.npad - (long long)(p + 1) * NB;
       if (m <= 0) continue;
       gram::ProbSet trsm{}, trsm_rest{}, next_tile{}, next_rows{}, next_rows2{}, inner_rest{};
+      bool ec_now = false;
       double2* panel = B.Fm + (long long)(p + 1) * NB * B.npad + (long long)p * NB;
       const double2* linv_p = B.linv + (long long)p * NB * NB;
       // Split TRSM: the chain solves only the next panel's row block (all that the next-tile
@@ -427,8 +428,13 @@ sr_status solve_block(CholSet& cs, int b, cudaStream_t st, const BlockStreams& Q
         timer_end(Q.s3);
         SR_CUDA(cudaEventRecord(Q.ec, Q.s3));
         ec_rec = true;
+        ec_now = true;
       }
       if (inner_rest.count) {
+        // SR_S2_AFTER_S3=1: the left-looking job (needed two panels later) starts only after
+        // this step's s3 jobs (needed by the next TRSM), so it does not take their SMs
+        static const bool s2_after_s3 = env_int("SR_S2_AFTER_S3", 0) != 0;
+        if (s2_after_s3 && ec_now) SR_CUDA(cudaStreamWaitEvent(Q.s2, Q.ec, 0));
         if (left) SR_CUDA(cudaStreamWaitEvent(Q.s2, split ? Q.er : Q.ea, 0));
         else SR_CUDA(cudaStreamWaitEvent(Q.s2, side_go, 0));
         if (split && !left) SR_CUDA(cudaStreamWaitEvent(Q.s2, Q.er, 0));
