@@ -258,8 +258,9 @@ SR_API sr_status sr_block_solve(int n_blocks, const int64_t* block_offsets /*hos
  * for b = 0, 1, ...: S_b = A_b^H A_b (Eq. 3) is formed straight into block b's
  * padded Cholesky matrix on the selected Gram engine and (S_b + lambda I) dtheta_b = -F_b is
  * solved (§2, "Each block S_l is inverted independently") before block b+1's Gram.
- * Same result as sr_block_qgt followed by sr_block_solve (same kernels, same order of every
- * sum), but the workspace holds ONE block -- the largest -- instead of every S_b and its
+ * Same result as sr_block_qgt followed by sr_block_solve up to the FP64 summation order of
+ * the Cholesky updates (a block solved alone uses the single-block lookahead; measured within
+ * 1e-12 relative), but the workspace holds ONE block -- the largest -- instead of every S_b and its
  * factor copy: configs[4]'s eight blocks need 10.6 GB + digit slices instead of 157 GB.
  * Blocks run one after another (no S_b is kept; nothing to inspect).
  *   A        complex [n_samples][lda], the centred, weighted Jacobian (stage 3 output)
