@@ -363,6 +363,26 @@ SR_API sr_status sr_gram_tn(int64_t m, int64_t n, int64_t k, const double* A, in
                             int64_t ldb, double* C, int64_t ldc, void* stream);
 SR_API sr_status sr_gram_nh_sub(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
                                 int64_t ldb, double* C, int64_t ldc, void* stream);
+/* The same panels on the int8 digit-slice engine (exact to FP64 level, as sr_block_qgt_i8):
+ *   sr_cols_i8_prepare  splits all n_cols columns of A (n_samples x n_cols, lda) into the
+ *                       workspace (sr_cols_i8_workspace_bytes: 21 bytes per sample and column);
+ *   sr_cols_i8_gram     C (m x n, ldc) = (or += with accumulate != 0) A[:, row0:row0+m]^H A[:, 0:n]
+ *                       on the prepared workspace (row0 + m <= n_cols, n <= n_cols);
+ *   sr_rows_i8_prepare  splits the rows of L (rows x K row-major, K <= 8192) into the workspace
+ *                       (sr_rows_i8_sub_workspace_bytes);
+ *   sr_rows_i8_sub      C (m x n, ldc) -= L[row0:row0+m] L[0:n]^H on the prepared workspace:
+ *                       the trailing update of a rank's panel row by the broadcast panel column
+ *                       (the Cholesky trailing-update kernel, gram_i8<MODE_SUB>, on a rectangle). */
+SR_API size_t sr_cols_i8_workspace_bytes(int64_t n_samples, int64_t n_cols);
+SR_API sr_status sr_cols_i8_prepare(int64_t n_samples, int64_t n_cols, const double* A, int64_t lda, void* workspace,
+                                    size_t workspace_bytes, void* stream);
+SR_API sr_status sr_cols_i8_gram(int64_t n_samples, int64_t n_cols, int64_t row0, int64_t m, int64_t n, double* C,
+                                 int64_t ldc, int accumulate, void* workspace, size_t workspace_bytes, void* stream);
+SR_API size_t sr_rows_i8_sub_workspace_bytes(int64_t rows, int64_t K);
+SR_API sr_status sr_rows_i8_prepare(int64_t rows, int64_t K, const double* L, int64_t ldl, void* workspace,
+                                    size_t workspace_bytes, void* stream);
+SR_API sr_status sr_rows_i8_sub(int64_t rows, int64_t K, int64_t row0, int64_t m, int64_t n, double* C, int64_t ldc,
+                                void* workspace, size_t workspace_bytes, void* stream);
 SR_API size_t sr_chol_inv_workspace_bytes(int64_t n);
 SR_API sr_status sr_chol_inv(int64_t n, const double* M, double lambda, double* L, int64_t ldl, double* Linv,
                              int64_t ldv, int32_t* info, void* workspace, size_t workspace_bytes, void* stream);

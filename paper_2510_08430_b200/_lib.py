@@ -45,6 +45,12 @@ SIGNATURES = {
     "sr_cg_xpby": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp]),
     "sr_gram_tn": (_i32, [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
     "sr_gram_nh_sub": (_i32, [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
+    "sr_cols_i8_workspace_bytes": (_sz, [_i64, _i64]),
+    "sr_cols_i8_prepare": (_i32, [_i64, _i64, _vp, _i64, _vp, _sz, _vp]),
+    "sr_cols_i8_gram": (_i32, [_i64, _i64, _i64, _i64, _i64, _vp, _i64, _i32, _vp, _sz, _vp]),
+    "sr_rows_i8_sub_workspace_bytes": (_sz, [_i64, _i64]),
+    "sr_rows_i8_prepare": (_i32, [_i64, _i64, _vp, _i64, _vp, _sz, _vp]),
+    "sr_rows_i8_sub": (_i32, [_i64, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _sz, _vp]),
     "sr_chol_inv_workspace_bytes": (_sz, [_i64]),
     "sr_chol_inv": (_i32, [_i64, _vp, _dbl, _vp, _i64, _vp, _i64, _vp, _vp, _sz, _vp]),
     "sr_graph_capture_begin": (_i32, [C.c_void_p]),
@@ -395,6 +401,44 @@ def sr_gram_nh_sub(A, B, C_out):
         raise SRError("sr_gram_nh_sub: shape mismatch")
     _check(load().sr_gram_nh_sub(A.shape[0], B.shape[0], A.shape[1], _ptr(A), lda, _ptr(B), ldb, _ptr(C_out), ldc,
                                  _stream(A.device)), "sr_gram_nh_sub")
+
+
+class ColSlices:
+    """Digit slices of all columns of A on the int8 engine (sr_cols_i8_prepare), for
+    rectangles of its Gram: C (+)= A[:, row0:row0+m]^H A[:, 0:n] (sr_cols_i8_gram)."""
+
+    def __init__(self, A):
+        lib = load()
+        self.ns, self.ncols = A.shape
+        lda = _cols(A, "A")
+        self.ws = _workspace(lib.sr_cols_i8_workspace_bytes(self.ns, self.ncols), A.device, None)
+        self.dev = A.device
+        _check(lib.sr_cols_i8_prepare(self.ns, self.ncols, _ptr(A), lda, *_ws_args(self.ws), _stream(A.device)),
+               "sr_cols_i8_prepare")
+
+    def gram(self, row0, C_out, accumulate=False):
+        m, n = C_out.shape
+        _check(load().sr_cols_i8_gram(self.ns, self.ncols, int(row0), m, n, _ptr(C_out), _cols(C_out, "C"),
+                                      1 if accumulate else 0, *_ws_args(self.ws), _stream(self.dev)), "sr_cols_i8_gram")
+
+
+class RowSlices:
+    """Digit slices of the rows of L (rows x K <= 8192, sr_rows_i8_prepare), for rectangular
+    trailing updates C -= L[row0:row0+m] L[0:n]^H (sr_rows_i8_sub)."""
+
+    def __init__(self, L, workspace=None):
+        lib = load()
+        self.rows, self.K = L.shape
+        ldl = _cols(L, "L")
+        self.ws = _workspace(lib.sr_rows_i8_sub_workspace_bytes(self.rows, self.K), L.device, workspace)
+        self.dev = L.device
+        _check(lib.sr_rows_i8_prepare(self.rows, self.K, _ptr(L), ldl, *_ws_args(self.ws), _stream(L.device)),
+               "sr_rows_i8_prepare")
+
+    def sub(self, row0, C_out):
+        m, n = C_out.shape
+        _check(load().sr_rows_i8_sub(self.rows, self.K, int(row0), m, n, _ptr(C_out), _cols(C_out, "C"),
+                                     *_ws_args(self.ws), _stream(self.dev)), "sr_rows_i8_sub")
 
 
 def sr_chol_inv(M, lam, L_out, Linv_out, info=None, workspace=None):

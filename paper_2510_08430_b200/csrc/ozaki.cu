@@ -94,6 +94,9 @@ struct Blk {
   long long tile_begin;  // first global tile index (tiles come in Re/Im pairs)
   int n, RT, CT;
   int jlim;              // > 0: only column tiles J < jlim (a lower trapezoid, row-major); 0: all
+  int rect;              // 1: a full m x n rectangle C = X^H Y (rows of X from row0), no mirror
+  int m;                 // rect: rows of C
+  long long row0;        // rect: first A-operand row (slice-matrix row) relative to col0
 };
 // Epilogues: MODE_HERM writes S = G with its conjugate mirror (stage 4); MODE_SUB applies
 // C -= G to the lower triangle i >= j (Cholesky trailing update, chol.cu).
@@ -204,6 +207,11 @@ __device__ __forceinline__ void decode(const Params& P, long long t, int& b, int
   pass = (int)(u & 1);
   u >>= 1;
   const int RT = P.b[b].RT, CT = P.b[b].CT;
+  if (P.b[b].rect) {   // rectangle: column-major (the tiles of one column panel share its B operand)
+    I = (int)(u % RT);
+    J = (int)(u / RT);
+    return;
+  }
   if (P.b[b].jlim > 0) {   // trapezoid: row I holds min(CT, 2I + 2, jlim) tiles
     const int jl = min(CT, P.b[b].jlim);
     for (int i = 0; i < RT; i++) {
@@ -296,7 +304,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (long long t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
         int b, I, J, pass;
         decode(P, t, b, I, J, pass);
-        const int rowA = SR_OZ_EXP == 3 ? (int)P.b[b].col0 : (int)(P.b[b].col0 + (long long)I * BM);
+        const int rowA = SR_OZ_EXP == 3 ? (int)P.b[b].col0
+                                         : (int)(P.b[b].col0 + (P.b[b].rect ? P.b[b].row0 : 0) + (long long)I * BM);
         const int rowB = SR_OZ_EXP == 3 ? (int)P.b[b].col0 : (int)(P.b[b].col0 + (long long)J * BN);
         const int kB = pass ? (int)P.Kp : 0;
         for (int kk = 0; kk < P.kstages; kk++) {
@@ -452,8 +461,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Blk& B = P.b[b];
       const int n = B.n;
       const int i = I * BM + rl;
-      const bool row_ok = i < n;
-      const int ei = row_ok ? P.expo[B.col0 + i] : 0;
+      const bool row_ok = i < (B.rect ? B.m : n);
+      const int ei = row_ok ? P.expo[B.col0 + (B.rect ? B.row0 : 0) + i] : 0;
       double* Cb = reinterpret_cast<double*>(B.C);
       const long long ldc = B.ldc;
       for (int ch = 0; ch < nchunks; ch++, c++) {
@@ -499,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int e = 0; e < BN / 2; e++, mp += mstep) {
           const int ej = __shfl_sync(0xffffffffu, ej_lane, e);
           const int j = jb + e;
-          if (!row_ok || j >= n || j > i) continue;
+          if (!row_ok || j >= n || (!B.rect && j > i)) continue;
           // a non-finite input column poisons its row and column of the result, as in FP64
           const double val = (ei == kNonFinite || ej == kNonFinite) ? __longlong_as_double(0x7FF8000000000000LL)
                                                                      : pow2_scale(vals[e], ei + ej - 60);
@@ -508,6 +517,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             // (red.global.add.f64): each element receives exactly one addend per launch
             // (Re pass -> .x, Im pass -> .y), so the result is deterministic.
             atomicAdd(dp + 2 * e, -val);
+            continue;
+          }
+          if (B.rect) {   // rectangle: store or accumulate, no mirror, no diagonal special case
+            double acc = val;
+            if (ch > 0 || P.acc_in) acc += dp[2 * e];
+            dp[2 * e] = acc;
             continue;
           }
           if (nchunks == 1 && !P.acc_in && !P.defer) {
@@ -1323,6 +1338,123 @@ sr_status gram_rows_i8(const double2* L, long long ldl, long long m, long long K
   SR_TRY(make_map(ma, E, Kp, m, BM, kSplitBar ? 1 : kSlices));
   SR_TRY(make_map(mb, E, Kp, m, BN, kSplitBar ? 1 : kSlices));
   return launch_herm(ma, mb, P, 2 * Kp / BKB, st);
+}
+
+// ---------------------------------------------------------------- rectangles
+// The distributed dense full QGT (parallel.dist_full_qgt) needs rectangles of the Gram,
+// C = A[:, row0:row0+m]^H A[:, 0:n] (a panel row of S), and rectangular trailing updates,
+// C -= L[row0:row0+m] L[0:n]^H (a rank's panel row against the broadcast panel column).  Both
+// are the same engine with one "rect" block: the tile grid is the full m x n rectangle
+// (column-major), the A operand starts at row0 of the slice matrix, and the epilogue writes
+// (or adds, or subtracts) every element, with no conjugate mirror.
+
+size_t cols_workspace_bytes(long long ns, long long ncols) {
+  const long long Kp = pad_k(ns);
+  return round256(slice_bytes(Kp, ncols)) + round256((size_t)ncols * 8) + round256((size_t)ncols * 4);
+}
+
+sr_status cols_prepare(const double2* A, long long lda, long long ns, long long ncols, void* ws, size_t ws_bytes,
+                       cudaStream_t st) {
+  if (ws_bytes < cols_workspace_bytes(ns, ncols) || !ws) {
+    set_error("cols_prepare: workspace too small");
+    return SR_ERR_WORKSPACE;
+  }
+  SR_TRY(set_attrs());
+  const long long Kp = pad_k(ns);
+  Arena a(ws, ws_bytes);
+  int8_t* E = a.take<int8_t>(slice_bytes(Kp, ncols));
+  unsigned long long* mx = a.take<unsigned long long>(ncols);
+  int* expo = a.take<int>(ncols);
+  SR_CUDA(cudaMemsetAsync(mx, 0, (size_t)ncols * 8, st));
+  const int rows_per = 256;
+  dim3 g1((unsigned)((ncols + 255) / 256), (unsigned)((ns + rows_per - 1) / rows_per));
+  oz_colmax<<<g1, 256, 0, st>>>(A, lda, 0, (int)ncols, ns, rows_per, mx);
+  SR_LAUNCHED();
+  dim3 g2((unsigned)((ncols + 31) / 32), (unsigned)(Kp / 64));
+  oz_split<<<g2, 256, kSplitSmem, st>>>(A, lda, 0, (int)ncols, ns, Kp, mx, E, expo);
+  SR_LAUNCHED();
+  return SR_OK;
+}
+
+sr_status cols_rect_gram(long long ns, long long ncols, void* ws, size_t ws_bytes, long long row0, long long m,
+                         long long n, double2* C, long long ldc, bool accumulate, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return SR_OK;
+  if (row0 < 0 || row0 + m > ncols || n > ncols || ws_bytes < cols_workspace_bytes(ns, ncols) || !ws) {
+    set_error("cols_rect_gram: bad range or workspace");
+    return SR_ERR_INVALID;
+  }
+  if (ns == 0) {
+    if (!accumulate) SR_CUDA(cudaMemset2DAsync(C, ldc * sizeof(double2), 0, n * sizeof(double2), m, st));
+    return SR_OK;
+  }
+  SR_TRY(set_attrs());
+  const long long Kp = pad_k(ns);
+  Arena a(ws, ws_bytes);
+  int8_t* E = a.take<int8_t>(slice_bytes(Kp, ncols));
+  a.take<unsigned long long>(ncols);
+  int* expo = a.take<int>(ncols);
+  Params P{};
+  P.nblk = 1;
+  P.Kp = Kp;
+  P.spc = kChunkK / BKB;
+  P.expo = expo;
+  Blk& B = P.b[0];
+  B.col0 = 0;
+  B.rect = 1;
+  B.row0 = row0;
+  B.m = (int)m;
+  B.n = (int)n;
+  B.C = C;
+  B.ldc = ldc;
+  B.RT = (int)((m + BM - 1) / BM);
+  B.CT = (int)((n + BN - 1) / BN);
+  B.tile_begin = 0;
+  P.total_tiles = 2LL * B.RT * B.CT;
+  CUtensorMap ma, mb;
+  SR_TRY(make_map(ma, E, Kp, ncols, BM, kSplitBar ? 1 : kSlices));
+  SR_TRY(make_map(mb, E, Kp, ncols, BN, kSplitBar ? 1 : kSlices));
+  return launch_herm(ma, mb, P, 2 * Kp / BKB, st, accumulate);
+}
+
+sr_status rows_rect_sub(long long rows, long long K, long long row0, long long m, long long n, double2* C,
+                        long long ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (m <= 0 || n <= 0 || K <= 0) return SR_OK;
+  if (row0 < 0 || row0 + m > rows || n > rows || ws_bytes < trail_workspace_bytes(rows, K) || !ws) {
+    set_error("rows_rect_sub: bad range or workspace");
+    return SR_ERR_INVALID;
+  }
+  SR_TRY(set_attrs());
+  const long long Kp = pad_k(K);
+  Arena a(ws, trail_workspace_bytes(rows, K));
+  int8_t* E = a.take<int8_t>((size_t)kSlices * 3 * Kp * rows);
+  int* expo = a.take<int>(rows);
+  Params P{};
+  P.nblk = 1;
+  P.Kp = Kp;
+  P.kstages = (int)(2 * Kp / BKB);
+  P.spc = kChunkK / BKB;
+  P.expo = expo;
+  Blk& B = P.b[0];
+  B.col0 = 0;
+  B.rect = 1;
+  B.row0 = row0;
+  B.m = (int)m;
+  B.n = (int)n;
+  B.C = C;
+  B.ldc = ldc;
+  B.RT = (int)((m + BM - 1) / BM);
+  B.CT = (int)((n + BN - 1) / BN);
+  B.tile_begin = 0;
+  P.total_tiles = 2LL * B.RT * B.CT;
+  CUtensorMap ma, mb;
+  SR_TRY(make_map(ma, E, Kp, rows, BM, kSplitBar ? 1 : kSlices));
+  SR_TRY(make_map(mb, E, Kp, rows, BN, kSplitBar ? 1 : kSlices));
+  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(P.total_tiles, kNumSMs));
+  timer_begin("trail_i8", st);
+  gram_i8<MODE_SUB><<<grid, kThreads, kSmem, st>>>(ma, mb, P);
+  timer_end(st);
+  SR_LAUNCHED();
+  return SR_OK;
 }
 
 }  // namespace oz

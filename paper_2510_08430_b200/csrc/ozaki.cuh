@@ -44,5 +44,17 @@ sr_status trail_split_i8(const double2* L, long long ldl, long long m, long long
 sr_status trail_apply_i8(long long m, long long K, double2* C, long long ldc, void* ws, long long r0, int jlim,
                          long long ctas, cudaStream_t st);
 
+// Rectangles of the same engine (the distributed dense full QGT): cols_prepare splits all
+// ncols columns of A once; cols_rect_gram then forms C (m x n) (+)= A[:, row0:row0+m]^H A[:, 0:n];
+// rows_rect_sub applies C -= L[row0:row0+m] L[0:n]^H for the rows of L (rows x K, K <= 8192)
+// split by trail_split_i8 into the same workspace.
+size_t cols_workspace_bytes(long long ns, long long ncols);
+sr_status cols_prepare(const double2* A, long long lda, long long ns, long long ncols, void* ws, size_t ws_bytes,
+                       cudaStream_t st);
+sr_status cols_rect_gram(long long ns, long long ncols, void* ws, size_t ws_bytes, long long row0, long long m,
+                         long long n, double2* C, long long ldc, bool accumulate, cudaStream_t st);
+sr_status rows_rect_sub(long long rows, long long K, long long row0, long long m, long long n, double2* C,
+                        long long ldc, void* ws, size_t ws_bytes, cudaStream_t st);
+
 }  // namespace oz
 }  // namespace sr

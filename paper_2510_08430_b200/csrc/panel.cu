@@ -13,6 +13,7 @@
 
 #include "chol.cuh"
 #include "gram.cuh"
+#include "ozaki.cuh"
 
 namespace sr {
 namespace {
@@ -127,6 +128,51 @@ SR_API sr_status sr_gram_nh_sub(int64_t m, int64_t n, int64_t k, const double* A
   gram::add_prob(ps, reinterpret_cast<const double2*>(A), lda, reinterpret_cast<const double2*>(B), ldb,
                  reinterpret_cast<double2*>(C), ldc, (int)m, (int)n, k, false);
   return gram::launch<gram::NH, gram::SUB>(ps, (cudaStream_t)stream);
+}
+
+SR_API size_t sr_cols_i8_workspace_bytes(int64_t n_samples, int64_t n_cols) {
+  if (n_samples < 0 || n_cols < 1) return 0;
+  return oz::cols_workspace_bytes(n_samples, n_cols);
+}
+
+SR_API sr_status sr_cols_i8_prepare(int64_t n_samples, int64_t n_cols, const double* A, int64_t lda, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(n_samples >= 0 && n_cols >= 1 && lda >= n_cols && n_cols < (1LL << 31) / oz::kSlices, "bad sizes");
+  SR_CHECK_ARG(workspace && (A || n_samples == 0), "null pointer");
+  if (n_samples == 0) return SR_OK;
+  return oz::cols_prepare(reinterpret_cast<const double2*>(A), lda, n_samples, n_cols, workspace, workspace_bytes,
+                          (cudaStream_t)stream);
+}
+
+SR_API sr_status sr_cols_i8_gram(int64_t n_samples, int64_t n_cols, int64_t row0, int64_t m, int64_t n, double* C,
+                                 int64_t ldc, int accumulate, void* workspace, size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(n_samples >= 0 && n_cols >= 1 && m >= 0 && n >= 0 && ldc >= n, "bad sizes");
+  SR_CHECK_ARG(row0 >= 0 && row0 + m <= n_cols && n <= n_cols, "rows / columns outside the prepared matrix");
+  SR_CHECK_ARG((C || m == 0 || n == 0) && workspace, "null pointer");
+  return oz::cols_rect_gram(n_samples, n_cols, workspace, workspace_bytes, row0, m, n, reinterpret_cast<double2*>(C),
+                            ldc, accumulate != 0, (cudaStream_t)stream);
+}
+
+SR_API size_t sr_rows_i8_sub_workspace_bytes(int64_t rows, int64_t K) {
+  if (rows < 1 || K < 1) return 0;
+  return oz::trail_workspace_bytes(rows, K);
+}
+
+SR_API sr_status sr_rows_i8_prepare(int64_t rows, int64_t K, const double* L, int64_t ldl, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(rows >= 1 && K >= 1 && K <= 8192 && ldl >= K && rows < (1LL << 31) / oz::kSlices, "bad sizes");
+  SR_CHECK_ARG(L && workspace, "null pointer");
+  return oz::trail_split_i8(reinterpret_cast<const double2*>(L), ldl, rows, K, workspace, workspace_bytes,
+                            (cudaStream_t)stream);
+}
+
+SR_API sr_status sr_rows_i8_sub(int64_t rows, int64_t K, int64_t row0, int64_t m, int64_t n, double* C, int64_t ldc,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+  SR_CHECK_ARG(rows >= 1 && K >= 1 && K <= 8192 && m >= 0 && n >= 0 && ldc >= n, "bad sizes");
+  SR_CHECK_ARG(row0 >= 0 && row0 + m <= rows && n <= rows, "rows outside L");
+  SR_CHECK_ARG((C || m == 0 || n == 0) && workspace, "null pointer");
+  return oz::rows_rect_sub(rows, K, row0, m, n, reinterpret_cast<double2*>(C), ldc, workspace, workspace_bytes,
+                           (cudaStream_t)stream);
 }
 
 SR_API size_t sr_chol_inv_workspace_bytes(int64_t n) { return n < 1 ? 0 : chol_inv_ws(n); }

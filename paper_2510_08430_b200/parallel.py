@@ -126,6 +126,18 @@ class CudaOps:
     def chol_inv(self, M, lam, L, Linv):
         sr.sr_chol_inv(M, lam, L, Linv)
 
+    def cols_prepare(self, A):
+        return sr.ColSlices(A)
+
+    def cols_gram(self, cs, row0, C, accumulate=False):
+        cs.gram(row0, C, accumulate)
+
+    def rows_prepare(self, L):
+        return sr.RowSlices(L)
+
+    def rows_sub(self, rs, row0, C):
+        rs.sub(row0, C)
+
     # matrix-free full-QGT CG (full_qgt_cg)
     def av(self, A, v, alpha, out):
         sr.sr_av(A, v, alpha, out)
@@ -192,7 +204,7 @@ def full_qgt_cg(ops, comm, A, F, lam, tol=1e-12, maxit=500):
     return x, it, res
 
 
-def dist_full_qgt(ops, comm, rank, world, A, F, lam, nb=1024):
+def dist_full_qgt(ops, comm, rank, world, A, F, lam, nb=1024, engine=None):
     """Full-QGT solve with S = sum_r A_r^H A_r FORMED and factorised across ranks (§2
     "S . delta theta = -F"; north_star "full-QGT ... baselines shard the same way").
 
@@ -208,28 +220,55 @@ def dist_full_qgt(ops, comm, rank, world, A, F, lam, nb=1024):
                    update S_qj -= L_qp L_jp^H for its panels q (sr_gram_nh_sub);
       back         x_p = L_pp^{-H} (y_p - sum_{q>p} L_qp^H x_q): each rank's part of the sum
                    (sr_aHv), all-reduced, the owner forms x_p, broadcast.
-    b = -F, so x = dtheta.  Returns dtheta on every rank."""
+    b = -F, so x = dtheta.  Returns dtheta on every rank.
+
+    engine "int8" (default when the ops offer it, as CudaOps does): the partial rows are formed
+    on the int8 digit-slice engine from one split of all the rank's columns (sr_cols_i8_*, when
+    the 21 bytes per sample and column fit), and the trailing updates run on the Cholesky
+    trailing-update kernel gram_i8<MODE_SUB> over one split of the panel column per step
+    (sr_rows_i8_*); "fp64": sr_gram_tn / sr_gram_nh_sub on DMMA."""
     c = torch.complex128
     dev = F.device
     n = F.numel()
+    if engine is None:
+        engine = getattr(ops, "gram_engine", "int8") if hasattr(ops, "cols_prepare") else "fp64"
+    i8 = engine == "int8" and hasattr(ops, "cols_prepare")
+    cs = None
+    chunk_rows = 0          # one rank whose slices do not fit at once: sample chunks, accumulated
+    if i8 and A.shape[0]:
+        need = 21 * A.shape[0] * n
+        free = torch.cuda.mem_get_info(dev)[0] if dev.type == "cuda" else 2 * need + 1
+        if need < 0.45 * free:
+            cs = ops.cols_prepare(A)
+        elif world == 1:   # a third of the free memory per chunk (the rectangles' outputs are resident)
+            chunk_rows = max(64, int(0.3 * free / (21 * n)) // 64 * 64)
     P = (n + nb - 1) // nb
     rows = [(p * nb, min(n, (p + 1) * nb)) for p in range(P)]
     owner = [p % world for p in range(P)]
     mine = [p for p in range(P) if owner[p] == rank]
     R = {p: torch.empty(rows[p][1] - rows[p][0], rows[p][1], dtype=c, device=dev) for p in mine}
     stage = None
-    for q in range(P):                                   # formation, panel by panel
+    if chunk_rows:   # world == 1: every panel is owned; each chunk's rectangles added into R
+        for k0 in range(0, A.shape[0], chunk_rows):
+            cs_k = ops.cols_prepare(A[k0:k0 + chunk_rows])
+            for q in range(P):
+                ops.cols_gram(cs_k, rows[q][0], R[q], accumulate=k0 > 0)
+            del cs_k
+    for q in ([] if chunk_rows else range(P)):           # formation, panel by panel
         lo, hi = rows[q]
         tgt = R[q] if owner[q] == rank else None
         if tgt is None:
             if stage is None or stage.numel() < (hi - lo) * hi:
                 stage = torch.empty((nb * n,), dtype=c, device=dev)
             tgt = stage[:(hi - lo) * hi].view(hi - lo, hi)
-        if A.shape[0]:
+        if cs is not None:
+            ops.cols_gram(cs, lo, tgt)
+        elif A.shape[0]:
             ops.gram_tn(A[:, lo:hi], A[:, :hi], tgt)
         else:
             tgt.zero_()
         comm.reduce(tgt, dst=owner[q])
+    del cs
     one = torch.ones(1, dtype=c, device=dev)
     b = {}
     for p in mine:                                       # right-hand side b = -F
@@ -279,10 +318,14 @@ def dist_full_qgt(ops, comm, rank, world, A, F, lam, nb=1024):
                 qlo, qhi = rows[q]
                 col[qlo - hi:qhi - hi].copy_(packs[g][i, :qhi - qlo])
         del packs, pack
+        rs = ops.rows_prepare(col) if (i8 and later and h <= 8192) else None
         for q in later:                                  # trailing update of this rank's panels
             qlo, qhi = rows[q]
-            ops.gram_nh_sub(R[q][:, lo:hi], col[:qhi - hi], R[q][:, hi:qhi])
-        del col
+            if rs is not None:                           # C -= col[q rows] col[:qhi - hi]^H
+                ops.rows_sub(rs, qlo - hi, R[q][:, hi:qhi])
+            else:
+                ops.gram_nh_sub(R[q][:, lo:hi], col[:qhi - hi], R[q][:, hi:qhi])
+        del col, rs
     x = {}
     for p in reversed(range(P)):                         # back substitution
         lo, hi = rows[p]

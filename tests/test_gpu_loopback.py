@@ -250,6 +250,35 @@ def test_panel_kernels():
         assert np.linalg.norm(Lih @ Lh - np.eye(n)) / np.sqrt(n) < 1e-12
 
 
+def test_int8_rectangles():
+    """sr_cols_i8_prepare / sr_cols_i8_gram (C (+)= A[:, row0:row0+m]^H A[:, 0:n], K-split for
+    more than 8192 samples) and sr_rows_i8_prepare / sr_rows_i8_sub (C -= L[row0:row0+m]
+    L[0:n]^H) against numpy, entrywise to 1e-11 of sqrt(|x_i|^2 |y_j|^2)."""
+    import paper_2510_08430_b200 as sr
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(21)
+    cx = lambda *s: rng.standard_normal(s) + 1j * rng.standard_normal(s)   # noqa: E731
+    for ns, ncols, row0, m, n in ((700, 300, 37, 130, 250), (9000, 200, 0, 200, 200), (5, 70, 69, 1, 70)):
+        A = cx(ns, ncols) * np.exp(rng.uniform(-4, 4, ncols))[None, :]
+        cs = sr.ColSlices(torch.from_numpy(A).to(dev))
+        C = torch.empty(m, n, dtype=torch.complex128, device=dev)
+        cs.gram(row0, C)
+        ref = A[:, row0:row0 + m].conj().T @ A[:, :n]
+        scale = np.outer(np.linalg.norm(A[:, row0:row0 + m], axis=0), np.linalg.norm(A[:, :n], axis=0))
+        assert np.all(np.abs(C.cpu().numpy() - ref) <= 1e-11 * scale)
+        cs.gram(row0, C, accumulate=True)
+        assert np.all(np.abs(C.cpu().numpy() - 2 * ref) <= 2e-11 * scale)
+    for rows, K, row0, m, n in ((500, 64, 100, 129, 300), (1100, 1024, 1000, 100, 1100), (3, 7, 2, 1, 3)):
+        L = cx(rows, K)
+        C0 = cx(m, n)
+        C = torch.from_numpy(C0).to(dev)
+        rs = sr.RowSlices(torch.from_numpy(L).to(dev))
+        rs.sub(row0, C)
+        ref = C0 - L[row0:row0 + m] @ L[:n].conj().T
+        scale = np.outer(np.linalg.norm(L[row0:row0 + m], axis=1), np.linalg.norm(L[:n], axis=1))
+        assert np.all(np.abs(C.cpu().numpy() - ref) <= 1e-11 * scale + 1e-15 * np.abs(C0))
+
+
 @pytest.mark.parametrize("world,nb", [(1, 1024), (3, 200)])
 def test_dist_full_qgt_gpu(world, nb):
     """parallel.dist_full_qgt with the real kernels (sr_gram_tn formation reduced to panel
@@ -277,13 +306,15 @@ def test_dist_full_qgt_gpu(world, nb):
             comm, lock = cl
             ops = parallel.locked(parallel.CudaOps([4, 4], 1, 1, dev), lock)
             lo, hi = bounds[r]
-            x = parallel.dist_full_qgt(ops, comm, r, world, Ad[lo:hi], Fd, lam, nb=nb_)
+            xs = [parallel.dist_full_qgt(ops, comm, r, world, Ad[lo:hi], Fd, lam, nb=nb_, engine=eng)
+                  for eng in ("int8", "fp64")]
             torch.cuda.synchronize()
-            return x
+            return xs
         outs = parallel.run_loopback(world, make, work)
         for o in outs[1:]:
-            assert torch.equal(o, outs[0])
-        return outs[0]
+            assert torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1])
+        assert _rel(outs[0][0], outs[0][1]) < 1e-10      # int8 rectangles vs FP64 DMMA
+        return outs[0][0]
 
     x = solve(torch.from_numpy(A).to(dev), torch.from_numpy(F).to(dev), min(nb, 128))
     assert np.linalg.norm(x.cpu().numpy() - ref) / np.linalg.norm(ref) < 1e-10

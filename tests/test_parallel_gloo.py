@@ -77,6 +77,22 @@ class OracleOps:
     def gram_nh_sub(self, A, B, C):
         C.sub_(A @ B.conj().T)
 
+    # the int8 rectangle interface of dist_full_qgt (the oracle forms the same products)
+    def cols_prepare(self, A):
+        return A
+
+    def cols_gram(self, A, row0, C, accumulate=False):
+        m, n = C.shape
+        prod = A[:, row0:row0 + m].conj().T @ A[:, :n]
+        C.add_(prod) if accumulate else C.copy_(prod)
+
+    def rows_prepare(self, L):
+        return L
+
+    def rows_sub(self, L, row0, C):
+        m, n = C.shape
+        C.sub_(L[row0:row0 + m] @ L[:n].conj().T)
+
     def chol_inv(self, M, lam, L, Linv):
         m = M.numpy()
         m = np.tril(m) + np.tril(m, -1).conj().T + lam * np.eye(m.shape[0])
@@ -249,12 +265,14 @@ def test_dist_full_qgt_o1_conditioned(world, nb):
     def work(r, cl):
         comm, lock = cl
         lo, hi = bounds[r]
-        return parallel.dist_full_qgt(parallel.locked(OracleOps(), lock), comm, r, world,
-                                      torch.from_numpy(A[lo:hi].copy()), torch.from_numpy(F), lam, nb=nb).numpy()
+        return [parallel.dist_full_qgt(parallel.locked(OracleOps(), lock), comm, r, world,
+                                       torch.from_numpy(A[lo:hi].copy()), torch.from_numpy(F), lam, nb=nb,
+                                       engine=eng).numpy() for eng in ("fp64", "int8")]
 
     outs = parallel.run_loopback(world, make, work)
-    for x in outs:
-        assert np.linalg.norm(x - ref) / np.linalg.norm(ref) < 1e-10
+    for xs in outs:
+        for x in xs:
+            assert np.linalg.norm(x - ref) / np.linalg.norm(ref) < 1e-10
 
 
 def test_loopback_ragged_tiny_shards_all_paths():

@@ -18,6 +18,7 @@ from paper_2510_08430_b200 import parallel  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else bench.DEFAULT_WORKLOAD
 nb = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
+eng = sys.argv[3] if len(sys.argv) > 3 else "int8"
 w = bench.workload_for(name, 1)
 spins, params = bench.workloads.make_inputs(w)
 ij, jj = sr.lattice.for_workload(w)
@@ -48,12 +49,12 @@ torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 t0 = time.perf_counter()
 e0.record()
-x = parallel.dist_full_qgt(step.ops, _One(), 0, 1, b.O, b.F, w.lam, nb=nb)
+x = parallel.dist_full_qgt(step.ops, _One(), 0, 1, b.O, b.F, w.lam, nb=nb, engine=eng)
 e1.record()
 torch.cuda.synchronize()
 nrm = lambda v: float(torch.linalg.vector_norm(v).item())  # noqa: E731
 n = w.n_params
-print(json.dumps({"workload": name, "n_p": n, "n_samples": w.n_samples, "panel_rows": nb,
+print(json.dumps({"workload": name, "n_p": n, "n_samples": w.n_samples, "panel_rows": nb, "engine": eng,
                   "ms": e0.elapsed_time(e1), "wall_s": time.perf_counter() - t0,
                   "form_flops": 8.0 * w.n_samples * n * (n + 1) / 2, "chol_flops": 4.0 * n ** 3 / 3,
                   "rel_l2_dense_vs_cg": nrm(x - x_cg) / nrm(x_cg), "rel_l2_block_vs_dense": nrm(d_block - x) / nrm(x),
