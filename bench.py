@@ -517,8 +517,10 @@ def compare_solves(sr, torch, step, w, dev):
              "full_qgt_solve": lambda ws: sr.sr_full_qgt_solve(b.O, b.F, w.lam, out_d["full_qgt_solve"], workspace=ws),
              "full_qgt_cg": full_cg,
              "ntk_solve": lambda ws: sr.sr_ntk_solve(b.O, b.e_tilde, w.lam, out_d["ntk_solve"], workspace=ws)}
-    if b.n_p <= 40000:   # the formed-and-factorised distributed path, as one rank (configs[3]: 72 s, not timed here)
-        calls["full_qgt_dist"] = full_dist
+    # the formed-and-factorised distributed path, as one rank (configs[3]: ~29 s on the int8
+    # engine; timed once, without the warm call, above 40000 parameters)
+    calls["full_qgt_dist"] = full_dist
+    once = {"full_qgt_dist"} if b.n_p > 40000 else set()
     need = {"full_qgt_solve": lib.sr_full_qgt_solve_workspace_bytes(ns, b.n_p) + 16 * b.n_p,
             "ntk_solve": lib.sr_ntk_solve_workspace_bytes(ns, b.n_p) + 16 * b.n_p}
     ms, skipped = {}, {}
@@ -535,7 +537,8 @@ def compare_solves(sr, torch, step, w, dev):
                 continue
             ws = torch.empty(int(need[name]), dtype=torch.uint8, device=dev)
             out_d[name] = torch.empty_like(b.dtheta)
-        fn(ws)
+        if name not in once:
+            fn(ws)
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -547,8 +550,13 @@ def compare_solves(sr, torch, step, w, dev):
         torch.cuda.empty_cache()
     nrm = lambda x: float(torch.linalg.vector_norm(x).item())   # noqa: E731
     out = {"ms": ms, "sizes": {"full_qgt": b.n_p, "ntk": int(ns), "blocks": [int(x) for x in block_sizes(w)]},
-           "note": "eager, one timed call each after a warm call; A, F, e from the step above"}
-    ref = next((k for k in ("full_qgt_solve", "full_qgt_cg", "ntk_solve") if k in ms), None)
+           "note": ("eager, one timed call each after a warm call (full_qgt_dist above 40000 parameters: one "
+                    "call, no warm call); A, F, e from the step above; full_qgt_dist = parallel.dist_full_qgt as "
+                    "one rank: the full QGT formed and factorised by panels")}
+    ref = next((k for k in ("full_qgt_solve", "full_qgt_dist", "full_qgt_cg", "ntk_solve") if k in ms), None)
+    if "full_qgt_dist" in ms and "full_qgt_cg" in ms:
+        out["rel_l2_full_dist_vs_cg"] = (nrm(out_d["full_qgt_dist"] - out_d["full_qgt_cg"])
+                                         / nrm(out_d["full_qgt_cg"]))
     if "full_qgt_solve" in ms and "ntk_solve" in ms:
         out["rel_l2_full_vs_ntk"] = nrm(out_d["full_qgt_solve"] - out_d["ntk_solve"]) / nrm(out_d["full_qgt_solve"])
     if "full_qgt_dist" in ms and "full_qgt_solve" in ms:
