@@ -373,3 +373,19 @@ def test_block_qgt_i8_acc():
     sr.sr_block_qgt_i8_acc(A[:0], offs, S2)
     assert torch.equal(S2, before)
     assert _rel(S2, S1) < 1e-14
+
+
+def test_per_block_schedule_fp64_engine():
+    """The per-block schedule on the FP64 DMMA engine (block Gram into the factor matrix by the
+    TMA-staged DMMA kernel, FP64 trailing updates) equals the batched FP64 schedule."""
+    sr, w, spins, params, ij, jj, dev, theta = _setup(1)
+    from paper_2510_08430_b200 import parallel
+    prev = sr.sr_set_gram_engine(sr.GRAM_FP64)
+    try:
+        d_b = parallel.LocalStep(w.widths, spins, ij, jj, w.lam, dev, gram_engine="fp64").run(theta)[0].clone()
+        d_p = parallel.LocalStep(w.widths, spins, ij, jj, w.lam, dev, gram_engine="fp64",
+                                 schedule="per_block").run(theta)[0].clone()
+        torch.cuda.synchronize()
+    finally:
+        sr.sr_set_gram_engine(prev)
+    assert _rel(d_p, d_b) < 1e-12
