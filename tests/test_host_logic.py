@@ -110,3 +110,15 @@ def test_lncosh_series_constants_and_accuracy():
     assert h["c"] == [float(x) for x in c] and h["t"] == [float(x) for x in t]
     el, et = ls.max_rel_errors(n=800)
     assert el < 5e-16 and et < 5e-16
+
+
+def test_bench_config_chunked_and_full_samples():
+    """bench.config_of for the sample-chunked configs[4] run (all 65536 samples on one GPU):
+    not labelled weak scaling, the resident O is one chunk."""
+    import bench
+    w = workloads.BY_NAME["j1j2_10x10_w160"]
+    c = bench.config_of(w, 1, "int8", False, "chunked", 8192)
+    assert c["n_samples"] == 65536 and c["scaling"].startswith("strong")
+    assert "25.75 GB resident" in c["l2"] and "206 GB over the chunks" in c["l2"]
+    c1 = bench.config_of(bench.workload_for("j1j2_10x10_w160", 1), 1, "int8", False, "per_block")
+    assert c1["scaling"].startswith("weak") and c1["n_samples"] == 8192
